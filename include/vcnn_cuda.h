@@ -1,0 +1,290 @@
+/*
+ * vcnn_cuda.h -- C ABI of libvcnn_cuda.so, the B200 (sm_100a) implementation
+ * of the VCNN Imp-6 training path (arXiv 1501.07338).
+ *
+ * The reference (/root/reference/proj) has no FFI: its operator API is the
+ * C++ header-template surface of proj/include/vcnn/(name).hpp.  Every entry point
+ * below replaces one function of that surface; the comment cites the
+ * reference file:line it stands in for (paths relative to
+ * /root/reference/proj/include/vcnn).  Plain pointers and sizes only; no
+ * torch or C++ types.  Conventions:
+ *   - all tensors fp32 NCHW (linear index ((b*C+c)*H+y)*W+x, tensor.hpp:80-82),
+ *     matrices row-major (tensor.hpp:106-127);
+ *   - op-level functions take CALLER-OWNED DEVICE pointers and a
+ *     cudaStream_t passed as void* (NULL = legacy default stream), are
+ *     stream-ordered and do not synchronise unless documented;
+ *   - every function returns a vcnn_status; on error, vcnn_last_error()
+ *     returns a message (thread-local).  Geometry / shape / bounds errors are
+ *     raised on the host before any launch, mirroring the exceptions of the
+ *     reference constructors (vectorize.hpp:22-26, :144-148; layers.hpp:77-89).
+ *   - precision: VCNN_PREC_TF32 (tcgen05 kind::tf32, fp32 accumulate),
+ *     VCNN_PREC_3XTF32 (split hi/lo, three tcgen05 MMAs, fp32-faithful),
+ *     VCNN_PREC_FP32 (SIMT fp32 FMA; the on-device exactness reference).
+ * There is no CPU fallback: without a usable sm_100 device every compute
+ * entry point returns VCNN_ECUDA.
+ */
+#ifndef VCNN_CUDA_H
+#define VCNN_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VCNN_ABI_VERSION 1
+
+/* status codes; the C++ host layer rethrows them as the reference exception
+ * types (common.hpp:26-46) */
+typedef enum {
+  VCNN_OK = 0,
+  VCNN_ESHAPE = 1,     /* ShapeError */
+  VCNN_EGEOMETRY = 2,  /* GeometryError */
+  VCNN_EBOUNDS = 3,    /* BoundsError */
+  VCNN_ECUDA = 4,      /* CUDA runtime / no device */
+  VCNN_ENCCL = 5,      /* collective failure */
+  VCNN_ECONFIG = 6,    /* ConfigError */
+  VCNN_ETRAINING = 7   /* TrainingError */
+} vcnn_status;
+
+/* Activation (layers.hpp:13) */
+enum { VCNN_ACT_IDENTITY = 0, VCNN_ACT_RELU = 1, VCNN_ACT_SIGMOID = 2, VCNN_ACT_TANH = 3 };
+/* PoolMode (vectorize.hpp:127) */
+enum { VCNN_POOL_MAX = 0, VCNN_POOL_AVG = 1 };
+/* PoolBackwardMode (vectorize.hpp:217) */
+enum { VCNN_POOLBWD_EXACT = 0, VCNN_POOLBWD_PAPER_NN = 1 };
+/* LossKind (layers.hpp:375) */
+enum { VCNN_LOSS_SOFTMAX_CE = 0, VCNN_LOSS_MSE = 1 };
+/* LayerSpec alternatives (network.hpp:12-32) */
+enum { VCNN_LAYER_CONV = 0, VCNN_LAYER_POOL = 1, VCNN_LAYER_FULL = 2 };
+/* arithmetic of the GEMM-shaped kernels */
+enum { VCNN_PREC_TF32 = 0, VCNN_PREC_3XTF32 = 1, VCNN_PREC_FP32 = 2 };
+/* Reducer (tensor.hpp:185) */
+enum { VCNN_REDUCE_SUM = 0, VCNN_REDUCE_MAX = 1, VCNN_REDUCE_MEAN = 2 };
+
+/* ConvGeometry (vectorize.hpp:13-42), valid convolution, no padding */
+typedef struct {
+  int in_h, in_w, channels, batch;
+  int kh, kw, stride;
+  int out_h, out_w;
+} vcnn_conv_geometry;
+
+/* PoolGeometry (vectorize.hpp:134-162), overlap allowed */
+typedef struct {
+  int in_h, in_w, channels, batch;
+  int ph, pw, stride, mode;
+  int out_h, out_w;
+} vcnn_pool_geometry;
+
+/* one LayerSpec (network.hpp:12-32): conv uses units=maps,kh,kw,stride,act;
+ * pool uses kh,kw (=ph,pw),stride,pool_mode,pool_bias,act; full uses units,act */
+typedef struct {
+  int kind;
+  int units;
+  int kh, kw;
+  int stride;
+  int pool_mode;
+  int pool_bias;
+  int act;
+} vcnn_layer_spec;
+
+/* NetworkSpec (network.hpp:37-73) */
+typedef struct {
+  int in_h, in_w, in_c;
+  int nlayers;
+  const vcnn_layer_spec* layers;
+  int loss;
+  uint64_t seed;
+} vcnn_net_spec;
+
+/* ------------------------------------------------------------------------ */
+/* library                                                                   */
+/* ------------------------------------------------------------------------ */
+int vcnn_abi_version(void);
+const char* vcnn_last_error(void);
+/* SM count / compute capability of the current device; VCNN_ECUDA if none */
+int vcnn_device_info(int* sm_count, int* cc_major, int* cc_minor);
+/* kernels launched by this library since load (gpu_launches evidence) */
+int64_t vcnn_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* geometry (host only, no device needed)                                    */
+/* ------------------------------------------------------------------------ */
+/* ConvGeometry(Shape, kh, kw, stride) (vectorize.hpp:19-29) */
+int vcnn_conv_geometry_init(vcnn_conv_geometry* g, int in_h, int in_w, int channels, int batch,
+                            int kh, int kw, int stride);
+/* PoolGeometry(Shape, ph, pw, stride, mode) (vectorize.hpp:141-151) */
+int vcnn_pool_geometry_init(vcnn_pool_geometry* g, int in_h, int in_w, int channels, int batch,
+                            int ph, int pw, int stride, int mode);
+/* NetworkSpec::chain (network.hpp:45-67): per-layer (h,w,c), 3 ints each */
+int vcnn_net_spec_chain(const vcnn_net_spec* spec, int* shapes);
+
+/* ------------------------------------------------------------------------ */
+/* L1 tensor primitives (tensor.hpp)                                         */
+/* ------------------------------------------------------------------------ */
+/* matmul: C[m][n] = A[m][k] * B[k][n] (tensor.hpp:131-150) */
+int vcnn_matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
+                int precision, void* stream);
+/* matmul_transB: C[m][n] = A[m][k] * B[n][k]^T (tensor.hpp:154-174) */
+int vcnn_matmul_transB(int64_t m, int64_t k, int64_t n, const float* a, const float* b,
+                       float* c, int precision, void* stream);
+/* accumulate_by_index (tensor.hpp:228-266): out[t] = reducer over
+ * {values[s] : (s,t) in map}, pairs consumed in map order (deterministic);
+ * empty buckets 0. */
+int vcnn_accumulate_by_index(const float* values, int64_t source_len, const int64_t* source,
+                             const int64_t* target, int64_t pairs, int64_t target_len,
+                             int reducer, float* out, void* stream);
+/* accumulate_max_arg (tensor.hpp:271-289): ties -> lowest source, empty -> (0,-1) */
+int vcnn_accumulate_max_arg(const float* values, int64_t source_len, const int64_t* source,
+                            const int64_t* target, int64_t pairs, int64_t target_len,
+                            float* out, int64_t* arg, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* L2 vectorize ops (vectorize.hpp)                                          */
+/* ------------------------------------------------------------------------ */
+/* im2col (vectorize.hpp:54-79): patch[(c*kh+ky)*kw+kx][b*OH*OW+oy*OW+ox] */
+int vcnn_im2col(const vcnn_conv_geometry* g, const float* x, float* patch, void* stream);
+/* col2im (vectorize.hpp:111-120): exact adjoint of im2col, gather form,
+ * each input cell sums its patch cells in (ky,kx) ascending order */
+int vcnn_col2im(const vcnn_conv_geometry* g, const float* dpatch, float* dx, void* stream);
+/* build_col2im_map (vectorize.hpp:84-106): pairs in (c,ky,kx,b,oy,ox) order;
+ * source and target each hold patch_len*cols int64 entries */
+int vcnn_col2im_map(const vcnn_conv_geometry* g, int64_t* source, int64_t* target, void* stream);
+/* build_pool_map (vectorize.hpp:167-191): pairs in (b,c,oy,ox,py,px) order */
+int vcnn_pool_map(const vcnn_pool_geometry* g, int64_t* source, int64_t* target, void* stream);
+/* pool_forward (vectorize.hpp:197-215): max (strict >, first element seeds,
+ * ties -> lowest index; arg = global input index) or avg (sum / window);
+ * arg may be NULL; for avg pools it is filled with -1 when given */
+int vcnn_pool_forward(const vcnn_pool_geometry* g, const float* x, float* y, int64_t* arg,
+                      void* stream);
+/* pool_backward (vectorize.hpp:224-249), gather form (deterministic under
+ * overlap): exact max -> argmax routing, exact avg -> dy/window, paper_nn ->
+ * unscaled nearest-neighbour upsampling */
+int vcnn_pool_backward(const vcnn_pool_geometry* g, int bwd_mode, const float* dy,
+                       const int64_t* arg, float* dx, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* L3 layers (layers.hpp)                                                    */
+/* ------------------------------------------------------------------------ */
+/* apply_activation (layers.hpp:50-54): y = act(x); x may equal y */
+int vcnn_activation_forward(int64_t n, int act, const float* x, float* y, void* stream);
+/* apply_activation_grad (layers.hpp:57-61): grad *= act'(y) (from output) */
+int vcnn_activation_backward(int64_t n, int act, const float* y, float* grad, void* stream);
+/* conv_forward (layers.hpp:139-149): y = act(W*col(x) + b), NCHW out
+ * [batch][maps][out_h][out_w]; implicit GEMM, no patch matrix */
+int vcnn_conv_forward(const vcnn_conv_geometry* g, int maps, const float* x, const float* w,
+                      const float* bias, int act, int precision, float* y, void* stream);
+/* conv_backward (layers.hpp:183-195): dy is the gradient of the
+ * post-activation output; dw [maps][C*kh*kw], db [maps], dx (nullable)
+ * [batch][C][H][W]. Implicit wgrad (deterministic split-K) and dgrad. */
+int vcnn_conv_backward(const vcnn_conv_geometry* g, int maps, const float* x, const float* w,
+                       const float* y, const float* dy, int act, int precision, float* dw,
+                       float* db, float* dx, void* stream);
+/* full_forward (layers.hpp:230-247): y[b][o] = act(sum_i x[b][i] W[o][i] + b[o]) */
+int vcnn_full_forward(int batch, int in_units, int out_units, const float* x, const float* w,
+                      const float* bias, int act, int precision, float* y, void* stream);
+/* full_backward (layers.hpp:269-278) */
+int vcnn_full_backward(int batch, int in_units, int out_units, const float* x, const float* w,
+                       const float* y, const float* dy, int act, int precision, float* dw,
+                       float* db, float* dx, void* stream);
+/* pool_layer_forward (layers.hpp:305-321): pool + optional per-channel bias
+ * (NULL = none) + activation; arg may be NULL */
+int vcnn_pool_layer_forward(const vcnn_pool_geometry* g, const float* x, const float* bias,
+                            int act, float* y, int64_t* arg, void* stream);
+/* pool_layer_backward (layers.hpp:356-363): dbias may be NULL */
+int vcnn_pool_layer_backward(const vcnn_pool_geometry* g, int bwd_mode, const float* y, int act,
+                             const float* dy, const int64_t* arg, float* dx, float* dbias,
+                             void* stream);
+/* loss_forward (layers.hpp:402-434); *loss is a DEVICE scalar.  Class
+ * indices are checked on the device; an out-of-range class makes this call
+ * synchronise and return VCNN_EBOUNDS (layers.hpp:413-415). */
+int vcnn_loss_forward(int kind, int batch, int units, const float* pred, const int* cls,
+                      const float* values, float* loss, void* stream);
+/* loss_backward (layers.hpp:436-468) */
+int vcnn_loss_backward(int kind, int batch, int units, const float* pred, const int* cls,
+                       const float* values, float* grad, void* stream);
+/* fused loss_forward + loss_backward in one kernel */
+int vcnn_loss_fused(int kind, int batch, int units, const float* pred, const int* cls,
+                    const float* values, float* loss, float* grad, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* L4 update (network.hpp)                                                   */
+/* ------------------------------------------------------------------------ */
+/* sgd_step (network.hpp:242-273) over one flat buffer:
+ * v = mom*v + grad_scale*g; w -= lr*v  (grad_scale = 1 is the reference) */
+int vcnn_sgd_step(int64_t n, float* w, float* v, const float* g, float lr, float mom,
+                  float grad_scale, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* L4-L6 network engine: build_network + Executor<float>(imp6) + sgd_step     */
+/* with device-resident parameters, trace and CUDA-graph replay              */
+/* ------------------------------------------------------------------------ */
+typedef struct vcnn_net vcnn_net;
+
+/* build_network (network.hpp:102-130) + Executor<float>(Variant::imp6)
+ * (variants.hpp:336): parameters initialised on the host with the
+ * reference's Rng(spec.seed) Glorot stream (layers.hpp:473-501), uploaded
+ * once; buffers sized for max_batch. */
+int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcnn_net** out);
+int vcnn_net_destroy(vcnn_net* net);
+int64_t vcnn_net_num_params(const vcnn_net* net);
+/* flat parameter layout: per layer, weights then bias (NetGrads order) */
+int vcnn_net_param_layout(const vcnn_net* net, int64_t* w_off, int64_t* w_len, int64_t* b_off,
+                          int64_t* b_len);
+/* per-layer output sizes for one sample */
+int vcnn_net_layer_out_size(const vcnn_net* net, int layer, int64_t* per_sample);
+int vcnn_net_set_stream(vcnn_net* net, void* stream);
+/* Executor::set_pool_backward_mode (variants.hpp:342) */
+int vcnn_net_set_pool_backward_mode(vcnn_net* net, int mode);
+int vcnn_net_set_precision(vcnn_net* net, int precision);
+/* host <-> device parameter / gradient / velocity transfers (synchronous) */
+int vcnn_net_get_params(vcnn_net* net, float* host);
+int vcnn_net_set_params(vcnn_net* net, const float* host);
+int vcnn_net_get_grads(vcnn_net* net, float* host);
+int vcnn_net_get_velocity(vcnn_net* net, float* host);
+int vcnn_net_set_velocity(vcnn_net* net, const float* host);
+/* device pointers of the flat buffers (for collectives: all-reduce grads) */
+int vcnn_net_device_buffers(vcnn_net* net, float** params, float** grads, float** velocity);
+/* device pointers of the input slots (x [max_batch][C][H][W], cls, values) */
+int vcnn_net_input_buffers(vcnn_net* net, float** x, int** cls, float** values);
+/* stage a batch already in device memory (copied, stream-ordered) */
+int vcnn_net_set_batch_device(vcnn_net* net, int batch, const float* x, const int* cls,
+                              const float* values);
+/* Executor::run_batch with targets (variants.hpp:353-376): forward, fused
+ * loss, backward; grads land in the device grads buffer, loss in a device
+ * scalar.  Stream-ordered, no host sync. */
+int vcnn_net_forward_backward(vcnn_net* net, int batch);
+/* Executor::forward (variants.hpp:346-348) */
+int vcnn_net_forward(vcnn_net* net, int batch);
+/* sgd_step over all parameters; grad_scale multiplies the gradient (1/world
+ * for a summed data-parallel all-reduce) */
+int vcnn_net_sgd_step(vcnn_net* net, float lr, float mom, float grad_scale);
+/* forward_backward + sgd_step; replayed from a CUDA graph when enabled */
+int vcnn_net_train_step(vcnn_net* net, int batch, float lr, float mom);
+/* end-to-end: HOST batch in (validated: class bounds -> VCNN_EBOUNDS),
+ * H2D copy, train step, D2H loss; synchronous */
+int vcnn_net_train_step_host(vcnn_net* net, int batch, const float* x, const int* cls,
+                             const float* values, float lr, float mom, float* loss_out);
+/* end-to-end inference: HOST batch in, HOST output out; synchronous */
+int vcnn_net_forward_host(vcnn_net* net, int batch, const float* x, float* out);
+/* CUDA-graph capture of train_step (per batch size); 0 disables */
+int vcnn_net_enable_graph(vcnn_net* net, int enable);
+/* results (synchronous reads) */
+int vcnn_net_get_loss(vcnn_net* net, float* loss);
+int vcnn_net_get_output(vcnn_net* net, float* host);
+int vcnn_net_get_layer_output(vcnn_net* net, int layer, float* host);
+/* pool argmax of a max-pool layer as int64 global input indices */
+int vcnn_net_get_pool_arg(vcnn_net* net, int layer, int64_t* host);
+/* kernels per train step (fwd+bwd+sgd) at the current settings */
+int vcnn_net_kernels_per_step(vcnn_net* net, int* count);
+/* BreakdownTimer (variants.hpp:249-274) with CUDA events: enable, then read
+ * the 8 component seconds {conv,pool,full,other}x{f,b} accumulated since the
+ * last reset (synchronises) */
+int vcnn_net_enable_breakdown(vcnn_net* net, int enable);
+int vcnn_net_read_breakdown(vcnn_net* net, double* seconds8);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VCNN_CUDA_H */

@@ -1,0 +1,740 @@
+// engine.cu -- the device-resident network engine behind the net-level C ABI:
+// build_network + Executor<float>(imp6).run_batch + sgd_step
+// (network.hpp:102-130, variants.hpp:353-376 / 484-668, network.hpp:242-273).
+//
+// Layout in HBM (one net):
+//   params | grads | velocity : three flat fp32 buffers in NetGrads order
+//                               (per layer: weights row-major, then bias), so
+//                               SGD is ONE kernel and a data-parallel
+//                               all-reduce is ONE collective over `grads`;
+//   per layer: out  [B][C][H][W] post-activation (the forward trace; also the
+//                                 activation-derivative source in backward),
+//              gpre [B][C][H][W] gradient w.r.t. the PRE-activation,
+//              arg  [B][C][OH][OW] int32 global argmax (max pools);
+//   input slots x / cls / values sized for max_batch.
+// Backward writes gpre of layer i-1 directly from layer i's dgrad / pool
+// backward / FC dgrad epilogue (act' fused), so there are no standalone
+// activation passes.  A whole train step can be captured once into a CUDA
+// graph and replayed.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace vcnn_b200;
+
+namespace {
+
+struct LayerRt {
+  vcnn_layer_spec spec;
+  int in_h, in_w, in_c;
+  int out_h, out_w, out_c;
+  int64_t w_off = 0, w_len = 0, b_off = 0, b_len = 0;
+  int64_t in_per = 0, out_per = 0;
+  float* out = nullptr;
+  float* gpre = nullptr;
+  int32_t* arg = nullptr;
+};
+
+// host Rng identical to the reference (common.hpp:51-66): mt19937_64 with
+// uniform = (u64 >> 11) * 2^-53
+struct HostRng {
+  uint64_t mt[312];
+  int idx;
+  explicit HostRng(uint64_t seed) {
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i)
+      mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+    idx = 312;
+  }
+  uint64_t next() {
+    if (idx >= 312) {
+      for (int i = 0; i < 312; ++i) {
+        uint64_t x = (mt[i] & 0xFFFFFFFF80000000ULL) | (mt[(i + 1) % 312] & 0x7FFFFFFFULL);
+        uint64_t y = x >> 1;
+        if (x & 1ULL) y ^= 0xB5026F5AA96619E9ULL;
+        mt[i] = mt[(i + 156) % 312] ^ y;
+      }
+      idx = 0;
+    }
+    uint64_t x = mt[idx++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= (x >> 43);
+    return x;
+  }
+  double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+  // fused like the reference build (gnu++20 contracts lo + (hi-lo)*u to an FMA)
+  double uniform(double lo, double hi) { return std::fma(hi - lo, uniform(), lo); }
+};
+
+enum Comp { CONV_F = 0, CONV_B, POOL_F, POOL_B, FULL_F, FULL_B, OTHER_F, OTHER_B };
+
+}  // namespace
+
+struct vcnn_net {
+  std::vector<vcnn_layer_spec> specs;
+  vcnn_net_spec spec{};
+  std::vector<LayerRt> L;
+  int max_batch = 0;
+  int precision = VCNN_PREC_TF32;
+  int pool_bwd_mode = VCNN_POOLBWD_EXACT;
+  int64_t nparams = 0;
+  float* params = nullptr;
+  float* grads = nullptr;
+  float* vel = nullptr;
+  float* x = nullptr;
+  int* cls = nullptr;
+  float* values = nullptr;
+  int64_t in_per = 0, out_units = 0;
+  float* loss = nullptr;
+  int* err = nullptr;
+  Workspace ws;
+  cudaStream_t stream = nullptr;
+  // graph replay
+  bool use_graph = false;
+  cudaGraphExec_t gexec = nullptr;
+  int g_batch = -1;
+  float g_lr = 0, g_mom = 0;
+  int kernels_per_step = 0;
+  // breakdown timer
+  bool breakdown = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+  double seconds[8] = {0};
+};
+
+namespace {
+
+#define TRY(expr)      \
+  do {                 \
+    int _s = (expr);   \
+    if (_s) return _s; \
+  } while (0)
+
+ConvDesc conv_of(const LayerRt& l, int B) {
+  ConvDesc d;
+  d.B = B;
+  d.C = l.in_c;
+  d.H = l.in_h;
+  d.W = l.in_w;
+  d.K = l.spec.units;
+  d.kh = l.spec.kh;
+  d.kw = l.spec.kw;
+  d.s = l.spec.stride;
+  d.OH = l.out_h;
+  d.OW = l.out_w;
+  return d;
+}
+
+PoolDesc pool_of(const LayerRt& l, int B) {
+  PoolDesc d;
+  d.B = B;
+  d.C = l.in_c;
+  d.H = l.in_h;
+  d.W = l.in_w;
+  d.ph = l.spec.kh;
+  d.pw = l.spec.kw;
+  d.s = l.spec.stride;
+  d.mode = l.spec.pool_mode;
+  d.OH = l.out_h;
+  d.OW = l.out_w;
+  return d;
+}
+
+// -------- breakdown marks (eager mode only) --------
+cudaEvent_t next_event(vcnn_net* n) {
+  if (n->event_next == n->event_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    n->event_pool.push_back(e);
+  }
+  return n->event_pool[n->event_next++];
+}
+
+struct Mark {
+  vcnn_net* n;
+  int comp;
+  cudaEvent_t a = nullptr;
+  Mark(vcnn_net* net, int c) : n(net), comp(c) {
+    if (n->breakdown) {
+      a = next_event(n);
+      cudaEventRecord(a, n->stream);
+    }
+  }
+  ~Mark() {
+    if (n->breakdown) {
+      cudaEvent_t b = next_event(n);
+      cudaEventRecord(b, n->stream);
+      n->marks.push_back({comp, {a, b}});
+    }
+  }
+};
+
+int run_forward(vcnn_net* n, int B) {
+  const cudaStream_t st = n->stream;
+  for (size_t i = 0; i < n->L.size(); ++i) {
+    LayerRt& l = n->L[i];
+    const float* in = i == 0 ? n->x : n->L[i - 1].out;
+    const float* W = n->params + l.w_off;
+    const float* b = n->params + l.b_off;
+    if (l.spec.kind == VCNN_LAYER_CONV) {
+      Mark m(n, CONV_F);
+      TRY(launch_conv_fwd(conv_of(l, B), in, W, b, l.spec.act, l.out, n->precision, n->ws, st));
+    } else if (l.spec.kind == VCNN_LAYER_POOL) {
+      Mark m(n, POOL_F);
+      PoolDesc d = pool_of(l, B);
+      TRY(launch_pool_fwd<int32_t>(d, in, l.b_len ? b : nullptr, l.spec.act, l.out,
+                                   d.mode == VCNN_POOL_MAX ? l.arg : nullptr, st));
+    } else {
+      Mark m(n, FULL_F);
+      TRY(launch_full_fwd(B, (int)l.in_per, l.spec.units, in, W, b, l.spec.act, l.out,
+                          n->precision, n->ws, st));
+    }
+  }
+  return VCNN_OK;
+}
+
+int run_backward(vcnn_net* n, int B) {
+  const cudaStream_t st = n->stream;
+  LayerRt& last = n->L.back();
+  {
+    Mark m(n, OTHER_F);
+    TRY(launch_loss(n->spec.loss, B, (int)n->out_units, last.out, n->cls, n->values, n->loss,
+                    last.gpre, last.spec.act, n->err, st));
+  }
+  for (int i = (int)n->L.size() - 1; i >= 0; --i) {
+    LayerRt& l = n->L[i];
+    const float* in = i == 0 ? n->x : n->L[i - 1].out;
+    const float* yprev = i > 0 ? n->L[i - 1].out : nullptr;
+    const int act_prev = i > 0 ? n->L[i - 1].spec.act : VCNN_ACT_IDENTITY;
+    float* gprev = i > 0 ? n->L[i - 1].gpre : nullptr;
+    const float* W = n->params + l.w_off;
+    float* gW = n->grads + l.w_off;
+    float* gB = n->grads + l.b_off;
+    if (l.spec.kind == VCNN_LAYER_CONV) {
+      Mark m(n, CONV_B);
+      ConvDesc d = conv_of(l, B);
+      TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, n->ws, st));
+      if (gprev)
+        TRY(launch_conv_dgrad(d, l.gpre, W, gprev, yprev, act_prev, n->precision, n->ws, st));
+    } else if (l.spec.kind == VCNN_LAYER_POOL) {
+      Mark m(n, POOL_B);
+      PoolDesc d = pool_of(l, B);
+      if (l.b_len) TRY(launch_pool_bias_grad(d, l.gpre, gB, st));
+      if (gprev)
+        TRY(launch_pool_bwd<int32_t>(d, n->pool_bwd_mode, l.gpre, l.arg, gprev, yprev, act_prev,
+                                     st));
+    } else {
+      Mark m(n, FULL_B);
+      TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
+                            n->ws, st));
+      if (gprev)
+        TRY(launch_full_dgrad(B, (int)l.in_per, l.spec.units, l.gpre, W, gprev, yprev, act_prev,
+                              n->precision, n->ws, st));
+    }
+  }
+  return VCNN_OK;
+}
+
+int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
+  Mark m(n, OTHER_B);
+  return launch_sgd(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, n->stream);
+}
+
+int check_batch(vcnn_net* n, int batch) {
+  if (batch < 1 || batch > n->max_batch)
+    return fail(VCNN_ESHAPE, "batch " + std::to_string(batch) + " outside [1," +
+                                 std::to_string(n->max_batch) + "]");
+  return VCNN_OK;
+}
+
+int check_cfg(float lr, float mom) {
+  if (!(lr > 0)) return fail(VCNN_ECONFIG, "learning rate must be positive");
+  if (mom < 0 || mom >= 1) return fail(VCNN_ECONFIG, "momentum must be in [0,1)");
+  return VCNN_OK;
+}
+
+void drop_graph(vcnn_net* n) {
+  if (n->gexec) cudaGraphExecDestroy(n->gexec);
+  n->gexec = nullptr;
+  n->g_batch = -1;
+}
+
+int eager_step(vcnn_net* n, int batch, float lr, float mom) {
+  const int64_t before = g_launches.load();
+  TRY(run_forward(n, batch));
+  TRY(run_backward(n, batch));
+  TRY(run_sgd(n, lr, mom, 1.0f));
+  n->kernels_per_step = (int)(g_launches.load() - before);
+  return VCNN_OK;
+}
+
+int train_step(vcnn_net* n, int batch, float lr, float mom) {
+  TRY(check_batch(n, batch));
+  TRY(check_cfg(lr, mom));
+  if (!n->use_graph || n->breakdown) return eager_step(n, batch, lr, mom);
+  if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom) {
+    drop_graph(n);
+    cudaGraph_t g = nullptr;
+    VCNN_CUDA_TRY(cudaStreamBeginCapture(n->stream, cudaStreamCaptureModeRelaxed));
+    int s = eager_step(n, batch, lr, mom);
+    cudaError_t e = cudaStreamEndCapture(n->stream, &g);
+    if (s) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&n->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    n->g_batch = batch;
+    n->g_lr = lr;
+    n->g_mom = mom;
+  }
+  VCNN_CUDA_TRY(cudaGraphLaunch(n->gexec, n->stream));
+  g_launches.fetch_add(n->kernels_per_step);
+  return VCNN_OK;
+}
+
+int copy_out(vcnn_net* n, void* host, const void* dev, size_t bytes) {
+  VCNN_CUDA_TRY(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, n->stream));
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  return VCNN_OK;
+}
+
+int copy_in(vcnn_net* n, void* dev, const void* host, size_t bytes) {
+  VCNN_CUDA_TRY(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, n->stream));
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  return VCNN_OK;
+}
+
+int check_errflag(vcnn_net* n) {
+  int h = 0;
+  TRY(copy_out(n, &h, n->err, sizeof(int)));
+  if (h) {
+    cudaMemsetAsync(n->err, 0, sizeof(int), n->stream);
+    return fail(VCNN_EBOUNDS, "loss: class index out of range [0," +
+                                  std::to_string(n->out_units) + ")");
+  }
+  return VCNN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// NetworkSpec::chain (network.hpp:45-67)
+int vcnn_net_spec_chain(const vcnn_net_spec* spec, int* shapes) {
+  if (!spec) return fail(VCNN_ESHAPE, "null spec");
+  int h = spec->in_h, w = spec->in_w, c = spec->in_c;
+  if (h < 1 || w < 1 || c < 1) return fail(VCNN_ESHAPE, "shape extent must be >= 1");
+  if (spec->loss != VCNN_LOSS_SOFTMAX_CE && spec->loss != VCNN_LOSS_MSE)
+    return fail(VCNN_ECONFIG, "unknown loss kind");
+  for (int i = 0; i < spec->nlayers; ++i) {
+    const vcnn_layer_spec& l = spec->layers[i];
+    const std::string pre = "layer " + std::to_string(i) + ": ";
+    if (l.act < VCNN_ACT_IDENTITY || l.act > VCNN_ACT_TANH)
+      return fail(VCNN_ECONFIG, pre + "unknown activation");
+    if (l.kind == VCNN_LAYER_CONV) {
+      vcnn_conv_geometry g;
+      if (vcnn_conv_geometry_init(&g, h, w, c, 1, l.kh, l.kw, l.stride))
+        return fail(VCNN_ESHAPE, pre + last_error());
+      if (l.units < 1) return fail(VCNN_ESHAPE, pre + "shape extent must be >= 1");
+      h = g.out_h;
+      w = g.out_w;
+      c = l.units;
+    } else if (l.kind == VCNN_LAYER_POOL) {
+      vcnn_pool_geometry g;
+      if (vcnn_pool_geometry_init(&g, h, w, c, 1, l.kh, l.kw, l.stride, l.pool_mode))
+        return fail(VCNN_ESHAPE, pre + last_error());
+      h = g.out_h;
+      w = g.out_w;
+    } else if (l.kind == VCNN_LAYER_FULL) {
+      if (l.units < 1) return fail(VCNN_ESHAPE, pre + "full layer needs units >= 1");
+      h = 1;
+      w = 1;
+      c = l.units;
+    } else {
+      return fail(VCNN_ECONFIG, pre + "unknown layer kind");
+    }
+    if (shapes) {
+      shapes[3 * i] = h;
+      shapes[3 * i + 1] = w;
+      shapes[3 * i + 2] = c;
+    }
+  }
+  return VCNN_OK;
+}
+
+int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcnn_net** out) {
+  if (!out) return fail(VCNN_ESHAPE, "null out");
+  *out = nullptr;
+  if (!spec || spec->nlayers < 1) return fail(VCNN_ESHAPE, "network needs at least one layer");
+  if (max_batch < 1) return fail(VCNN_ESHAPE, "max_batch must be >= 1");
+  if (precision < VCNN_PREC_TF32 || precision > VCNN_PREC_FP32)
+    return fail(VCNN_ECONFIG, "unknown precision");
+  std::vector<int> shapes(3 * spec->nlayers);
+  TRY(vcnn_net_spec_chain(spec, shapes.data()));
+  TRY(require_device());
+
+  vcnn_net* n = new vcnn_net();
+  n->specs.assign(spec->layers, spec->layers + spec->nlayers);
+  n->spec = *spec;
+  n->spec.layers = n->specs.data();
+  n->max_batch = max_batch;
+  n->precision = precision;
+  n->in_per = (int64_t)spec->in_h * spec->in_w * spec->in_c;
+
+  // parameter layout + host init (build_network, network.hpp:102-130)
+  int h = spec->in_h, w = spec->in_w, c = spec->in_c;
+  int64_t off = 0;
+  for (int i = 0; i < spec->nlayers; ++i) {
+    LayerRt l;
+    l.spec = spec->layers[i];
+    l.in_h = h;
+    l.in_w = w;
+    l.in_c = c;
+    l.out_h = shapes[3 * i];
+    l.out_w = shapes[3 * i + 1];
+    l.out_c = shapes[3 * i + 2];
+    l.in_per = (int64_t)h * w * c;
+    l.out_per = (int64_t)l.out_h * l.out_w * l.out_c;
+    if (l.spec.kind == VCNN_LAYER_CONV) {
+      l.w_len = (int64_t)l.spec.units * l.spec.kh * l.spec.kw * c;
+      l.b_len = l.spec.units;
+    } else if (l.spec.kind == VCNN_LAYER_POOL) {
+      l.b_len = l.spec.pool_bias ? c : 0;
+    } else {
+      l.w_len = (int64_t)l.spec.units * l.in_per;
+      l.b_len = l.spec.units;
+    }
+    l.w_off = off;
+    off += l.w_len;
+    l.b_off = off;
+    off += l.b_len;
+    n->L.push_back(l);
+    h = l.out_h;
+    w = l.out_w;
+    c = l.out_c;
+  }
+  n->nparams = off;
+  n->out_units = n->L.back().out_per;
+
+  std::vector<float> hp((size_t)(n->nparams > 0 ? n->nparams : 1), 0.f);
+  {
+    HostRng rng(spec->seed);  // one stream, layer order (layers.hpp:473-501)
+    for (const LayerRt& l : n->L) {
+      if (l.spec.kind == VCNN_LAYER_POOL) continue;
+      double fan_in, fan_out;
+      if (l.spec.kind == VCNN_LAYER_CONV) {
+        fan_in = (double)l.spec.kh * l.spec.kw * l.in_c;
+        fan_out = (double)l.spec.kh * l.spec.kw * l.spec.units;
+      } else {
+        fan_in = (double)l.in_per;
+        fan_out = (double)l.spec.units;
+      }
+      const double a = std::sqrt(6.0 / (fan_in + fan_out));
+      for (int64_t k = 0; k < l.w_len; ++k) hp[l.w_off + k] = (float)rng.uniform(-a, a);
+    }
+  }
+
+  auto dalloc = [&](void** p, size_t bytes) -> int {
+    VCNN_CUDA_TRY(cudaMalloc(p, bytes < 16 ? 16 : bytes));
+    return VCNN_OK;
+  };
+  int s = VCNN_OK;
+  const size_t pbytes = sizeof(float) * (size_t)(n->nparams > 0 ? n->nparams : 1);
+  s = s ? s : dalloc((void**)&n->params, pbytes);
+  s = s ? s : dalloc((void**)&n->grads, pbytes);
+  s = s ? s : dalloc((void**)&n->vel, pbytes);
+  s = s ? s : dalloc((void**)&n->x, sizeof(float) * n->in_per * max_batch);
+  s = s ? s : dalloc((void**)&n->cls, sizeof(int) * max_batch);
+  s = s ? s : dalloc((void**)&n->values, sizeof(float) * n->out_units * max_batch);
+  s = s ? s : dalloc((void**)&n->loss, sizeof(float) * 4);
+  s = s ? s : dalloc((void**)&n->err, sizeof(int) * 4);
+  size_t wsb = 0;
+  for (LayerRt& l : n->L) {
+    const size_t ob = sizeof(float) * (size_t)(l.out_per * max_batch);
+    s = s ? s : dalloc((void**)&l.out, ob);
+    s = s ? s : dalloc((void**)&l.gpre, ob);
+    if (l.spec.kind == VCNN_LAYER_POOL && l.spec.pool_mode == VCNN_POOL_MAX)
+      s = s ? s : dalloc((void**)&l.arg, sizeof(int32_t) * (size_t)(l.out_per * max_batch));
+    if (l.spec.kind == VCNN_LAYER_CONV) {
+      for (int prec = VCNN_PREC_TF32; prec <= VCNN_PREC_FP32; ++prec) {
+        const size_t need = conv_wgrad_workspace(conv_of(l, max_batch), prec);
+        if (need > wsb) wsb = need;
+      }
+    }
+  }
+  if (wsb) {
+    s = s ? s : dalloc((void**)&n->ws.ptr, wsb);
+    n->ws.bytes = wsb;
+  }
+  if (!s) {
+    if (cudaMemcpy(n->params, hp.data(), sizeof(float) * (size_t)n->nparams,
+                   cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemset(n->grads, 0, pbytes) != cudaSuccess ||
+        cudaMemset(n->vel, 0, pbytes) != cudaSuccess ||
+        cudaMemset(n->values, 0, sizeof(float) * n->out_units * max_batch) != cudaSuccess ||
+        cudaMemset(n->cls, 0, sizeof(int) * max_batch) != cudaSuccess ||
+        cudaMemset(n->err, 0, sizeof(int) * 4) != cudaSuccess)
+      s = fail(VCNN_ECUDA, "net_create: initial upload failed");
+  }
+  if (s) {
+    vcnn_net_destroy(n);
+    return s;
+  }
+  *out = n;
+  return VCNN_OK;
+}
+
+int vcnn_net_destroy(vcnn_net* n) {
+  if (!n) return VCNN_OK;
+  if (n->stream) cudaStreamSynchronize(n->stream);
+  else cudaDeviceSynchronize();
+  drop_graph(n);
+  for (LayerRt& l : n->L) {
+    cudaFree(l.out);
+    cudaFree(l.gpre);
+    cudaFree(l.arg);
+  }
+  cudaFree(n->params);
+  cudaFree(n->grads);
+  cudaFree(n->vel);
+  cudaFree(n->x);
+  cudaFree(n->cls);
+  cudaFree(n->values);
+  cudaFree(n->loss);
+  cudaFree(n->err);
+  cudaFree(n->ws.ptr);
+  for (cudaEvent_t e : n->event_pool) cudaEventDestroy(e);
+  delete n;
+  return VCNN_OK;
+}
+
+int64_t vcnn_net_num_params(const vcnn_net* n) { return n ? n->nparams : -1; }
+
+int vcnn_net_param_layout(const vcnn_net* n, int64_t* w_off, int64_t* w_len, int64_t* b_off,
+                          int64_t* b_len) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  for (size_t i = 0; i < n->L.size(); ++i) {
+    if (w_off) w_off[i] = n->L[i].w_off;
+    if (w_len) w_len[i] = n->L[i].w_len;
+    if (b_off) b_off[i] = n->L[i].b_off;
+    if (b_len) b_len[i] = n->L[i].b_len;
+  }
+  return VCNN_OK;
+}
+
+int vcnn_net_layer_out_size(const vcnn_net* n, int layer, int64_t* per_sample) {
+  if (!n || layer < 0 || layer >= (int)n->L.size())
+    return fail(VCNN_EBOUNDS, "layer index out of range");
+  *per_sample = n->L[layer].out_per;
+  return VCNN_OK;
+}
+
+int vcnn_net_set_stream(vcnn_net* n, void* stream) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (n->stream != as_stream(stream)) drop_graph(n);
+  n->stream = as_stream(stream);
+  return VCNN_OK;
+}
+
+int vcnn_net_set_pool_backward_mode(vcnn_net* n, int mode) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (mode != VCNN_POOLBWD_EXACT && mode != VCNN_POOLBWD_PAPER_NN)
+    return fail(VCNN_ECONFIG, "unknown pool backward mode");
+  if (mode != n->pool_bwd_mode) drop_graph(n);
+  n->pool_bwd_mode = mode;
+  return VCNN_OK;
+}
+
+int vcnn_net_set_precision(vcnn_net* n, int precision) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (precision < VCNN_PREC_TF32 || precision > VCNN_PREC_FP32)
+    return fail(VCNN_ECONFIG, "unknown precision");
+  if (precision != n->precision) drop_graph(n);
+  n->precision = precision;
+  return VCNN_OK;
+}
+
+int vcnn_net_get_params(vcnn_net* n, float* host) {
+  return copy_out(n, host, n->params, sizeof(float) * n->nparams);
+}
+int vcnn_net_set_params(vcnn_net* n, const float* host) {
+  return copy_in(n, n->params, host, sizeof(float) * n->nparams);
+}
+int vcnn_net_get_grads(vcnn_net* n, float* host) {
+  return copy_out(n, host, n->grads, sizeof(float) * n->nparams);
+}
+int vcnn_net_get_velocity(vcnn_net* n, float* host) {
+  return copy_out(n, host, n->vel, sizeof(float) * n->nparams);
+}
+int vcnn_net_set_velocity(vcnn_net* n, const float* host) {
+  return copy_in(n, n->vel, host, sizeof(float) * n->nparams);
+}
+
+int vcnn_net_device_buffers(vcnn_net* n, float** params, float** grads, float** velocity) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (params) *params = n->params;
+  if (grads) *grads = n->grads;
+  if (velocity) *velocity = n->vel;
+  return VCNN_OK;
+}
+
+int vcnn_net_input_buffers(vcnn_net* n, float** x, int** cls, float** values) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (x) *x = n->x;
+  if (cls) *cls = n->cls;
+  if (values) *values = n->values;
+  return VCNN_OK;
+}
+
+int vcnn_net_set_batch_device(vcnn_net* n, int batch, const float* x, const int* cls,
+                              const float* values) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(check_batch(n, batch));
+  VCNN_CUDA_TRY(cudaMemcpyAsync(n->x, x, sizeof(float) * n->in_per * batch,
+                                cudaMemcpyDeviceToDevice, n->stream));
+  if (cls)
+    VCNN_CUDA_TRY(cudaMemcpyAsync(n->cls, cls, sizeof(int) * batch, cudaMemcpyDeviceToDevice,
+                                  n->stream));
+  if (values)
+    VCNN_CUDA_TRY(cudaMemcpyAsync(n->values, values, sizeof(float) * n->out_units * batch,
+                                  cudaMemcpyDeviceToDevice, n->stream));
+  return VCNN_OK;
+}
+
+int vcnn_net_forward_backward(vcnn_net* n, int batch) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(check_batch(n, batch));
+  TRY(run_forward(n, batch));
+  return run_backward(n, batch);
+}
+
+int vcnn_net_forward(vcnn_net* n, int batch) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(check_batch(n, batch));
+  return run_forward(n, batch);
+}
+
+int vcnn_net_sgd_step(vcnn_net* n, float lr, float mom, float grad_scale) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(check_cfg(lr, mom));
+  return run_sgd(n, lr, mom, grad_scale);
+}
+
+int vcnn_net_train_step(vcnn_net* n, int batch, float lr, float mom) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  return train_step(n, batch, lr, mom);
+}
+
+int vcnn_net_train_step_host(vcnn_net* n, int batch, const float* x, const int* cls,
+                             const float* values, float lr, float mom, float* loss_out) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(check_batch(n, batch));
+  if (n->spec.loss == VCNN_LOSS_SOFTMAX_CE) {
+    if (!cls) return fail(VCNN_ESHAPE, "loss: class targets required");
+    for (int b = 0; b < batch; ++b)
+      if (cls[b] < 0 || cls[b] >= n->out_units)
+        return fail(VCNN_EBOUNDS, "loss: class index " + std::to_string(cls[b]) +
+                                      " out of range [0," + std::to_string(n->out_units) + ")");
+  } else if (!values) {
+    return fail(VCNN_ESHAPE, "loss: value targets required");
+  }
+  VCNN_CUDA_TRY(cudaMemcpyAsync(n->x, x, sizeof(float) * n->in_per * batch,
+                                cudaMemcpyHostToDevice, n->stream));
+  if (n->spec.loss == VCNN_LOSS_SOFTMAX_CE)
+    VCNN_CUDA_TRY(cudaMemcpyAsync(n->cls, cls, sizeof(int) * batch, cudaMemcpyHostToDevice,
+                                  n->stream));
+  else
+    VCNN_CUDA_TRY(cudaMemcpyAsync(n->values, values, sizeof(float) * n->out_units * batch,
+                                  cudaMemcpyHostToDevice, n->stream));
+  TRY(train_step(n, batch, lr, mom));
+  float l = 0;
+  TRY(copy_out(n, &l, n->loss, sizeof(float)));
+  if (loss_out) *loss_out = l;
+  return VCNN_OK;
+}
+
+int vcnn_net_forward_host(vcnn_net* n, int batch, const float* x, float* out) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(check_batch(n, batch));
+  VCNN_CUDA_TRY(cudaMemcpyAsync(n->x, x, sizeof(float) * n->in_per * batch,
+                                cudaMemcpyHostToDevice, n->stream));
+  TRY(run_forward(n, batch));
+  return copy_out(n, out, n->L.back().out, sizeof(float) * n->out_units * batch);
+}
+
+int vcnn_net_enable_graph(vcnn_net* n, int enable) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  n->use_graph = enable != 0;
+  if (!n->use_graph) drop_graph(n);
+  return VCNN_OK;
+}
+
+int vcnn_net_get_loss(vcnn_net* n, float* loss) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(copy_out(n, loss, n->loss, sizeof(float)));
+  return check_errflag(n);
+}
+
+int vcnn_net_get_output(vcnn_net* n, float* host) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  return copy_out(n, host, n->L.back().out, sizeof(float) * n->out_units * n->max_batch);
+}
+
+int vcnn_net_get_layer_output(vcnn_net* n, int layer, float* host) {
+  if (!n || layer < 0 || layer >= (int)n->L.size())
+    return fail(VCNN_EBOUNDS, "layer index out of range");
+  const LayerRt& l = n->L[layer];
+  return copy_out(n, host, l.out, sizeof(float) * l.out_per * n->max_batch);
+}
+
+int vcnn_net_get_pool_arg(vcnn_net* n, int layer, int64_t* host) {
+  if (!n || layer < 0 || layer >= (int)n->L.size())
+    return fail(VCNN_EBOUNDS, "layer index out of range");
+  const LayerRt& l = n->L[layer];
+  if (!l.arg) return fail(VCNN_ESHAPE, "layer has no argmax (not a max pool)");
+  const size_t cnt = (size_t)(l.out_per * n->max_batch);
+  std::vector<int32_t> tmp(cnt);
+  TRY(copy_out(n, tmp.data(), l.arg, sizeof(int32_t) * cnt));
+  for (size_t i = 0; i < cnt; ++i) host[i] = tmp[i];
+  return VCNN_OK;
+}
+
+int vcnn_net_kernels_per_step(vcnn_net* n, int* count) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  *count = n->kernels_per_step;
+  return VCNN_OK;
+}
+
+int vcnn_net_enable_breakdown(vcnn_net* n, int enable) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  n->breakdown = enable != 0;
+  n->marks.clear();
+  n->event_next = 0;
+  for (double& s : n->seconds) s = 0;
+  return VCNN_OK;
+}
+
+int vcnn_net_read_breakdown(vcnn_net* n, double* seconds8) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  for (auto& m : n->marks) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, m.second.first, m.second.second);
+    n->seconds[m.first] += ms * 1e-3;
+  }
+  n->marks.clear();
+  n->event_next = 0;
+  for (int i = 0; i < 8; ++i) seconds8[i] = n->seconds[i];
+  return VCNN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,130 @@
+// kernels.cuh -- internal launcher API shared by the C ABI (capi.cu) and the
+// network engine (engine.cu).  All launchers are stream-ordered and return a
+// vcnn_status.  "gpre" is always a gradient w.r.t. a layer's PRE-activation
+// (dY * act'(Y)), which is how the engine fuses every activation derivative
+// into the kernel that produces the gradient (no standalone act' pass).
+#pragma once
+
+#include "common.cuh"
+
+namespace vcnn_b200 {
+
+// ConvGeometry + map count (vectorize.hpp:13-42)
+struct ConvDesc {
+  int B, C, H, W;  // input
+  int K;           // output maps
+  int kh, kw, s;
+  int OH, OW;
+  __host__ __device__ int64_t kd() const { return (int64_t)C * kh * kw; }
+  __host__ __device__ int64_t ohw() const { return (int64_t)OH * OW; }
+  __host__ __device__ int64_t pixels() const { return ohw() * B; }
+  __host__ __device__ int64_t in_size() const { return (int64_t)B * C * H * W; }
+  __host__ __device__ int64_t out_size() const { return (int64_t)B * K * OH * OW; }
+};
+
+// PoolGeometry (vectorize.hpp:134-162)
+struct PoolDesc {
+  int B, C, H, W;
+  int ph, pw, s, mode;
+  int OH, OW;
+  __host__ __device__ int64_t in_size() const { return (int64_t)B * C * H * W; }
+  __host__ __device__ int64_t out_size() const { return (int64_t)B * C * OH * OW; }
+};
+
+// Device scratch for split-K partial sums and loss reductions.
+struct Workspace {
+  float* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+// ---- memory-bound kernels (simt.cu) ----
+int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st);
+int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st);
+int launch_col2im_map(const ConvDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st);
+int launch_pool_map(const PoolDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st);
+template <class IdxT>
+int launch_pool_fwd(const PoolDesc& d, const float* x, const float* bias, int act, float* y,
+                    IdxT* arg, cudaStream_t st);
+// dx = pool_backward(gpre) * act_prev'(yprev)   (yprev may be null)
+template <class IdxT>
+int launch_pool_bwd(const PoolDesc& d, int bwd_mode, const float* gpre, const IdxT* arg,
+                    float* dx, const float* yprev, int act_prev, cudaStream_t st);
+int launch_pool_bias_grad(const PoolDesc& d, const float* gpre, float* dbias, cudaStream_t st);
+int launch_act_fwd(int64_t n, int act, const float* x, float* y, cudaStream_t st);
+// g = dy * act'(y)  (dy may equal g)
+int launch_act_bwd(int64_t n, int act, const float* y, const float* dy, float* g,
+                   cudaStream_t st);
+// fused loss forward+backward; grad = dL/dpred * act_last'(pred); err set on
+// out-of-range class.  Any of loss/grad may be null.
+int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
+                const float* values, float* loss, float* grad, int act_last, int* err,
+                cudaStream_t st);
+int launch_sgd(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+               cudaStream_t st);
+int launch_accumulate(const float* values, const int64_t* source, const int64_t* target,
+                      int64_t pairs, int64_t target_len, int reducer, float* out, int64_t* arg,
+                      cudaStream_t st);
+
+// ---- GEMM-shaped kernels: SIMT fp32 reference (simt.cu) or tcgen05 (tc.cu) ----
+int launch_conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
+                    float* y, int prec, const Workspace& ws, cudaStream_t st);
+// dw [K][kd], db [K] from the pre-activation gradient gpre [B][K][OH][OW]
+int launch_conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw,
+                      float* db, int prec, const Workspace& ws, cudaStream_t st);
+// dx [B][C][H][W] = col2im(W^T gpre) * act_prev'(yprev)
+int launch_conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
+                      const float* yprev, int act_prev, int prec, const Workspace& ws,
+                      cudaStream_t st);
+int launch_full_fwd(int B, int in, int out, const float* x, const float* w, const float* b,
+                    int act, float* y, int prec, const Workspace& ws, cudaStream_t st);
+int launch_full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw,
+                      float* db, int prec, const Workspace& ws, cudaStream_t st);
+int launch_full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
+                      const float* yprev, int act_prev, int prec, const Workspace& ws,
+                      cudaStream_t st);
+// C[m][n] = A[m][k] * (transB ? B[n][k] : B[k][n])
+int launch_matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
+                  bool transB, int prec, const Workspace& ws, cudaStream_t st);
+
+// workspace bytes the GEMM launchers need for a shape (0 if none)
+size_t conv_wgrad_workspace(const ConvDesc& d, int prec);
+size_t full_wgrad_workspace(int B, int in, int out, int prec);
+
+// ---- SIMT implementations (simt.cu) used for VCNN_PREC_FP32 ----
+namespace simt {
+int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
+             float* y, cudaStream_t st);
+int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
+               cudaStream_t st);
+int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
+               const float* yprev, int act_prev, cudaStream_t st);
+int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
+             float* y, cudaStream_t st);
+int full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw, float* db,
+               cudaStream_t st);
+int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
+               const float* yprev, int act_prev, cudaStream_t st);
+int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
+           bool transB, cudaStream_t st);
+}  // namespace simt
+
+// ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----
+namespace tc {
+int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
+             float* y, bool split3, cudaStream_t st);
+int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
+               bool split3, const Workspace& ws, cudaStream_t st);
+int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
+               const float* yprev, int act_prev, bool split3, cudaStream_t st);
+int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
+             float* y, bool split3, cudaStream_t st);
+int full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw, float* db,
+               bool split3, cudaStream_t st);
+int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
+               const float* yprev, int act_prev, bool split3, cudaStream_t st);
+int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
+           bool transB, bool split3, cudaStream_t st);
+size_t conv_wgrad_workspace(const ConvDesc& d);
+}  // namespace tc
+
+}  // namespace vcnn_b200

@@ -1,0 +1,723 @@
+// simt.cu -- memory-bound kernels (index maps, pooling, activations, losses,
+// SGD) and the SIMT fp32 reference GEMM/conv path (VCNN_PREC_FP32).
+//
+// Every kernel is deterministic: reductions run in a fixed order (strided
+// per-thread partials + a fixed shared-memory tree), scatters of the
+// reference (col2im, pool_backward) are rewritten as gathers so no float
+// atomics are needed.  Reference paths: /root/reference/proj/include/vcnn.
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace vcnn_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline unsigned grid_for(int64_t n, int threads = kThreads) {
+  int64_t g = cdiv(n, threads);
+  if (g > (1LL << 30)) g = 1LL << 30;
+  return (unsigned)(g < 1 ? 1 : g);
+}
+
+// fixed-order block tree reduction (deterministic for a fixed blockDim)
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = NT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  float r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// im2col (vectorize.hpp:54-79): one thread per patch cell, column fastest so
+// the patch-matrix writes are coalesced.
+__global__ void im2col_kernel(ConvDesc d, const float* __restrict__ x, float* __restrict__ P) {
+  const int64_t cols = d.pixels();
+  const int64_t total = d.kd() * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / cols, col = i - row * cols;
+    const int kx = (int)(row % d.kw);
+    const int ky = (int)((row / d.kw) % d.kh);
+    const int c = (int)(row / ((int64_t)d.kw * d.kh));
+    const int64_t b = col / d.ohw();
+    const int64_t r = col - b * d.ohw();
+    const int oy = (int)(r / d.OW), ox = (int)(r - (int64_t)oy * d.OW);
+    P[i] = x[((b * d.C + c) * d.H + (int64_t)oy * d.s + ky) * d.W + (int64_t)ox * d.s + kx];
+  }
+}
+
+// col2im (vectorize.hpp:111-120) in gather form: each input cell sums the
+// patch cells it fed in (ky,kx) ascending order -- the same per-cell order
+// as the reference's pair-ordered scatter (build_col2im_map enumerates
+// c,ky,kx,b,oy,ox), so results are bit-identical to a sequential scatter.
+__global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* __restrict__ dX) {
+  const int64_t cols = d.pixels();
+  const int64_t total = d.in_size();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % d.W);
+    const int y = (int)((i / d.W) % d.H);
+    const int c = (int)((i / ((int64_t)d.W * d.H)) % d.C);
+    const int64_t b = i / ((int64_t)d.W * d.H * d.C);
+    float acc = 0.f;
+    for (int ky = 0; ky < d.kh; ++ky) {
+      const int ty = y - ky;
+      if (ty < 0 || ty % d.s) continue;
+      const int oy = ty / d.s;
+      if (oy >= d.OH) continue;
+      for (int kx = 0; kx < d.kw; ++kx) {
+        const int tx = x - kx;
+        if (tx < 0 || tx % d.s) continue;
+        const int ox = tx / d.s;
+        if (ox >= d.OW) continue;
+        const int64_t row = ((int64_t)c * d.kh + ky) * d.kw + kx;
+        acc += dP[row * cols + b * d.ohw() + (int64_t)oy * d.OW + ox];
+      }
+    }
+    dX[i] = acc;
+  }
+}
+
+// build_col2im_map (vectorize.hpp:84-106): pair k enumerates
+// (row=(c,ky,kx), b, oy, ox); its source is k itself.
+__global__ void col2im_map_kernel(ConvDesc d, int64_t* __restrict__ src,
+                                  int64_t* __restrict__ tgt) {
+  const int64_t cols = d.pixels();
+  const int64_t total = d.kd() * cols;
+  const int64_t plane = (int64_t)d.H * d.W;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = k / cols, col = k - row * cols;
+    const int kx = (int)(row % d.kw);
+    const int ky = (int)((row / d.kw) % d.kh);
+    const int64_t c = row / ((int64_t)d.kw * d.kh);
+    const int64_t b = col / d.ohw();
+    const int64_t r = col - b * d.ohw();
+    const int64_t oy = r / d.OW, ox = r - oy * d.OW;
+    src[k] = k;
+    tgt[k] = (b * d.C + c) * plane + (oy * d.s + ky) * d.W + (ox * d.s + kx);
+  }
+}
+
+// build_pool_map (vectorize.hpp:167-191): pairs (b,c,oy,ox,py,px)
+__global__ void pool_map_kernel(PoolDesc d, int64_t* __restrict__ src,
+                                int64_t* __restrict__ tgt) {
+  const int64_t ws = (int64_t)d.ph * d.pw;
+  const int64_t total = d.out_size() * ws;
+  const int64_t plane = (int64_t)d.H * d.W;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = k / ws, w = k - t * ws;
+    const int py = (int)(w / d.pw), px = (int)(w - (int64_t)py * d.pw);
+    const int64_t ox = t % d.OW, oy = (t / d.OW) % d.OH, bc = t / ((int64_t)d.OW * d.OH);
+    src[k] = bc * plane + (oy * d.s + py) * d.W + (ox * d.s + px);
+    tgt[k] = t;
+  }
+}
+
+// pool_forward (vectorize.hpp:197-210 -> tensor.hpp:240-289) + pool layer
+// bias and activation (layers.hpp:305-321).  Max: the first window element
+// seeds, then strict '>' in (py,px) order == ties to the lowest input index,
+// and a NaN survives only if it is first (no fmaxf).
+template <class IdxT>
+__global__ void pool_fwd_kernel(PoolDesc d, const float* __restrict__ x,
+                                const float* __restrict__ bias, int act, float* __restrict__ y,
+                                IdxT* __restrict__ arg) {
+  const int64_t total = d.out_size();
+  const int64_t plane = (int64_t)d.H * d.W;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int ox = (int)(t % d.OW), oy = (int)((t / d.OW) % d.OH);
+    const int64_t bc = t / ((int64_t)d.OW * d.OH);
+    const int64_t base = bc * plane + (int64_t)oy * d.s * d.W + (int64_t)ox * d.s;
+    float v;
+    if (d.mode == VCNN_POOL_MAX) {
+      float best = x[base];
+      int64_t a = base;
+      for (int py = 0; py < d.ph; ++py)
+        for (int px = 0; px < d.pw; ++px) {
+          const int64_t s = base + (int64_t)py * d.W + px;
+          const float xv = x[s];
+          if (xv > best) {
+            best = xv;
+            a = s;
+          }
+        }
+      v = best;
+      if (arg) arg[t] = (IdxT)a;
+    } else {
+      float acc = 0.f;
+      for (int py = 0; py < d.ph; ++py)
+        for (int px = 0; px < d.pw; ++px) acc += x[base + (int64_t)py * d.W + px];
+      v = acc / (float)(d.ph * d.pw);
+      if (arg) arg[t] = (IdxT)-1;
+    }
+    if (bias) v += bias[bc % d.C];
+    y[t] = act_fwd(act, v);
+  }
+}
+
+// pool_backward (vectorize.hpp:224-249) in gather form: each input cell
+// visits its covering windows in window order (the reference's scatter
+// order), then the upstream activation derivative is applied.
+template <class IdxT>
+__global__ void pool_bwd_kernel(PoolDesc d, int bwd_mode, const float* __restrict__ g,
+                                const IdxT* __restrict__ arg, float* __restrict__ dx,
+                                const float* __restrict__ yprev, int act_prev) {
+  const int64_t total = d.in_size();
+  const float scale = 1.0f / (float)(d.ph * d.pw);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % d.W), y = (int)((i / d.W) % d.H);
+    const int64_t bc = i / ((int64_t)d.W * d.H);
+    int oy0 = y - d.ph + 1;
+    oy0 = oy0 <= 0 ? 0 : (oy0 + d.s - 1) / d.s;
+    int oy1 = y / d.s;
+    if (oy1 > d.OH - 1) oy1 = d.OH - 1;
+    int ox0 = x - d.pw + 1;
+    ox0 = ox0 <= 0 ? 0 : (ox0 + d.s - 1) / d.s;
+    int ox1 = x / d.s;
+    if (ox1 > d.OW - 1) ox1 = d.OW - 1;
+    float acc = 0.f;
+    for (int oy = oy0; oy <= oy1; ++oy)
+      for (int ox = ox0; ox <= ox1; ++ox) {
+        const int64_t t = (bc * d.OH + oy) * d.OW + ox;
+        if (bwd_mode == VCNN_POOLBWD_PAPER_NN) {
+          acc += g[t];
+        } else if (d.mode == VCNN_POOL_MAX) {
+          if ((int64_t)arg[t] == i) acc += g[t];
+        } else {
+          acc += g[t] * scale;
+        }
+      }
+    if (yprev) acc *= act_grad_from_out(act_prev, yprev[i]);
+    dx[i] = acc;
+  }
+}
+
+// pool bias gradient (layers.hpp:341-351): per-channel sum over batch and
+// plane; one block per channel.
+__global__ void pool_bias_grad_kernel(PoolDesc d, const float* __restrict__ g,
+                                      float* __restrict__ db) {
+  __shared__ float sh[kThreads];
+  const int c = blockIdx.x;
+  const int64_t plane = (int64_t)d.OH * d.OW;
+  const int64_t n = plane * d.B;
+  float acc = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) {
+    const int64_t b = i / plane, p = i - b * plane;
+    acc += g[(b * d.C + c) * plane + p];
+  }
+  acc = block_sum<kThreads>(acc, sh);
+  if (threadIdx.x == 0) db[c] = acc;
+}
+
+__global__ void act_fwd_kernel(int64_t n, int act, const float* __restrict__ x,
+                               float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = act_fwd(act, x[i]);
+}
+
+__global__ void act_bwd_kernel(int64_t n, int act, const float* __restrict__ y, const float* dy,
+                               float* g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    g[i] = dy[i] * act_grad_from_out(act, y[i]);
+}
+
+// loss_forward + loss_backward, softmax-CE (layers.hpp:402-459): one warp
+// per sample with shuffle max/sum; per-sample losses summed by thread 0 in
+// sample order (the reference's order), then / B.
+constexpr int kLossThreads = 512;
+__global__ void softmax_ce_kernel(int B, int units, const float* __restrict__ pred,
+                                  const int* __restrict__ cls, float* __restrict__ loss,
+                                  float* __restrict__ grad, int act_last, int* err) {
+  extern __shared__ float per_sample[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = blockDim.x >> 5;
+  const float inv_b = 1.0f / (float)B;
+  for (int b = warp; b < B; b += nwarps) {
+    const float* l = pred + (int64_t)b * units;
+    int c = cls[b];
+    const bool bad = c < 0 || c >= units;
+    if (bad && lane == 0 && err) atomicExch(err, 1);
+    float m = -INFINITY;
+    for (int u = lane; u < units; u += 32) m = fmaxf(m, l[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float s = 0.f;
+    for (int u = lane; u < units; u += 32) s += expf(l[u] - m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (grad) {
+      for (int u = lane; u < units; u += 32) {
+        float gv = expf(l[u] - m) / s * inv_b;
+        if (u == c) gv -= inv_b;
+        if (act_last != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(act_last, l[u]);
+        grad[(int64_t)b * units + u] = gv;
+      }
+    }
+    if (lane == 0) per_sample[b] = bad ? 0.f : (m + logf(s) - l[c]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && loss) {
+    float total = 0.f;
+    for (int b = 0; b < B; ++b) total += per_sample[b];
+    *loss = total / (float)B;
+  }
+}
+
+// MSE (layers.hpp:425-433, :461-467): loss = mean (p-t)^2, grad 2(p-t)/n
+__global__ void mse_kernel(int64_t n, const float* __restrict__ p, const float* __restrict__ t,
+                           float* __restrict__ loss, float* __restrict__ grad, int act_last) {
+  __shared__ float sh[kLossThreads];
+  const float scale = 2.0f / (float)n;
+  float acc = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const float dd = p[i] - t[i];
+    acc += dd * dd;
+    if (grad) {
+      float gv = scale * dd;
+      if (act_last != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(act_last, p[i]);
+      grad[i] = gv;
+    }
+  }
+  acc = block_sum<kLossThreads>(acc, sh);
+  if (threadIdx.x == 0 && loss) *loss = acc / (float)n;
+}
+
+// sgd_step (network.hpp:242-273): v = mom*v + g; w -= lr*v
+__global__ void sgd_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
+                           const float* __restrict__ g, float lr, float mom, float scale,
+                           int vec) {
+  const int64_t n4 = vec ? (n >> 2) : 0;
+  float4* w4 = reinterpret_cast<float4*>(w);
+  float4* v4 = reinterpret_cast<float4*>(v);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 wv = w4[i], vv = v4[i], gv = g4[i];
+    vv.x = mom * vv.x + scale * gv.x;
+    vv.y = mom * vv.y + scale * gv.y;
+    vv.z = mom * vv.z + scale * gv.z;
+    vv.w = mom * vv.w + scale * gv.w;
+    wv.x -= lr * vv.x;
+    wv.y -= lr * vv.y;
+    wv.z -= lr * vv.z;
+    wv.w -= lr * vv.w;
+    w4[i] = wv;
+    v4[i] = vv;
+  }
+  for (int64_t i = (n4 << 2) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += stride) {
+    const float vv = mom * v[i] + scale * g[i];
+    v[i] = vv;
+    w[i] -= lr * vv;
+  }
+}
+
+// generic accumulate_by_index / accumulate_max_arg (tensor.hpp:228-289):
+// pairs stably sorted by target, so each bucket is reduced in map order.
+__global__ void accumulate_kernel(const float* __restrict__ values,
+                                  const int64_t* __restrict__ skeys,
+                                  const int64_t* __restrict__ sidx,
+                                  const int64_t* __restrict__ source, int64_t pairs,
+                                  int64_t target_len, int reducer, float* __restrict__ out,
+                                  int64_t* __restrict__ arg) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < target_len;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = pairs;  // lower_bound(t)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (skeys[mid] < t) lo = mid + 1; else hi = mid;
+    }
+    float acc = 0.f;
+    int64_t a = -1, cnt = 0;
+    for (int64_t p = lo; p < pairs && skeys[p] == t; ++p) {
+      const int64_t s = source[sidx[p]];
+      const float v = values[s];
+      if (reducer == VCNN_REDUCE_MAX) {
+        if (arg) {
+          if (a < 0 || v > acc || (v == acc && s < a)) {
+            acc = v;
+            a = s;
+          }
+        } else if (cnt == 0 || v > acc) {
+          acc = v;
+        }
+      } else {
+        acc += v;
+      }
+      ++cnt;
+    }
+    if (reducer == VCNN_REDUCE_MEAN && cnt > 0) acc /= (float)cnt;
+    if (cnt == 0) acc = 0.f;
+    out[t] = acc;
+    if (arg) arg[t] = a;
+  }
+}
+
+__global__ void iota_kernel(int64_t n, int64_t* __restrict__ v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = i;
+}
+
+// ---------------------------------------------------------------------------
+// SIMT fp32 GEMM-shaped kernels (VCNN_PREC_FP32).  Straight restatements
+// with ascending-k accumulation; block-tree reductions where the reduction
+// dimension is the batch.
+__global__ void conv_fwd_simt(ConvDesc d, const float* __restrict__ x,
+                              const float* __restrict__ w, const float* __restrict__ b, int act,
+                              float* __restrict__ y) {
+  const int64_t total = d.out_size();
+  const int64_t kd = d.kd();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int ox = (int)(i % d.OW), oy = (int)((i / d.OW) % d.OH);
+    const int n = (int)((i / d.ohw()) % d.K);
+    const int64_t bb = i / (d.ohw() * d.K);
+    const float* wr = w + n * kd;
+    const float* xb = x + bb * d.C * d.H * d.W + (int64_t)oy * d.s * d.W + (int64_t)ox * d.s;
+    float acc = 0.f;
+    for (int c = 0; c < d.C; ++c)
+      for (int ky = 0; ky < d.kh; ++ky)
+        for (int kx = 0; kx < d.kw; ++kx)
+          acc += wr[((int64_t)c * d.kh + ky) * d.kw + kx] *
+                 xb[((int64_t)c * d.H + ky) * d.W + kx];
+    y[i] = act_fwd(act, acc + b[n]);
+  }
+}
+
+// one block per (n, k) of dW, plus blocks k == kd computing db[n]
+__global__ void conv_wgrad_simt(ConvDesc d, const float* __restrict__ x,
+                                const float* __restrict__ g, float* __restrict__ dw,
+                                float* __restrict__ db) {
+  __shared__ float sh[kThreads];
+  const int64_t kd = d.kd();
+  const int64_t k = blockIdx.x;  // 0..kd (kd = bias)
+  const int n = blockIdx.y;
+  const int64_t pix = d.pixels();
+  int c = 0, ky = 0, kx = 0;
+  if (k < kd) {
+    kx = (int)(k % d.kw);
+    ky = (int)((k / d.kw) % d.kh);
+    c = (int)(k / ((int64_t)d.kw * d.kh));
+  }
+  float acc = 0.f;
+  for (int64_t p = threadIdx.x; p < pix; p += kThreads) {
+    const int64_t bb = p / d.ohw(), r = p - bb * d.ohw();
+    const int oy = (int)(r / d.OW), ox = (int)(r - (int64_t)oy * d.OW);
+    const float gv = g[(bb * d.K + n) * d.ohw() + r];
+    if (k < kd)
+      acc += gv * x[((bb * d.C + c) * d.H + (int64_t)oy * d.s + ky) * d.W + (int64_t)ox * d.s + kx];
+    else
+      acc += gv;
+  }
+  acc = block_sum<kThreads>(acc, sh);
+  if (threadIdx.x == 0) {
+    if (k < kd) dw[(int64_t)n * kd + k] = acc;
+    else db[n] = acc;
+  }
+}
+
+__global__ void conv_dgrad_simt(ConvDesc d, const float* __restrict__ g,
+                                const float* __restrict__ w, float* __restrict__ dx,
+                                const float* __restrict__ yprev, int act_prev) {
+  const int64_t total = d.in_size();
+  const int64_t kd = d.kd();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % d.W), y = (int)((i / d.W) % d.H);
+    const int c = (int)((i / ((int64_t)d.W * d.H)) % d.C);
+    const int64_t bb = i / ((int64_t)d.W * d.H * d.C);
+    float acc = 0.f;
+    for (int n = 0; n < d.K; ++n) {
+      const float* gb = g + (bb * d.K + n) * d.ohw();
+      const float* wr = w + n * kd + (int64_t)c * d.kh * d.kw;
+      for (int ky = 0; ky < d.kh; ++ky) {
+        const int ty = y - ky;
+        if (ty < 0 || ty % d.s) continue;
+        const int oy = ty / d.s;
+        if (oy >= d.OH) continue;
+        for (int kx = 0; kx < d.kw; ++kx) {
+          const int tx = x - kx;
+          if (tx < 0 || tx % d.s) continue;
+          const int ox = tx / d.s;
+          if (ox >= d.OW) continue;
+          acc += wr[ky * d.kw + kx] * gb[(int64_t)oy * d.OW + ox];
+        }
+      }
+    }
+    if (yprev) acc *= act_grad_from_out(act_prev, yprev[i]);
+    dx[i] = acc;
+  }
+}
+
+__global__ void full_fwd_simt(int B, int in, int out, const float* __restrict__ x,
+                              const float* __restrict__ w, const float* __restrict__ b, int act,
+                              float* __restrict__ y) {
+  const int64_t total = (int64_t)B * out;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(i % out);
+    const int64_t bb = i / out;
+    const float* xr = x + bb * in;
+    const float* wr = w + (int64_t)o * in;
+    float acc = 0.f;
+    for (int k = 0; k < in; ++k) acc += xr[k] * wr[k];
+    y[i] = act_fwd(act, acc + b[o]);
+  }
+}
+
+// dW[o][i] = sum_b g[b][o] x[b][i]; column i == in gives db[o]
+__global__ void full_wgrad_simt(int B, int in, int out, const float* __restrict__ x,
+                                const float* __restrict__ g, float* __restrict__ dw,
+                                float* __restrict__ db) {
+  const int64_t total = (int64_t)out * (in + 1);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % (in + 1));
+    const int o = (int)(t / (in + 1));
+    float acc = 0.f;
+    if (i < in) {
+      for (int bb = 0; bb < B; ++bb) acc += g[(int64_t)bb * out + o] * x[(int64_t)bb * in + i];
+      dw[(int64_t)o * in + i] = acc;
+    } else {
+      for (int bb = 0; bb < B; ++bb) acc += g[(int64_t)bb * out + o];
+      db[o] = acc;
+    }
+  }
+}
+
+__global__ void full_dgrad_simt(int B, int in, int out, const float* __restrict__ g,
+                                const float* __restrict__ w, float* __restrict__ dx,
+                                const float* __restrict__ yprev, int act_prev) {
+  const int64_t total = (int64_t)B * in;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % in);
+    const int64_t bb = t / in;
+    float acc = 0.f;
+    for (int o = 0; o < out; ++o) acc += g[bb * out + o] * w[(int64_t)o * in + i];
+    if (yprev) acc *= act_grad_from_out(act_prev, yprev[t]);
+    dx[t] = acc;
+  }
+}
+
+__global__ void matmul_simt(int64_t m, int64_t k, int64_t n, const float* __restrict__ a,
+                            const float* __restrict__ b, float* __restrict__ c, bool transB) {
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t % n, i = t / n;
+    float acc = 0.f;
+    if (transB)
+      for (int64_t q = 0; q < k; ++q) acc += a[i * k + q] * b[j * k + q];
+    else
+      for (int64_t q = 0; q < k; ++q) acc += a[i * k + q] * b[q * n + j];
+    c[t] = acc;
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st) {
+  im2col_kernel<<<grid_for(d.kd() * d.pixels()), kThreads, 0, st>>>(d, x, P);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st) {
+  col2im_kernel<<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_col2im_map(const ConvDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st) {
+  col2im_map_kernel<<<grid_for(d.kd() * d.pixels()), kThreads, 0, st>>>(d, src, tgt);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_pool_map(const PoolDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st) {
+  pool_map_kernel<<<grid_for(d.out_size() * d.ph * d.pw), kThreads, 0, st>>>(d, src, tgt);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+template <class IdxT>
+int launch_pool_fwd(const PoolDesc& d, const float* x, const float* bias, int act, float* y,
+                    IdxT* arg, cudaStream_t st) {
+  pool_fwd_kernel<IdxT><<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, bias, act, y, arg);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+template int launch_pool_fwd<int32_t>(const PoolDesc&, const float*, const float*, int, float*,
+                                      int32_t*, cudaStream_t);
+template int launch_pool_fwd<int64_t>(const PoolDesc&, const float*, const float*, int, float*,
+                                      int64_t*, cudaStream_t);
+
+template <class IdxT>
+int launch_pool_bwd(const PoolDesc& d, int bwd_mode, const float* gpre, const IdxT* arg,
+                    float* dx, const float* yprev, int act_prev, cudaStream_t st) {
+  pool_bwd_kernel<IdxT><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, bwd_mode, gpre, arg, dx,
+                                                                     yprev, act_prev);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+template int launch_pool_bwd<int32_t>(const PoolDesc&, int, const float*, const int32_t*, float*,
+                                      const float*, int, cudaStream_t);
+template int launch_pool_bwd<int64_t>(const PoolDesc&, int, const float*, const int64_t*, float*,
+                                      const float*, int, cudaStream_t);
+
+int launch_pool_bias_grad(const PoolDesc& d, const float* gpre, float* dbias, cudaStream_t st) {
+  pool_bias_grad_kernel<<<d.C, kThreads, 0, st>>>(d, gpre, dbias);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_act_fwd(int64_t n, int act, const float* x, float* y, cudaStream_t st) {
+  act_fwd_kernel<<<grid_for(n), kThreads, 0, st>>>(n, act, x, y);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_act_bwd(int64_t n, int act, const float* y, const float* dy, float* g,
+                   cudaStream_t st) {
+  act_bwd_kernel<<<grid_for(n), kThreads, 0, st>>>(n, act, y, dy, g);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
+                const float* values, float* loss, float* grad, int act_last, int* err,
+                cudaStream_t st) {
+  if (kind == VCNN_LOSS_SOFTMAX_CE) {
+    const size_t smem = sizeof(float) * (size_t)B;
+    if (smem > 200 * 1024) return fail(VCNN_ESHAPE, "loss: batch too large for one block");
+    if (smem > 48 * 1024)
+      VCNN_CUDA_TRY(cudaFuncSetAttribute(softmax_ce_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+    softmax_ce_kernel<<<1, kLossThreads, smem, st>>>(B, units, pred, cls, loss, grad, act_last,
+                                                      err);
+  } else {
+    mse_kernel<<<1, kLossThreads, 0, st>>>((int64_t)B * units, pred, values, loss, grad,
+                                           act_last);
+  }
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_sgd(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+               cudaStream_t st) {
+  const bool aligned = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(v) |
+                         reinterpret_cast<uintptr_t>(g)) & 15) == 0;
+  const int64_t work = aligned ? ((n >> 2) > 0 ? (n >> 2) : 1) : n;
+  unsigned grid = grid_for(work);
+  if (grid > (unsigned)sm_count() * 8) grid = (unsigned)sm_count() * 8;
+  sgd_kernel<<<grid, kThreads, 0, st>>>(n, w, v, g, lr, mom, scale, aligned ? 1 : 0);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int launch_accumulate(const float* values, const int64_t* source, const int64_t* target,
+                      int64_t pairs, int64_t target_len, int reducer, float* out, int64_t* arg,
+                      cudaStream_t st) {
+  int64_t *keys_out = nullptr, *idx_in = nullptr, *idx_out = nullptr;
+  void* temp = nullptr;
+  size_t temp_bytes = 0;
+  const int64_t np = pairs > 0 ? pairs : 1;
+  VCNN_CUDA_TRY(cudaMallocAsync(&keys_out, sizeof(int64_t) * np, st));
+  VCNN_CUDA_TRY(cudaMallocAsync(&idx_in, sizeof(int64_t) * np, st));
+  VCNN_CUDA_TRY(cudaMallocAsync(&idx_out, sizeof(int64_t) * np, st));
+  if (pairs > 0) {
+    iota_kernel<<<grid_for(pairs), kThreads, 0, st>>>(pairs, idx_in);
+    VCNN_LAUNCHED();
+    // stable radix sort: equal targets keep their map order
+    VCNN_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, target, keys_out, idx_in,
+                                                  idx_out, pairs, 0, 64, st));
+    VCNN_CUDA_TRY(cudaMallocAsync(&temp, temp_bytes, st));
+    VCNN_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, target, keys_out, idx_in,
+                                                  idx_out, pairs, 0, 64, st));
+  }
+  accumulate_kernel<<<grid_for(target_len), kThreads, 0, st>>>(
+      values, keys_out, idx_out, source, pairs, target_len, reducer, out, arg);
+  VCNN_LAUNCHED();
+  if (temp) cudaFreeAsync(temp, st);
+  cudaFreeAsync(keys_out, st);
+  cudaFreeAsync(idx_in, st);
+  cudaFreeAsync(idx_out, st);
+  return VCNN_OK;
+}
+
+namespace simt {
+
+int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
+             float* y, cudaStream_t st) {
+  conv_fwd_simt<<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, w, b, act, y);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
+               cudaStream_t st) {
+  dim3 grid((unsigned)(d.kd() + 1), (unsigned)d.K);
+  conv_wgrad_simt<<<grid, kThreads, 0, st>>>(d, x, gpre, dw, db);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
+               const float* yprev, int act_prev, cudaStream_t st) {
+  conv_dgrad_simt<<<grid_for(d.in_size()), kThreads, 0, st>>>(d, gpre, w, dx, yprev, act_prev);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
+             float* y, cudaStream_t st) {
+  full_fwd_simt<<<grid_for((int64_t)B * out), kThreads, 0, st>>>(B, in, out, x, w, b, act, y);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw, float* db,
+               cudaStream_t st) {
+  full_wgrad_simt<<<grid_for((int64_t)out * (in + 1)), kThreads, 0, st>>>(B, in, out, x, gpre,
+                                                                          dw, db);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
+               const float* yprev, int act_prev, cudaStream_t st) {
+  full_dgrad_simt<<<grid_for((int64_t)B * in), kThreads, 0, st>>>(B, in, out, gpre, w, dx,
+                                                                  yprev, act_prev);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
+           bool transB, cudaStream_t st) {
+  matmul_simt<<<grid_for(m * n), kThreads, 0, st>>>(m, k, n, a, b, c, transB);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+}  // namespace simt
+}  // namespace vcnn_b200
