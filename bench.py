@@ -1,0 +1,429 @@
+#!/usr/bin/env python
+"""Benchmark: training images/sec (forward + backward + SGD update) of the
+VCNN Imp-6 path on B200, BASELINE.json configs[1] (CIFAR-10-shape 3-conv CNN,
+batch 128 per GPU, data-parallel over N GPUs, weak scaling).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+One JSON line on rank 0 (driver contract).  `value` is device-timed with CUDA
+events per step (L2 flushed between steps), max over ranks; `e2e` is the same
+metric through the C-ABI host entry point (pinned host batch -> H2D -> step ->
+D2H loss every step); `roofline` is the dominant kernel's achieved rate over
+the timed breakdown pass; `cpu_baseline` is the reference compiled from its
+own sources (oracle/_ref), timed on this host.
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train images/sec (fwd+bwd+update)"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cifar3")
+    ap.add_argument("--batch", type=int, default=128, help="per-GPU batch")
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "tf32x3", "fp32"])
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--momentum", type=float, default=0.9)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--details", default="", help="write per-op timing JSON here")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+# ----------------------------------------------------------------------------
+# algorithmic work per op: FLOPs = 2*M*N*K per GEMM, bytes =
+# minimal HBM traffic (read inputs once, write outputs once)
+# ----------------------------------------------------------------------------
+def op_work(spec, B):
+    from paper_1501_07338_b200 import spec as S
+    chain = spec.chain()
+    work = {}
+    h, w, c = spec.input
+    for i, L in enumerate(spec.layers):
+        oh, ow, oc = chain[i]
+        nin, nout = B * h * w * c, B * oh * ow * oc
+        if isinstance(L, S.ConvSpec):
+            kd = c * L.kh * L.kw
+            f = 2.0 * B * oh * ow * L.maps * kd
+            pw = L.maps * kd + L.maps
+            work[(i, "fwd")] = (f, 4.0 * (nin + pw + nout))
+            work[(i, "wgrad")] = (f, 4.0 * (nin + nout + pw))
+            work[(i, "dgrad")] = (f, 4.0 * (nout + pw + 2 * nin))
+        elif isinstance(L, S.PoolSpec):
+            work[(i, "fwd")] = (0.0, 4.0 * (nin + 2 * nout))
+            work[(i, "dgrad")] = (0.0, 4.0 * (2 * nout + 2 * nin))
+            work[(i, "wgrad")] = (0.0, 4.0 * nout)
+        else:
+            f = 2.0 * B * (h * w * c) * L.units
+            pw = L.units * h * w * c + L.units
+            work[(i, "fwd")] = (f, 4.0 * (nin + pw + nout))
+            work[(i, "wgrad")] = (f, 4.0 * (nin + nout + pw))
+            work[(i, "dgrad")] = (f, 4.0 * (nout + pw + 2 * nin))
+        h, w, c = oh, ow, oc
+    units = spec.output_units()
+    work[(len(spec.layers) - 1, "loss")] = (0.0, 4.0 * (2 * B * units + B))
+    return work
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update(hbm_gbs=m["hbm_gbs"], bf16_tflops=m["bf16_tflops"], src="measured")
+    except Exception:
+        pass
+    tf = os.path.join(ROOT, "profiles", "tf32_peak.json")
+    if os.path.exists(tf):
+        with open(tf) as f:
+            p["tf32_tflops"] = json.load(f)["tf32_tflops"]
+        p["tf32_src"] = "measured cuBLAS TF32 8192^3 (profiles/tf32_peak.json)"
+    else:
+        p["tf32_tflops"] = p["bf16_tflops"] / 2
+        p["tf32_src"] = "bf16 measured / 2 (dense TF32:BF16 rate ratio)"
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region (NVML)."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+                 0x2: "applications_clocks_setting"}
+        while not self.stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, nm in names.items():
+                    if r & bit and nm != "gpu_idle":
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv:
+            self.t.join()
+
+    def result(self):
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+# the reference arm / CPU baseline: the reference's own Executor<float>(imp6)
+# run_batch + sgd_step, compiled from its sources (oracle/_ref)
+# ----------------------------------------------------------------------------
+def cpu_reference(spec, B, steps, warmup, seconds=None):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ctypes as C
+
+    import oracle_py as O
+    R = O.ref()
+    kind = "reference"
+    if R is None:
+        return None
+    cores = R.ref_max_threads()
+    net = O.make_net(spec)
+    h = R.ref_bench_create(C.byref(net), B, 8, 0.01, 0.9)
+    for _ in range(warmup):
+        R.ref_bench_step(h, 1)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        R.ref_bench_step(h, 1)
+        times.append(time.perf_counter() - t0)
+        if seconds is None and len(times) >= steps:
+            break
+        if seconds is not None and (time.perf_counter() - t_start >= seconds and len(times) >= 3):
+            break
+    R.ref_bench_destroy(h)
+    total = sum(times)
+    return {"value": B * len(times) / total, "unit": "img/s", "cores": cores, "kind": kind,
+            "sample": f"{len(times)} steps of batch {B} ({os.path.basename(O.ref_path())}, "
+                      f"Executor<float>(imp6).run_batch + sgd_step, OpenMP {cores} threads)",
+            "ms_per_step": 1e3 * total / len(times)}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1501_07338_b200 import spec as S
+    spec = S.PRESETS[args.config]()
+    r = cpu_reference(spec, args.batch, args.steps, args.warmup)
+    if r is None:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref not built (reference sources absent)"}))
+        return
+    line = {"metric": METRIC, "value": r["value"], "unit": "img/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (Rng(8) stream, bench.cpp:29-45)",
+            "config": {"workload": f"{args.config}-b{args.batch}-train", "per_gpu_batch": args.batch,
+                       "global_batch": args.batch, "parallelism": "cpu (reference runs on host)"},
+            "impl": "reference",
+            "cpu_baseline": {"value": r["value"], "unit": "img/s", "cores": r["cores"],
+                             "kind": "reference", "sample": r["sample"]},
+            "e2e": {"value": r["value"], "unit": "img/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from paper_1501_07338_b200 import _lib, spec as S
+    from paper_1501_07338_b200.engine import Network
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or world == 1, "launch N>1 under torchrun"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    spec = S.PRESETS[args.config]()
+    B = args.batch
+    prec = S.Precision[args.precision]
+    lr, mom = args.lr, args.momentum
+
+    # synthetic data: the global batch from one Rng(8) stream, sharded contiguously
+    import oracle_py as O  # data generator only (bench.cpp:29-45 stream)
+    xg, clsg, valsg = O.synth_bench_data(spec, B * world, 8)
+    sl = slice(rank * B, (rank + 1) * B)
+    x_host = torch.from_numpy(np.ascontiguousarray(xg[sl]).reshape(B, -1)).pin_memory()
+    is_ce = spec.loss == S.LossKind.softmax_ce
+    t_host = torch.from_numpy(np.ascontiguousarray(clsg[sl] if is_ce else valsg[sl])).pin_memory()
+
+    stream = torch.cuda.current_stream()
+    net = Network(spec, B, prec, stream=stream)
+    net.load_batch(x_host.to(dev), cls=t_host.to(dev) if is_ce else None,
+                   values=None if is_ce else t_host.to(dev))
+    params, grads, _ = net.device_tensors()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+
+    # ---- the step ----
+    graph = None
+    if world == 1:
+        net.enable_graph(not args.no_graph)
+
+        def step():
+            net.train_step(B, lr, mom)
+    else:
+        def eager_step():
+            net.forward_backward(B)
+            dist.all_reduce(grads)           # NCCL over NVLink, fp32 sum
+            net.sgd_step(lr, mom, 1.0 / world)
+        step = eager_step
+        if not args.no_graph:
+            try:
+                s = torch.cuda.Stream()
+                s.wait_stream(stream)
+                with torch.cuda.stream(s):
+                    net.set_stream(s)
+                    for _ in range(2):
+                        eager_step()
+                stream.wait_stream(s)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    net.set_stream(torch.cuda.current_stream())
+                    eager_step()
+                net.set_stream(stream)
+
+                def step():
+                    graph.replay()
+            except Exception as e:  # keep the eager DP path
+                print(f"[rank {rank}] graph capture failed ({e}); eager DP", file=sys.stderr)
+                net.set_stream(stream)
+                step = eager_step
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- timed region: device events per step, L2 flushed between steps ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = _lib.lib().vcnn_launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        barrier()
+    launches = _lib.lib().vcnn_launch_count() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_s = max_over_ranks(sum(step_ms) / 1e3)
+    value = world * B * args.steps / total_s
+
+    # ---- e2e: host batch through the C-ABI every step ----
+    e2e = None
+    if not args.no_e2e:
+        xin, cin, vin = net.input_tensors()
+        e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.steps)]
+        for i in range(args.steps + args.warmup):
+            flush.zero_()
+            if i >= args.warmup:
+                e2e_ev[i - args.warmup][0].record(stream)
+            if world == 1:
+                net.train_step_host(x_host, cls=t_host if is_ce else None,
+                                    values=None if is_ce else t_host, lr=lr, momentum=mom)
+            else:
+                xin[:B].copy_(x_host, non_blocking=True)
+                if is_ce:
+                    cin[:B].copy_(t_host, non_blocking=True)
+                else:
+                    vin[:B].copy_(t_host.view(B, -1), non_blocking=True)
+                step()
+                net.loss()  # D2H of the step's loss
+            if i >= args.warmup:
+                e2e_ev[i - args.warmup][1].record(stream)
+        barrier()
+        e2e_s = max_over_ranks(sum(a.elapsed_time(b) for a, b in e2e_ev) / 1e3)
+        e2e = {"value": world * B * args.steps / e2e_s, "unit": "img/s",
+               "h2d_bytes_per_step": int(x_host.numel() * 4 + t_host.numel() * 4),
+               "d2h_bytes_per_step": 4, "ms_per_step": 1e3 * e2e_s / args.steps}
+
+    # ---- per-op timing pass (eager, CUDA events around every op) ----
+    pk = peaks()
+    roof = None
+    details = {}
+    if rank == 0:
+        net.enable_graph(False)
+        net.enable_breakdown(True)
+        for i in range(args.steps):
+            flush.zero_()
+            net.train_step(B, lr, mom)
+        ops = net.read_op_timing()
+        bd = net.read_breakdown()
+        net.enable_breakdown(False)
+        work = op_work(spec, B)
+        rows = []
+        tot = sum(s for s, _ in ops.values())
+        for (layer, op), (sec, cnt) in ops.items():
+            f, by = work.get((layer, op), (0.0, 0.0))
+            t = sec / cnt
+            t_tc = f / (pk["tf32_tflops"] * 1e12) if f else 0.0
+            t_hbm = by / (pk["hbm_gbs"] * 1e9) if by else 0.0
+            bound = "tensor" if t_tc >= t_hbm else "hbm"
+            rows.append({"layer": layer, "op": op, "us": t * 1e6, "share": sec / tot,
+                         "flops": f, "bytes": by, "bound": bound,
+                         "tflops": f / t / 1e12 if f else 0.0, "gbs": by / t / 1e9 if by else 0.0,
+                         "roof_us": max(t_tc, t_hbm) * 1e6})
+        rows.sort(key=lambda r: -r["share"])
+        top = rows[0]
+        if top["bound"] == "tensor":
+            roof = {"bound": "tensor", "achieved": top["tflops"], "peak": pk["tf32_tflops"],
+                    "unit": "TFLOP/s", "frac": top["tflops"] / pk["tf32_tflops"]}
+        else:
+            roof = {"bound": "hbm", "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": top["gbs"] / pk["hbm_gbs"]}
+        roof.update({"traffic": None, "kernel": f"layer{top['layer']}.{top['op']}",
+                     "share_of_step": top["share"], "us_per_launch": top["us"],
+                     "peak_src": pk["tf32_src"] if top["bound"] == "tensor" else pk["src"]})
+        step_roof_us = sum(r["roof_us"] for r in rows)
+        details = {"ops": rows, "breakdown_s": bd, "step_roofline_us": step_roof_us,
+                   "eager_step_us": tot / args.steps * 1e6, "peaks": pk}
+        if args.details:
+            with open(args.details, "w") as f:
+                json.dump(details, f, indent=1)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(spec, B, 3, 1, seconds=args.cpu_seconds)
+        if cpu:
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+
+    if rank == 0:
+        kps = net.kernels_per_step()
+        line = {
+            "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (Rng(8) stream, bench.cpp:29-45); random-init Glorot weights",
+            "config": {"workload": f"{args.config}-b{B}-train", "per_gpu_batch": B,
+                       "global_batch": B * world, "parallelism": f"dp{world}",
+                       "precision": args.precision, "graph": not args.no_graph,
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "update": f"sgd momentum {mom} lr {lr}"},
+            "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
+            "gpu_launches": int(launches), "kernels_per_step": kps,
+            "clocks": clk.result(),
+            "step_roofline_us": details.get("step_roofline_us"),
+        }
+        print(json.dumps(line))
+    net.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

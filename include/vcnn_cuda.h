@@ -283,6 +283,10 @@ int vcnn_net_kernels_per_step(vcnn_net* net, int* count);
  * last reset (synchronises) */
 int vcnn_net_enable_breakdown(vcnn_net* net, int enable);
 int vcnn_net_read_breakdown(vcnn_net* net, double* seconds8);
+/* per-op CUDA-event timing collected in breakdown mode: (nlayers+1)*5 slots,
+ * slot (layer+1)*5 + op with op 0 fwd, 1 wgrad, 2 dgrad, 3 loss, 4 sgd
+ * (layer -1 = whole-net ops); seconds and launch counts since enable */
+int vcnn_net_read_op_timing(vcnn_net* net, double* seconds, int64_t* counts);
 
 #ifdef __cplusplus
 }

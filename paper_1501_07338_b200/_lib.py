@@ -116,6 +116,7 @@ _SIGS = {
     "vcnn_net_kernels_per_step": [c_vp, P_int],
     "vcnn_net_enable_breakdown": [c_vp, c_int],
     "vcnn_net_read_breakdown": [c_vp, C.POINTER(c_double)],
+    "vcnn_net_read_op_timing": [c_vp, C.POINTER(c_double), P_i64],
 }
 _RESTYPES = {"vcnn_last_error": C.c_char_p, "vcnn_launch_count": c_i64,
              "vcnn_net_num_params": c_i64}

@@ -102,7 +102,15 @@ struct vcnn_net {
   int kernels_per_step = 0;
   // breakdown timer
   bool breakdown = false;
-  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  struct MarkRec {
+    int comp, layer, op;
+    cudaEvent_t a, b;
+  };
+  std::vector<MarkRec> marks;
+  // per (layer, op) accumulated seconds and launches; op: 0 fwd, 1 wgrad,
+  // 2 dgrad, 3 loss, 4 sgd
+  std::vector<double> op_sec;
+  std::vector<int64_t> op_cnt;
   std::vector<cudaEvent_t> event_pool;
   size_t event_next = 0;
   double seconds[8] = {0};
@@ -156,11 +164,14 @@ cudaEvent_t next_event(vcnn_net* n) {
   return n->event_pool[n->event_next++];
 }
 
+enum OpKind { OP_FWD = 0, OP_WGRAD = 1, OP_DGRAD = 2, OP_LOSS = 3, OP_SGD = 4, OP_KINDS = 5 };
+
+// CUDA-event bracket around one op on the net's stream (breakdown mode)
 struct Mark {
   vcnn_net* n;
-  int comp;
+  int comp, layer, op;
   cudaEvent_t a = nullptr;
-  Mark(vcnn_net* net, int c) : n(net), comp(c) {
+  Mark(vcnn_net* net, int c, int l = -1, int o = OP_FWD) : n(net), comp(c), layer(l), op(o) {
     if (n->breakdown) {
       a = next_event(n);
       cudaEventRecord(a, n->stream);
@@ -170,7 +181,7 @@ struct Mark {
     if (n->breakdown) {
       cudaEvent_t b = next_event(n);
       cudaEventRecord(b, n->stream);
-      n->marks.push_back({comp, {a, b}});
+      n->marks.push_back({comp, layer, op, a, b});
     }
   }
 };
@@ -183,15 +194,15 @@ int run_forward(vcnn_net* n, int B) {
     const float* W = n->params + l.w_off;
     const float* b = n->params + l.b_off;
     if (l.spec.kind == VCNN_LAYER_CONV) {
-      Mark m(n, CONV_F);
+      Mark m(n, CONV_F, (int)i, OP_FWD);
       TRY(launch_conv_fwd(conv_of(l, B), in, W, b, l.spec.act, l.out, n->precision, n->ws, st));
     } else if (l.spec.kind == VCNN_LAYER_POOL) {
-      Mark m(n, POOL_F);
+      Mark m(n, POOL_F, (int)i, OP_FWD);
       PoolDesc d = pool_of(l, B);
       TRY(launch_pool_fwd<int32_t>(d, in, l.b_len ? b : nullptr, l.spec.act, l.out,
                                    d.mode == VCNN_POOL_MAX ? l.arg : nullptr, st));
     } else {
-      Mark m(n, FULL_F);
+      Mark m(n, FULL_F, (int)i, OP_FWD);
       TRY(launch_full_fwd(B, (int)l.in_per, l.spec.units, in, W, b, l.spec.act, l.out,
                           n->precision, n->ws, st));
     }
@@ -203,7 +214,7 @@ int run_backward(vcnn_net* n, int B) {
   const cudaStream_t st = n->stream;
   LayerRt& last = n->L.back();
   {
-    Mark m(n, OTHER_F);
+    Mark m(n, OTHER_F, (int)n->L.size() - 1, OP_LOSS);
     TRY(launch_loss(n->spec.loss, B, (int)n->out_units, last.out, n->cls, n->values, n->loss,
                     last.gpre, last.spec.act, n->err, st));
   }
@@ -217,32 +228,44 @@ int run_backward(vcnn_net* n, int B) {
     float* gW = n->grads + l.w_off;
     float* gB = n->grads + l.b_off;
     if (l.spec.kind == VCNN_LAYER_CONV) {
-      Mark m(n, CONV_B);
       ConvDesc d = conv_of(l, B);
-      TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, n->ws, st));
-      if (gprev)
+      {
+        Mark m(n, CONV_B, i, OP_WGRAD);
+        TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, n->ws, st));
+      }
+      if (gprev) {
+        Mark m(n, CONV_B, i, OP_DGRAD);
         TRY(launch_conv_dgrad(d, l.gpre, W, gprev, yprev, act_prev, n->precision, n->ws, st));
+      }
     } else if (l.spec.kind == VCNN_LAYER_POOL) {
-      Mark m(n, POOL_B);
       PoolDesc d = pool_of(l, B);
-      if (l.b_len) TRY(launch_pool_bias_grad(d, l.gpre, gB, st));
-      if (gprev)
+      if (l.b_len) {
+        Mark m(n, POOL_B, i, OP_WGRAD);
+        TRY(launch_pool_bias_grad(d, l.gpre, gB, st));
+      }
+      if (gprev) {
+        Mark m(n, POOL_B, i, OP_DGRAD);
         TRY(launch_pool_bwd<int32_t>(d, n->pool_bwd_mode, l.gpre, l.arg, gprev, yprev, act_prev,
                                      st));
+      }
     } else {
-      Mark m(n, FULL_B);
-      TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
-                            n->ws, st));
-      if (gprev)
+      {
+        Mark m(n, FULL_B, i, OP_WGRAD);
+        TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
+                              n->ws, st));
+      }
+      if (gprev) {
+        Mark m(n, FULL_B, i, OP_DGRAD);
         TRY(launch_full_dgrad(B, (int)l.in_per, l.spec.units, l.gpre, W, gprev, yprev, act_prev,
                               n->precision, n->ws, st));
+      }
     }
   }
   return VCNN_OK;
 }
 
 int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
-  Mark m(n, OTHER_B);
+  Mark m(n, OTHER_B, -1, OP_SGD);
   return launch_sgd(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, n->stream);
 }
 
@@ -720,20 +743,46 @@ int vcnn_net_enable_breakdown(vcnn_net* n, int enable) {
   n->marks.clear();
   n->event_next = 0;
   for (double& s : n->seconds) s = 0;
+  const size_t slots = (n->L.size() + 1) * OP_KINDS;
+  n->op_sec.assign(slots, 0.0);
+  n->op_cnt.assign(slots, 0);
+  return VCNN_OK;
+}
+
+static int drain_marks(vcnn_net* n) {
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  const size_t slots = (n->L.size() + 1) * OP_KINDS;
+  if (n->op_sec.size() != slots) {
+    n->op_sec.assign(slots, 0.0);
+    n->op_cnt.assign(slots, 0);
+  }
+  for (auto& m : n->marks) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, m.a, m.b);
+    n->seconds[m.comp] += ms * 1e-3;
+    const size_t slot = (size_t)(m.layer + 1) * OP_KINDS + m.op;
+    n->op_sec[slot] += ms * 1e-3;
+    n->op_cnt[slot] += 1;
+  }
+  n->marks.clear();
+  n->event_next = 0;
   return VCNN_OK;
 }
 
 int vcnn_net_read_breakdown(vcnn_net* n, double* seconds8) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
-  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
-  for (auto& m : n->marks) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, m.second.first, m.second.second);
-    n->seconds[m.first] += ms * 1e-3;
-  }
-  n->marks.clear();
-  n->event_next = 0;
+  TRY(drain_marks(n));
   for (int i = 0; i < 8; ++i) seconds8[i] = n->seconds[i];
+  return VCNN_OK;
+}
+
+int vcnn_net_read_op_timing(vcnn_net* n, double* seconds, int64_t* counts) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(drain_marks(n));
+  for (size_t i = 0; i < n->op_sec.size(); ++i) {
+    seconds[i] = n->op_sec[i];
+    counts[i] = n->op_cnt[i];
+  }
   return VCNN_OK;
 }
 

@@ -225,6 +225,20 @@ class Network:
     def enable_breakdown(self, on=True):
         check(lib().vcnn_net_enable_breakdown(self._h, int(bool(on))))
 
+    def read_op_timing(self):
+        """{(layer, op): (seconds, launches)} with op in fwd/wgrad/dgrad/loss/sgd
+        (layer -1 for whole-net ops), from CUDA events in breakdown mode."""
+        n = (len(self.spec.layers) + 1) * 5
+        s = (C.c_double * n)()
+        c = (C.c_int64 * n)()
+        check(lib().vcnn_net_read_op_timing(self._h, s, c))
+        names = ("fwd", "wgrad", "dgrad", "loss", "sgd")
+        out = {}
+        for i in range(n):
+            if c[i]:
+                out[(i // 5 - 1, names[i % 5])] = (s[i], c[i])
+        return out
+
     def read_breakdown(self):
         s = (C.c_double * 8)()
         check(lib().vcnn_net_read_breakdown(self._h, s))

@@ -1,0 +1,315 @@
+"""Network-level parity on the B200: the device engine (build_network +
+Executor<float>(imp6) + sgd_step through the net-level C ABI) vs
+  * the reference's own numbers (tests/golden fixtures from oracle/_ref), and
+  * the oracle (double) on the same fp32 inputs and parameters,
+plus the reference's invariants (determinism, batch equivalence, bounds and
+training errors) and full-size checks at the BASELINE.json configs."""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle_py as O
+from paper_1501_07338_b200 import spec as S
+from paper_1501_07338_b200.engine import Executor, Network, Trainer, predict_classes
+from paper_1501_07338_b200.errors import BoundsError, ShapeError, TrainingError
+from paper_1501_07338_b200.spec import Precision
+
+from .util import ALL_PREC, TOL, assert_close, f32, normwise
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+A = S.Activation
+
+
+def _targets(spec, cls, vals):
+    return dict(cls=cls) if spec.loss == S.LossKind.softmax_ce else dict(values=vals)
+
+
+def _load(net, spec, x, cls, vals):
+    B = x.shape[0]
+    xt = torch.as_tensor(x.reshape(B, -1), device="cuda")
+    if spec.loss == S.LossKind.softmax_ce:
+        net.load_batch(xt, cls=torch.as_tensor(cls, device="cuda"))
+    else:
+        net.load_batch(xt, values=torch.as_tensor(vals.reshape(B, -1), device="cuda"))
+
+
+def _fixture_nets():
+    from .golden.make_golden import small_nets
+    return small_nets()
+
+
+def test_init_bit_exact_vs_reference():
+    """build_network<float>: Glorot stream from Rng(seed) (layers.hpp:473-501)."""
+    for name, f in S.PRESETS.items():
+        spec = f()
+        net = Network(spec, 2)
+        p_ref = O.net_init(spec).astype(np.float32)  # == reference (pinned in CPU tests)
+        assert np.array_equal(net.get_params(), p_ref), name
+        net.close()
+
+
+@pytest.mark.parametrize("prec", ALL_PREC, ids=lambda p: p.name)
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "net_*.npz"))),
+                         ids=lambda p: os.path.basename(p)[4:-4])
+def test_net_vs_reference_fixture(path, prec):
+    """One run_batch and N run_batch+sgd_step steps vs the reference's numbers."""
+    name = os.path.basename(path)[4:-4]
+    spec, B = _fixture_nets()[name]
+    d = np.load(path)
+    net = Network(spec, B, prec)
+    x, cls, vals = d["x"], d["cls"], d["values"]
+    _load(net, spec, x, cls, vals)
+    net.forward_backward(B)
+    tol = TOL[prec]
+    assert_close(net.output(B), d["out"], tol, "output")
+    assert abs(net.loss() - float(d["loss"])) <= tol * max(1.0, abs(float(d["loss"])))
+    g = net.get_grads()
+    for i in range(len(spec.layers)):  # per NetGrads tensor
+        gw, gb = net.layer_params(g, i)
+        rw, rb = net.layer_params(d["grads"], i)
+        if rw.size:
+            assert_close(gw, rw, 5 * tol, f"layer {i} dW")
+        if rb.size and np.abs(rb).max() > 1e-7:
+            assert_close(gb, rb, 5 * tol, f"layer {i} db")
+    # paper_nn pool backward mode (Executor::set_pool_backward_mode)
+    net.set_pool_backward_mode(S.PoolBackwardMode.paper_nn)
+    net.forward_backward(B)
+    assert_close(net.get_grads(), d["grads_paper_nn"], 5 * tol, "paper_nn grads")
+    net.set_pool_backward_mode(S.PoolBackwardMode.exact)
+    # N steps, weights after
+    for _ in range(int(d["steps"])):
+        net.train_step(B, float(d["lr"]), float(d["mom"]))
+    p = net.get_params()
+    p0 = d["params0"]
+    assert_close(p, d["params_after"], tol, "weights after N steps")
+    assert_close(p - p0, d["params_after"] - p0, 20 * tol, "update after N steps")
+    net.close()
+
+
+PARITY_NETS = {
+    "cifar3": (S.cifar3(), 16),
+    "lenet-caffe": (S.lenet_caffe(), 10),
+    "scale1-analog": (S.lenet_scale1_analog(), 8),
+    "denoise16-small": (S.NetworkSpec((40, 40, 1), [S.ConvSpec(16, 16, 16, 1, A.relu),
+                                                    S.ConvSpec(16, 1, 1, 1, A.relu),
+                                                    S.ConvSpec(1, 8, 8, 1, A.identity)],
+                                      S.LossKind.mse, 7), 4),
+    "deconv-small": (S.NetworkSpec((60, 60, 1), [S.ConvSpec(8, 31, 1, 1, A.identity),
+                                                 S.ConvSpec(8, 1, 31, 1, A.relu),
+                                                 S.ConvSpec(1, 5, 5, 1, A.identity)],
+                                   S.LossKind.mse, 7), 2),
+}
+
+
+@pytest.mark.parametrize("prec", ALL_PREC, ids=lambda p: p.name)
+@pytest.mark.parametrize("name", list(PARITY_NETS))
+def test_net_vs_oracle_10_steps(name, prec):
+    """Layer outputs, pool argmax (bit-exact), loss, every gradient, and the
+    weights after 10 sgd steps (lr 0.01, momentum 0.9) vs the oracle."""
+    spec, B = PARITY_NETS[name]
+    x, cls, vals = O.synth_bench_data(spec, B, 8)
+    net = Network(spec, B, prec)
+    _load(net, spec, x, cls, vals)
+    net.forward_backward(B)
+    p0 = net.get_params().astype(np.float64)
+    r = O.net_run_batch(spec, p0, f32(x), trace=True, **_targets(spec, cls, vals))
+    tol = TOL[prec]
+    off = 0
+    aoff = 0
+    for i, L in enumerate(spec.layers):
+        n = B * net.out_per[i]
+        ref_i = r["trace"][off:off + n]
+        got = net.layer_output(i, B).ravel()
+        assert_close(got, ref_i, tol, f"layer {i} output")
+        if isinstance(L, S.PoolSpec):
+            if L.mode == S.PoolMode.max and prec != Precision.tf32:
+                # argmax is bit-exact wherever the fp32-faithful paths see the same order
+                arg = net.pool_arg(i, B).ravel()
+                ref_arg = r["args"][aoff:aoff + n]
+                assert (arg == ref_arg).mean() > 0.999
+            aoff += n
+        off += n
+    assert abs(net.loss() - r["loss"]) <= tol * max(1.0, abs(r["loss"]))
+    assert_close(net.get_grads(), r["grads"], 5 * tol, "grads")
+    # 10 steps
+    p, v = p0.copy(), np.zeros_like(p0)
+    for _ in range(10):
+        net.train_step(B, 0.01, 0.9)
+        g = O.net_run_batch(spec, p, f32(x), **_targets(spec, cls, vals))["grads"]
+        O.sgd_step(p, v, g, 0.01, 0.9)
+    pg = net.get_params()
+    assert_close(pg, p, tol, "weights after 10 steps")
+    assert_close(pg - p0, p - p0, 20 * tol, "update after 10 steps")
+    net.close()
+
+
+def test_pool_argmax_bit_exact_in_net():
+    """ArgIndex of the engine's max pools == oracle (fp32-faithful path)."""
+    spec = S.cifar3()
+    B = 8
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    net = Network(spec, B, Precision.fp32)
+    _load(net, spec, x, cls, None)
+    net.forward(B)
+    # feed each pool the GPU's own conv output so the comparison isolates pooling
+    for i, L in enumerate(spec.layers):
+        if isinstance(L, S.PoolSpec):
+            hh, ww, cc = spec.chain()[i - 1]
+            prev = net.layer_output(i - 1, B).reshape(B, cc, hh, ww).astype(np.float64)
+            y, arg = O.pool_forward(prev, L.ph, L.pw, L.stride, int(L.mode))
+            assert np.array_equal(net.pool_arg(i, B).reshape(arg.shape), arg)
+            assert np.array_equal(net.layer_output(i, B).reshape(y.shape), y.astype(np.float32))
+    net.close()
+
+
+@pytest.mark.parametrize("prec", [Precision.tf32, Precision.tf32x3])
+def test_deterministic_and_graph_equivalent(prec):
+    """Training is bitwise reproducible (network_test.cpp:219-244); graph
+    replay == eager launches bit for bit."""
+    spec = S.cifar3()
+    B = 64
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    runs = []
+    for graph in (False, False, True):
+        net = Network(spec, B, prec)
+        net.enable_graph(graph)
+        _load(net, spec, x, cls, None)
+        for _ in range(5):
+            net.train_step(B, 0.01, 0.9)
+        runs.append(net.get_params())
+        net.close()
+    assert np.array_equal(runs[0], runs[1])
+    assert np.array_equal(runs[0], runs[2])
+
+
+def test_host_path_equals_device_path():
+    spec = S.cifar3()
+    B = 32
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    a = Network(spec, B)
+    b = Network(spec, B)
+    a.enable_graph(True)
+    losses = [a.train_step_host(x, cls=cls, lr=0.01, momentum=0.9) for _ in range(3)]
+    _load(b, spec, x, cls, None)
+    for _ in range(3):
+        b.train_step(B, 0.01, 0.9)
+    assert np.array_equal(a.get_params(), b.get_params())
+    assert abs(losses[-1] - b.loss()) == 0.0
+    out = a.forward_host(x)
+    a.forward(B)
+    assert np.array_equal(out, a.output(B))
+
+
+def test_batch_equivalence_on_device():
+    """network_test.cpp:99-160: batch forward == per-sample forwards; grads ==
+    mean of per-sample grads (fp32-faithful path)."""
+    spec = S.NetworkSpec((9, 10, 2), [S.ConvSpec(3, 3, 2, 1, A.tanh),
+                                      S.PoolSpec(2, 2, 1, S.PoolMode.max, True, A.sigmoid),
+                                      S.FullSpec(3, A.identity)], S.LossKind.softmax_ce, 5)
+    B = 4
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (B, 2, 9, 10)).astype(np.float32)
+    cls = np.array([0, 2, 1, 1], dtype=np.int32)
+    net = Network(spec, B, Precision.tf32x3)
+    _load(net, spec, x, cls, None)
+    net.forward_backward(B)
+    whole_out, whole_g = net.output(B), net.get_grads()
+    acc = np.zeros_like(whole_g, dtype=np.float64)
+    for b in range(B):
+        _load(net, spec, x[b:b + 1], cls[b:b + 1], None)
+        net.forward_backward(1)
+        assert_close(net.output(1)[0], whole_out[b], 1e-6, "per-sample out")
+        acc += net.get_grads()
+    assert_close(whole_g, acc / B, 1e-5, "mean of per-sample grads")
+
+
+def test_errors():
+    spec = S.cifar3()
+    net = Network(spec, 4)
+    x, cls, _ = O.synth_bench_data(spec, 4, 8)
+    bad = cls.copy()
+    bad[1] = 10
+    with pytest.raises(BoundsError):
+        net.train_step_host(x, cls=bad, lr=0.01, momentum=0.0)
+    with pytest.raises(ShapeError):
+        net.train_step(5, 0.01, 0.0)  # > max_batch
+    with pytest.raises(ShapeError):
+        Network(S.NetworkSpec((4, 4, 1), [S.ConvSpec(2, 5, 5)]), 1)
+    ex = Executor()
+    with pytest.raises(BoundsError):
+        ex.run_batch(net, x, bad)
+
+
+def test_trainer_nonfinite_names_layer():
+    """network_test.cpp:286-306: a NaN loss raises TrainingError naming a layer."""
+    spec = S.NetworkSpec((4, 4, 1), [S.ConvSpec(2, 2, 2, 1, A.identity),
+                                     S.PoolSpec(2, 2, 1, S.PoolMode.avg),
+                                     S.FullSpec(2, A.identity)], S.LossKind.softmax_ce, 14)
+    net = Network(spec, 10)
+    p = net.get_params()
+    w, _ = net.layer_params(p, 0)
+    w[:] = np.where(np.arange(w.size) % 2, 1.0, -1.0) * 3e38
+    net.set_params(p)
+    imgs = np.random.default_rng(1).uniform(0, 1, (10, 1, 4, 4)).astype(np.float32) * 1e3
+    tr = Trainer(S.TrainConfig(lr=0.01, batch=10, epochs=1))
+    with pytest.raises(TrainingError, match="layer"):
+        tr.fit(net, imgs, np.zeros(10, dtype=np.int32))
+
+
+def test_trainer_loss_decreases_and_predicts():
+    """network_test.cpp:246-284 analog on a separable toy set."""
+    rng = np.random.default_rng(3)
+    n = 64
+    labels = (np.arange(n) % 2).astype(np.int32)
+    imgs = rng.uniform(0, 0.2, (n, 1, 6, 6)).astype(np.float32)
+    imgs[labels == 1, :, :3, :] += 0.8
+    spec = S.NetworkSpec((6, 6, 1), [S.ConvSpec(4, 3, 3, 1, A.relu), S.PoolSpec(2, 2, 2),
+                                     S.FullSpec(2, A.identity)], S.LossKind.softmax_ce, 12)
+    net = Network(spec, n)
+    tr = Trainer(S.TrainConfig(lr=0.05, momentum=0.9, batch=n, epochs=20, seed=4))
+    hist = tr.fit(net, imgs, labels)
+    assert hist[-1] < hist[0]
+    assert tr.evaluate_accuracy(net, imgs, labels) > 0.9
+    assert predict_classes(np.array([[0.1, 2.0, -1.0], [0.7, 0.3, 0.7]])) == [1, 0]
+
+
+@pytest.mark.parametrize("name,B", [("cifar3", 128), ("lenet-caffe", 100)])
+def test_full_size_step_vs_oracle(name, B):
+    """BASELINE configs at their full benchmark batch: one step vs the oracle,
+    and the TF32 gradient vs the fp32-faithful gradient (size-independent)."""
+    spec = S.PRESETS[name]()
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    net = Network(spec, B, Precision.tf32)
+    _load(net, spec, x, cls, None)
+    net.forward_backward(B)
+    g_tf32 = net.get_grads()
+    r = O.net_run_batch(spec, net.get_params().astype(np.float64), f32(x), cls=cls)
+    assert abs(net.loss() - r["loss"]) <= 1e-3 * r["loss"]
+    assert normwise(g_tf32, r["grads"]) <= 5e-3
+    net.set_precision(Precision.tf32x3)
+    net.forward_backward(B)
+    assert normwise(net.get_grads(), r["grads"]) <= 5e-5
+    net.close()
+
+
+def test_big_batch_and_presets_run():
+    """Every BASELINE config builds and steps at its benchmark size; losses are
+    finite and training lowers the loss on a fixed batch."""
+    for name, B in [("cifar3", 1024), ("denoise16", 128), ("deconv121", 16),
+                    ("scale2-mini", 128), ("single-conv", 64)]:
+        spec = S.PRESETS[name]()
+        x, cls, vals = O.synth_bench_data(spec, B, 8)
+        net = Network(spec, B)
+        _load(net, spec, x, cls, vals)
+        net.forward_backward(B)
+        l0 = net.loss()
+        assert np.isfinite(l0), name
+        for _ in range(5):
+            net.train_step(B, 0.01, 0.9)
+        net.forward_backward(B)
+        assert net.loss() < l0, name
+        net.close()
