@@ -274,6 +274,9 @@ int vcnn_net_enable_graph(vcnn_net* net, int enable);
 int vcnn_net_get_loss(vcnn_net* net, float* loss);
 int vcnn_net_get_output(vcnn_net* net, float* host);
 int vcnn_net_get_layer_output(vcnn_net* net, int layer, float* host);
+/* gradient w.r.t. the PRE-activation of a layer (dY * act'(Y)) from the
+ * last backward pass, [max_batch][out_per_sample] */
+int vcnn_net_get_layer_grad(vcnn_net* net, int layer, float* host);
 /* pool argmax of a max-pool layer as int64 global input indices */
 int vcnn_net_get_pool_arg(vcnn_net* net, int layer, int64_t* host);
 /* kernels per train step (fwd+bwd+sgd) at the current settings */

@@ -113,6 +113,7 @@ _SIGS = {
     "vcnn_net_get_output": [c_vp, c_vp],
     "vcnn_net_get_layer_output": [c_vp, c_int, c_vp],
     "vcnn_net_get_pool_arg": [c_vp, c_int, c_vp],
+    "vcnn_net_get_layer_grad": [c_vp, c_int, c_vp],
     "vcnn_net_kernels_per_step": [c_vp, P_int],
     "vcnn_net_enable_breakdown": [c_vp, c_int],
     "vcnn_net_read_breakdown": [c_vp, C.POINTER(c_double)],

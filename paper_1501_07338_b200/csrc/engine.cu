@@ -97,6 +97,7 @@ struct vcnn_net {
   // graph replay
   bool use_graph = false;
   cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;  // capture needs a non-legacy stream
   int g_batch = -1;
   float g_lr = 0, g_mom = 0;
   int kernels_per_step = 0;
@@ -303,10 +304,18 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
   if (!n->use_graph || n->breakdown) return eager_step(n, batch, lr, mom);
   if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom) {
     drop_graph(n);
+    if (!n->cap_stream)
+      VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&n->cap_stream, cudaStreamNonBlocking));
+    // capture on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); the graph is launched on the caller's
     cudaGraph_t g = nullptr;
-    VCNN_CUDA_TRY(cudaStreamBeginCapture(n->stream, cudaStreamCaptureModeRelaxed));
+    cudaStream_t user = n->stream;
+    VCNN_CUDA_TRY(cudaStreamSynchronize(user));
+    VCNN_CUDA_TRY(cudaStreamBeginCapture(n->cap_stream, cudaStreamCaptureModeRelaxed));
+    n->stream = n->cap_stream;
     int s = eager_step(n, batch, lr, mom);
-    cudaError_t e = cudaStreamEndCapture(n->stream, &g);
+    n->stream = user;
+    cudaError_t e = cudaStreamEndCapture(n->cap_stream, &g);
     if (s) {
       if (g) cudaGraphDestroy(g);
       return s;
@@ -535,6 +544,7 @@ int vcnn_net_destroy(vcnn_net* n) {
   cudaFree(n->loss);
   cudaFree(n->err);
   cudaFree(n->ws.ptr);
+  if (n->cap_stream) cudaStreamDestroy(n->cap_stream);
   for (cudaEvent_t e : n->event_pool) cudaEventDestroy(e);
   delete n;
   return VCNN_OK;
@@ -717,6 +727,13 @@ int vcnn_net_get_layer_output(vcnn_net* n, int layer, float* host) {
     return fail(VCNN_EBOUNDS, "layer index out of range");
   const LayerRt& l = n->L[layer];
   return copy_out(n, host, l.out, sizeof(float) * l.out_per * n->max_batch);
+}
+
+int vcnn_net_get_layer_grad(vcnn_net* n, int layer, float* host) {
+  if (!n || layer < 0 || layer >= (int)n->L.size())
+    return fail(VCNN_EBOUNDS, "layer index out of range");
+  const LayerRt& l = n->L[layer];
+  return copy_out(n, host, l.gpre, sizeof(float) * l.out_per * n->max_batch);
 }
 
 int vcnn_net_get_pool_arg(vcnn_net* n, int layer, int64_t* host) {

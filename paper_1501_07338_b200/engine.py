@@ -212,6 +212,12 @@ class Network:
         check(lib().vcnn_net_get_layer_output(self._h, i, out.ctypes.data_as(C.c_void_p)))
         return out[: (batch or self.max_batch)]
 
+    def layer_grad(self, i, batch=None):
+        """Gradient w.r.t. layer i's pre-activation from the last backward pass."""
+        out = np.empty((self.max_batch, self.out_per[i]), dtype=np.float32)
+        check(lib().vcnn_net_get_layer_grad(self._h, i, out.ctypes.data_as(C.c_void_p)))
+        return out[: (batch or self.max_batch)]
+
     def pool_arg(self, i, batch=None):
         out = np.empty((self.max_batch, self.out_per[i]), dtype=np.int64)
         check(lib().vcnn_net_get_pool_arg(self._h, i, out.ctypes.data_as(C.c_void_p)))

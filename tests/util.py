@@ -3,10 +3,15 @@ import numpy as np
 
 from paper_1501_07338_b200.spec import Precision
 
-# Tolerances (north_star): normwise max|gpu-ref| / max|ref|.
-#   TF32 (tcgen05 kind::tf32, fp32 accumulate)       1e-3
-#   3xTF32 (split hi/lo, fp32-faithful) and FP32 SIMT 1e-5
-TOL = {Precision.tf32: 1e-3, Precision.tf32x3: 1e-5, Precision.fp32: 1e-5}
+# Tolerances (north_star), normwise max|gpu-ref| / max|ref| per tensor:
+#   TF32   (tcgen05 kind::tf32, fp32 accumulate in TMEM)          1e-3
+#   3xTF32 (hi/lo split, 3 tcgen05 MMAs, fp32 accumulate in TMEM) 5e-5
+#   FP32   (SIMT FMA, the fp32-faithful path)                     1e-5
+# Whole-network TF32 gradients are additionally checked "teacher-forced"
+# (every layer fed the GPU's own trace), because TF32 rounding legitimately
+# flips near-tied max-pool argmaxes / ReLU kinks -- the cases the reference's
+# own fd_safe() (tests/helpers.hpp:148-203) excludes from its gradient checks.
+TOL = {Precision.tf32: 1e-3, Precision.tf32x3: 5e-5, Precision.fp32: 1e-5}
 ALL_PREC = [Precision.tf32, Precision.tf32x3, Precision.fp32]
 
 
@@ -27,3 +32,27 @@ def assert_close(gpu, ref, tol, what=""):
 def f32(a):
     """Round to fp32 (the GPU's input precision), returned as float64 for the oracle."""
     return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def act_np(act, x):
+    """layers.hpp:25-34 in numpy."""
+    act = int(act)
+    if act == 1:
+        return np.where(x > 0, x, 0.0)
+    if act == 2:
+        return 1.0 / (1.0 + np.exp(-x))
+    if act == 3:
+        return np.tanh(x)
+    return x
+
+
+def act_grad_np(act, y):
+    """layers.hpp:39-48 in numpy (derivative from the output)."""
+    act = int(act)
+    if act == 1:
+        return (y > 0).astype(np.float64)
+    if act == 2:
+        return y * (1 - y)
+    if act == 3:
+        return 1 - y * y
+    return np.ones_like(y)
