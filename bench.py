@@ -6,7 +6,8 @@ batch 128 per GPU, data-parallel over N GPUs, weak scaling).
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 One JSON line on rank 0 (driver contract).  `value` is device-timed with CUDA
-events per step (L2 flushed between steps), max over ranks; `e2e` is the same
+events per step (each step reads a different batch from a device pool larger
+than L2), max over ranks; `e2e` is the same
 metric through the C-ABI host entry point (pinned host batch -> H2D -> step ->
 D2H loss every step); `roofline` is the dominant kernel's achieved rate over
 the timed breakdown pass; `cpu_baseline` is the reference compiled from its
@@ -24,7 +25,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "train images/sec (fwd+bwd+update)"
-L2_FLUSH_BYTES = 256 << 20
+POOL_BYTES = 256 << 20  # input pool > 126 MB L2: every step's batch comes from HBM
 
 
 def parse():
@@ -251,7 +252,20 @@ def main():
     net.load_batch(x_host.to(dev), cls=t_host.to(dev) if is_ce else None,
                    values=None if is_ce else t_host.to(dev))
     params, grads, _ = net.device_tensors()
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    # device input pool larger than L2, cycled one batch per step (the D2D
+    # staging copy into the net's input slot is inside the timed step)
+    nbatch = max(2, -(-POOL_BYTES // (x_host.numel() * 4)))
+    xp, cp, vp = O.synth_bench_data(spec, B * nbatch, 9 + rank)
+    pool_x = torch.from_numpy(xp.reshape(nbatch, B, -1)).to(dev)
+    pool_t = torch.from_numpy((cp.reshape(nbatch, B) if is_ce else vp.reshape(nbatch, B, -1))).to(dev)
+    del xp, cp, vp
+
+    def load(i):
+        j = i % nbatch
+        if is_ce:
+            net.load_batch(pool_x[j], cls=pool_t[j])
+        else:
+            net.load_batch(pool_x[j], values=pool_t[j])
 
     # ---- the step ----
     graph = None
@@ -301,19 +315,20 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for _ in range(args.warmup):
+    for i in range(args.warmup):
+        load(i)
         step()
     barrier()
 
-    # ---- timed region: device events per step, L2 flushed between steps ----
+    # ---- timed region: device events per step, a fresh batch from HBM each ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches0 = _lib.lib().vcnn_launch_count()
     with ClockSampler(local) as clk:
         barrier()
         for i in range(args.steps):
-            flush.zero_()
             ev[i][0].record(stream)
+            load(args.warmup + i)
             step()
             ev[i][1].record(stream)
         barrier()
@@ -329,7 +344,6 @@ def main():
         e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                   for _ in range(args.steps)]
         for i in range(args.steps + args.warmup):
-            flush.zero_()
             if i >= args.warmup:
                 e2e_ev[i - args.warmup][0].record(stream)
             if world == 1:
@@ -359,7 +373,7 @@ def main():
         net.enable_graph(False)
         net.enable_breakdown(True)
         for i in range(args.steps):
-            flush.zero_()
+            load(i)
             net.train_step(B, lr, mom)
         ops = net.read_op_timing()
         bd = net.read_breakdown()
@@ -412,7 +426,9 @@ def main():
             "config": {"workload": f"{args.config}-b{B}-train", "per_gpu_batch": B,
                        "global_batch": B * world, "parallelism": f"dp{world}",
                        "precision": args.precision, "graph": not args.no_graph,
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "l2": f"inputs > L2: {nbatch} distinct batches cycled from a "
+                             f"{nbatch * x_host.numel() * 4 >> 20} MiB device pool, D2D staging "
+                             "copy inside each timed step",
                        "update": f"sgd momentum {mom} lr {lr}"},
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "kernels_per_step": kps,

@@ -83,6 +83,13 @@ struct Scratch {
     if (_s) return _s;    \
   } while (0)
 
+// stream-ordered scratch for the GEMM launchers (split-K partials, dP)
+#define WORKSPACE(var, bytes_expr)                                   \
+  Scratch var##_s(st);                                               \
+  const size_t var##_b = (bytes_expr);                               \
+  TRY(var##_s.alloc(var##_b));                                       \
+  Workspace var{static_cast<float*>(var##_s.p), var##_b}
+
 }  // namespace
 
 extern "C" {
@@ -164,7 +171,9 @@ int vcnn_matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b,
     VCNN_CUDA_TRY(cudaMemsetAsync(c, 0, sizeof(float) * m * n, as_stream(stream)));
     return VCNN_OK;
   }
-  return launch_matmul(m, k, n, a, b, c, false, precision, Workspace{}, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  WORKSPACE(ws, matmul_workspace(m, k, n, precision));
+  return launch_matmul(m, k, n, a, b, c, false, precision, ws, st);
 }
 
 int vcnn_matmul_transB(int64_t m, int64_t k, int64_t n, const float* a, const float* b,
@@ -177,7 +186,9 @@ int vcnn_matmul_transB(int64_t m, int64_t k, int64_t n, const float* a, const fl
     VCNN_CUDA_TRY(cudaMemsetAsync(c, 0, sizeof(float) * m * n, as_stream(stream)));
     return VCNN_OK;
   }
-  return launch_matmul(m, k, n, a, b, c, true, precision, Workspace{}, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  WORKSPACE(ws, matmul_workspace(m, k, n, precision));
+  return launch_matmul(m, k, n, a, b, c, true, precision, ws, st);
 }
 
 int vcnn_accumulate_by_index(const float* values, int64_t source_len, const int64_t* source,
@@ -277,7 +288,9 @@ int vcnn_conv_forward(const vcnn_conv_geometry* g, int maps, const float* x, con
   TRY(check_prec(precision));
   TRY(check_act(act));
   TRY(require_device());
-  return launch_conv_fwd(d, x, w, bias, act, y, precision, Workspace{}, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  WORKSPACE(ws, conv_workspace(d, precision));
+  return launch_conv_fwd(d, x, w, bias, act, y, precision, ws, st);
 }
 
 int vcnn_conv_backward(const vcnn_conv_geometry* g, int maps, const float* x, const float* w,
@@ -290,18 +303,16 @@ int vcnn_conv_backward(const vcnn_conv_geometry* g, int maps, const float* x, co
   TRY(require_device());
   cudaStream_t st = as_stream(stream);
   // gpre = dy * act'(y)  (conv_backward, layers.hpp:186-187)
-  Scratch gp(st), ws(st);
+  Scratch gp(st);
   const float* gpre = dy;
   if (act != VCNN_ACT_IDENTITY) {
     TRY(gp.alloc(sizeof(float) * d.out_size()));
     TRY(launch_act_bwd(d.out_size(), act, y, dy, static_cast<float*>(gp.p), st));
     gpre = static_cast<float*>(gp.p);
   }
-  const size_t wsb = conv_wgrad_workspace(d, precision);
-  TRY(ws.alloc(wsb));
-  Workspace w_s{static_cast<float*>(ws.p), wsb};
-  TRY(launch_conv_wgrad(d, x, gpre, dw, db, precision, w_s, st));
-  if (dx) TRY(launch_conv_dgrad(d, gpre, w, dx, nullptr, VCNN_ACT_IDENTITY, precision, w_s, st));
+  WORKSPACE(ws, conv_workspace(d, precision));
+  TRY(launch_conv_wgrad(d, x, gpre, dw, db, precision, ws, st));
+  if (dx) TRY(launch_conv_dgrad(d, gpre, w, dx, nullptr, VCNN_ACT_IDENTITY, precision, ws, st));
   return VCNN_OK;
 }
 
@@ -312,8 +323,9 @@ int vcnn_full_forward(int batch, int in_units, int out_units, const float* x, co
   TRY(check_prec(precision));
   TRY(check_act(act));
   TRY(require_device());
-  return launch_full_fwd(batch, in_units, out_units, x, w, bias, act, y, precision, Workspace{},
-                         as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  WORKSPACE(ws, full_workspace(batch, in_units, out_units, precision));
+  return launch_full_fwd(batch, in_units, out_units, x, w, bias, act, y, precision, ws, st);
 }
 
 int vcnn_full_backward(int batch, int in_units, int out_units, const float* x, const float* w,
@@ -333,10 +345,11 @@ int vcnn_full_backward(int batch, int in_units, int out_units, const float* x, c
     TRY(launch_act_bwd(n, act, y, dy, static_cast<float*>(gp.p), st));
     gpre = static_cast<float*>(gp.p);
   }
-  TRY(launch_full_wgrad(batch, in_units, out_units, x, gpre, dw, db, precision, Workspace{}, st));
+  WORKSPACE(ws, full_workspace(batch, in_units, out_units, precision));
+  TRY(launch_full_wgrad(batch, in_units, out_units, x, gpre, dw, db, precision, ws, st));
   if (dx)
     TRY(launch_full_dgrad(batch, in_units, out_units, gpre, w, dx, nullptr, VCNN_ACT_IDENTITY,
-                          precision, Workspace{}, st));
+                          precision, ws, st));
   return VCNN_OK;
 }
 

@@ -59,16 +59,22 @@ int sm_count() {
   return g_sm_count > 0 ? g_sm_count : 148;
 }
 
-size_t conv_wgrad_workspace(const ConvDesc& d, int prec) {
-  return prec == VCNN_PREC_FP32 ? 0 : tc::conv_wgrad_workspace(d);
+size_t conv_workspace(const ConvDesc& d, int prec) {
+  return prec == VCNN_PREC_FP32 ? 0 : tc::conv_workspace(d);
 }
 
-size_t full_wgrad_workspace(int, int, int, int) { return 0; }
+size_t full_workspace(int B, int in, int out, int prec) {
+  return prec == VCNN_PREC_FP32 ? 0 : tc::full_workspace(B, in, out);
+}
+
+size_t matmul_workspace(int64_t m, int64_t k, int64_t n, int prec) {
+  return prec == VCNN_PREC_FP32 ? 0 : tc::matmul_workspace(m, k, n);
+}
 
 int launch_conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
-                    float* y, int prec, const Workspace&, cudaStream_t st) {
+                    float* y, int prec, const Workspace& ws, cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::conv_fwd(d, x, w, b, act, y, st);
-  return tc::conv_fwd(d, x, w, b, act, y, prec == VCNN_PREC_3XTF32, st);
+  return tc::conv_fwd(d, x, w, b, act, y, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw,
@@ -78,35 +84,36 @@ int launch_conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, floa
 }
 
 int launch_conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
-                      const float* yprev, int act_prev, int prec, const Workspace&,
+                      const float* yprev, int act_prev, int prec, const Workspace& ws,
                       cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::conv_dgrad(d, gpre, w, dx, yprev, act_prev, st);
-  return tc::conv_dgrad(d, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, st);
+  return tc::conv_dgrad(d, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_full_fwd(int B, int in, int out, const float* x, const float* w, const float* b,
-                    int act, float* y, int prec, const Workspace&, cudaStream_t st) {
+                    int act, float* y, int prec, const Workspace& ws, cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::full_fwd(B, in, out, x, w, b, act, y, st);
-  return tc::full_fwd(B, in, out, x, w, b, act, y, prec == VCNN_PREC_3XTF32, st);
+  return tc::full_fwd(B, in, out, x, w, b, act, y, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw,
-                      float* db, int prec, const Workspace&, cudaStream_t st) {
+                      float* db, int prec, const Workspace& ws, cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::full_wgrad(B, in, out, x, gpre, dw, db, st);
-  return tc::full_wgrad(B, in, out, x, gpre, dw, db, prec == VCNN_PREC_3XTF32, st);
+  return tc::full_wgrad(B, in, out, x, gpre, dw, db, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
-                      const float* yprev, int act_prev, int prec, const Workspace&,
+                      const float* yprev, int act_prev, int prec, const Workspace& ws,
                       cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::full_dgrad(B, in, out, gpre, w, dx, yprev, act_prev, st);
-  return tc::full_dgrad(B, in, out, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, st);
+  return tc::full_dgrad(B, in, out, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, ws,
+                        st);
 }
 
 int launch_matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
-                  bool transB, int prec, const Workspace&, cudaStream_t st) {
+                  bool transB, int prec, const Workspace& ws, cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::matmul(m, k, n, a, b, c, transB, st);
-  return tc::matmul(m, k, n, a, b, c, transB, prec == VCNN_PREC_3XTF32, st);
+  return tc::matmul(m, k, n, a, b, c, transB, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 }  // namespace vcnn_b200

@@ -496,11 +496,15 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
     s = s ? s : dalloc((void**)&l.gpre, ob);
     if (l.spec.kind == VCNN_LAYER_POOL && l.spec.pool_mode == VCNN_POOL_MAX)
       s = s ? s : dalloc((void**)&l.arg, sizeof(int32_t) * (size_t)(l.out_per * max_batch));
-    if (l.spec.kind == VCNN_LAYER_CONV) {
-      for (int prec = VCNN_PREC_TF32; prec <= VCNN_PREC_FP32; ++prec) {
-        const size_t need = conv_wgrad_workspace(conv_of(l, max_batch), prec);
-        if (need > wsb) wsb = need;
-      }
+    // scratch (split-K partials, explicit-dgrad dP) for every batch size the
+    // net may run -- the split plan depends on the batch
+    for (int B = 1; B <= max_batch; ++B) {
+      size_t need = 0;
+      if (l.spec.kind == VCNN_LAYER_CONV)
+        need = conv_workspace(conv_of(l, B), VCNN_PREC_TF32);
+      else if (l.spec.kind == VCNN_LAYER_FULL)
+        need = full_workspace(B, (int)l.in_per, l.spec.units, VCNN_PREC_TF32);
+      if (need > wsb) wsb = need;
     }
   }
   if (wsb) {

@@ -39,7 +39,9 @@ struct Workspace {
 
 // ---- memory-bound kernels (simt.cu) ----
 int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st);
-int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st);
+// dX = col2im(dP) [* act_prev'(yprev)]
+int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st,
+                  const float* yprev = nullptr, int act_prev = VCNN_ACT_IDENTITY);
 int launch_col2im_map(const ConvDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st);
 int launch_pool_map(const PoolDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st);
 template <class IdxT>
@@ -87,8 +89,9 @@ int launch_matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* 
                   bool transB, int prec, const Workspace& ws, cudaStream_t st);
 
 // workspace bytes the GEMM launchers need for a shape (0 if none)
-size_t conv_wgrad_workspace(const ConvDesc& d, int prec);
-size_t full_wgrad_workspace(int B, int in, int out, int prec);
+size_t conv_workspace(const ConvDesc& d, int prec);
+size_t full_workspace(int B, int in, int out, int prec);
+size_t matmul_workspace(int64_t m, int64_t k, int64_t n, int prec);
 
 // ---- SIMT implementations (simt.cu) used for VCNN_PREC_FP32 ----
 namespace simt {
@@ -111,20 +114,25 @@ int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, floa
 // ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----
 namespace tc {
 int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
-             float* y, bool split3, cudaStream_t st);
+             float* y, bool split3, const Workspace& ws, cudaStream_t st);
 int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
                bool split3, const Workspace& ws, cudaStream_t st);
 int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
-               const float* yprev, int act_prev, bool split3, cudaStream_t st);
+               const float* yprev, int act_prev, bool split3, const Workspace& ws,
+               cudaStream_t st);
 int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
-             float* y, bool split3, cudaStream_t st);
+             float* y, bool split3, const Workspace& ws, cudaStream_t st);
 int full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw, float* db,
-               bool split3, cudaStream_t st);
+               bool split3, const Workspace& ws, cudaStream_t st);
 int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
-               const float* yprev, int act_prev, bool split3, cudaStream_t st);
+               const float* yprev, int act_prev, bool split3, const Workspace& ws,
+               cudaStream_t st);
 int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
-           bool transB, bool split3, cudaStream_t st);
-size_t conv_wgrad_workspace(const ConvDesc& d);
+           bool transB, bool split3, const Workspace& ws, cudaStream_t st);
+// scratch the launchers above need (split-K partials, explicit-dgrad dP)
+size_t conv_workspace(const ConvDesc& d);
+size_t full_workspace(int B, int in, int out);
+size_t matmul_workspace(int64_t m, int64_t k, int64_t n);
 }  // namespace tc
 
 }  // namespace vcnn_b200

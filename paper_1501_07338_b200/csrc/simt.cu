@@ -59,7 +59,8 @@ __global__ void im2col_kernel(ConvDesc d, const float* __restrict__ x, float* __
 // patch cells it fed in (ky,kx) ascending order -- the same per-cell order
 // as the reference's pair-ordered scatter (build_col2im_map enumerates
 // c,ky,kx,b,oy,ox), so results are bit-identical to a sequential scatter.
-__global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* __restrict__ dX) {
+__global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* __restrict__ dX,
+                              const float* __restrict__ yprev, int act_prev) {
   const int64_t cols = d.pixels();
   const int64_t total = d.in_size();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -83,6 +84,7 @@ __global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* _
         acc += dP[row * cols + b * d.ohw() + (int64_t)oy * d.OW + ox];
       }
     }
+    if (yprev) acc *= act_grad_from_out(act_prev, yprev[i]);
     dX[i] = acc;
   }
 }
@@ -541,8 +543,9 @@ int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st) 
   return VCNN_OK;
 }
 
-int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st) {
-  col2im_kernel<<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX);
+int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st,
+                  const float* yprev, int act_prev) {
+  col2im_kernel<<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX, yprev, act_prev);
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
