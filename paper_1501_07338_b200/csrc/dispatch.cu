@@ -90,22 +90,31 @@ int launch_conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, floa
   return tc::conv_dgrad(d, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
+// GEMMs below this many MACs run on the SIMT path in every precision mode:
+// a 128x10x64 FC layer is ~80K MACs -- far below one tcgen05 tile's worth of
+// work, where a tensor-core launch only adds TMEM / barrier setup latency.
+constexpr int64_t kTinyGemmMacs = 1 << 20;
+inline bool tiny(int64_t m, int64_t n, int64_t k) { return m * n * k < kTinyGemmMacs; }
+
 int launch_full_fwd(int B, int in, int out, const float* x, const float* w, const float* b,
                     int act, float* y, int prec, const Workspace& ws, cudaStream_t st) {
-  if (prec == VCNN_PREC_FP32) return simt::full_fwd(B, in, out, x, w, b, act, y, st);
+  if (prec == VCNN_PREC_FP32 || tiny(B, out, in))
+    return simt::full_fwd(B, in, out, x, w, b, act, y, st);
   return tc::full_fwd(B, in, out, x, w, b, act, y, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw,
                       float* db, int prec, const Workspace& ws, cudaStream_t st) {
-  if (prec == VCNN_PREC_FP32) return simt::full_wgrad(B, in, out, x, gpre, dw, db, st);
+  if (prec == VCNN_PREC_FP32 || tiny(out, in, B))
+    return simt::full_wgrad(B, in, out, x, gpre, dw, db, st);
   return tc::full_wgrad(B, in, out, x, gpre, dw, db, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
                       const float* yprev, int act_prev, int prec, const Workspace& ws,
                       cudaStream_t st) {
-  if (prec == VCNN_PREC_FP32) return simt::full_dgrad(B, in, out, gpre, w, dx, yprev, act_prev, st);
+  if (prec == VCNN_PREC_FP32 || tiny(B, in, out))
+    return simt::full_dgrad(B, in, out, gpre, w, dx, yprev, act_prev, st);
   return tc::full_dgrad(B, in, out, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, ws,
                         st);
 }

@@ -21,6 +21,8 @@ inline unsigned grid_for(int64_t n, int threads = kThreads) {
   return (unsigned)(g < 1 ? 1 : g);
 }
 
+inline bool fits32(int64_t v) { return v < (int64_t(1) << 31) - 1; }
+
 // fixed-order block tree reduction (deterministic for a fixed blockDim)
 template <int NT>
 __device__ __forceinline__ float block_sum(float v, float* sh) {
@@ -59,29 +61,34 @@ __global__ void im2col_kernel(ConvDesc d, const float* __restrict__ x, float* __
 // patch cells it fed in (ky,kx) ascending order -- the same per-cell order
 // as the reference's pair-ordered scatter (build_col2im_map enumerates
 // c,ky,kx,b,oy,ox), so results are bit-identical to a sequential scatter.
+template <class I>
 __global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* __restrict__ dX,
                               const float* __restrict__ yprev, int act_prev) {
-  const int64_t cols = d.pixels();
-  const int64_t total = d.in_size();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const I cols = (I)d.pixels();
+  const I total = (I)d.in_size();
+  const I ohw = (I)d.ohw();
+  for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
     const int x = (int)(i % d.W);
-    const int y = (int)((i / d.W) % d.H);
-    const int c = (int)((i / ((int64_t)d.W * d.H)) % d.C);
-    const int64_t b = i / ((int64_t)d.W * d.H * d.C);
+    const I t1 = i / d.W;
+    const int y = (int)(t1 % d.H);
+    const I t2 = t1 / d.H;
+    const int c = (int)(t2 % d.C);
+    const I b = t2 / d.C;
     float acc = 0.f;
     for (int ky = 0; ky < d.kh; ++ky) {
       const int ty = y - ky;
-      if (ty < 0 || ty % d.s) continue;
+      if (ty < 0) break;
+      if (ty % d.s) continue;
       const int oy = ty / d.s;
       if (oy >= d.OH) continue;
       for (int kx = 0; kx < d.kw; ++kx) {
         const int tx = x - kx;
-        if (tx < 0 || tx % d.s) continue;
+        if (tx < 0) break;
+        if (tx % d.s) continue;
         const int ox = tx / d.s;
         if (ox >= d.OW) continue;
-        const int64_t row = ((int64_t)c * d.kh + ky) * d.kw + kx;
-        acc += dP[row * cols + b * d.ohw() + (int64_t)oy * d.OW + ox];
+        const I row = ((I)c * d.kh + ky) * d.kw + kx;
+        acc += dP[row * cols + b * ohw + (I)oy * d.OW + ox];
       }
     }
     if (yprev) acc *= act_grad_from_out(act_prev, yprev[i]);
@@ -130,24 +137,25 @@ __global__ void pool_map_kernel(PoolDesc d, int64_t* __restrict__ src,
 // bias and activation (layers.hpp:305-321).  Max: the first window element
 // seeds, then strict '>' in (py,px) order == ties to the lowest input index,
 // and a NaN survives only if it is first (no fmaxf).
-template <class IdxT>
+template <class IdxT, class I>
 __global__ void pool_fwd_kernel(PoolDesc d, const float* __restrict__ x,
                                 const float* __restrict__ bias, int act, float* __restrict__ y,
                                 IdxT* __restrict__ arg) {
-  const int64_t total = d.out_size();
-  const int64_t plane = (int64_t)d.H * d.W;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int ox = (int)(t % d.OW), oy = (int)((t / d.OW) % d.OH);
-    const int64_t bc = t / ((int64_t)d.OW * d.OH);
-    const int64_t base = bc * plane + (int64_t)oy * d.s * d.W + (int64_t)ox * d.s;
+  const I total = (I)d.out_size();
+  const I plane = (I)d.H * d.W;
+  for (I t = blockIdx.x * (I)blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
+    const int ox = (int)(t % d.OW);
+    const I t1 = t / d.OW;
+    const int oy = (int)(t1 % d.OH);
+    const I bc = t1 / d.OH;
+    const I base = bc * plane + (I)oy * d.s * d.W + (I)ox * d.s;
     float v;
     if (d.mode == VCNN_POOL_MAX) {
       float best = x[base];
-      int64_t a = base;
+      I a = base;
       for (int py = 0; py < d.ph; ++py)
         for (int px = 0; px < d.pw; ++px) {
-          const int64_t s = base + (int64_t)py * d.W + px;
+          const I s = base + (I)py * d.W + px;
           const float xv = x[s];
           if (xv > best) {
             best = xv;
@@ -159,11 +167,11 @@ __global__ void pool_fwd_kernel(PoolDesc d, const float* __restrict__ x,
     } else {
       float acc = 0.f;
       for (int py = 0; py < d.ph; ++py)
-        for (int px = 0; px < d.pw; ++px) acc += x[base + (int64_t)py * d.W + px];
+        for (int px = 0; px < d.pw; ++px) acc += x[base + (I)py * d.W + px];
       v = acc / (float)(d.ph * d.pw);
       if (arg) arg[t] = (IdxT)-1;
     }
-    if (bias) v += bias[bc % d.C];
+    if (bias) v += bias[(int)(bc % d.C)];
     y[t] = act_fwd(act, v);
   }
 }
@@ -171,16 +179,17 @@ __global__ void pool_fwd_kernel(PoolDesc d, const float* __restrict__ x,
 // pool_backward (vectorize.hpp:224-249) in gather form: each input cell
 // visits its covering windows in window order (the reference's scatter
 // order), then the upstream activation derivative is applied.
-template <class IdxT>
+template <class IdxT, class I>
 __global__ void pool_bwd_kernel(PoolDesc d, int bwd_mode, const float* __restrict__ g,
                                 const IdxT* __restrict__ arg, float* __restrict__ dx,
                                 const float* __restrict__ yprev, int act_prev) {
-  const int64_t total = d.in_size();
+  const I total = (I)d.in_size();
   const float scale = 1.0f / (float)(d.ph * d.pw);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int x = (int)(i % d.W), y = (int)((i / d.W) % d.H);
-    const int64_t bc = i / ((int64_t)d.W * d.H);
+  for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const int x = (int)(i % d.W);
+    const I t1 = i / d.W;
+    const int y = (int)(t1 % d.H);
+    const I bc = t1 / d.H;
     int oy0 = y - d.ph + 1;
     oy0 = oy0 <= 0 ? 0 : (oy0 + d.s - 1) / d.s;
     int oy1 = y / d.s;
@@ -192,11 +201,11 @@ __global__ void pool_bwd_kernel(PoolDesc d, int bwd_mode, const float* __restric
     float acc = 0.f;
     for (int oy = oy0; oy <= oy1; ++oy)
       for (int ox = ox0; ox <= ox1; ++ox) {
-        const int64_t t = (bc * d.OH + oy) * d.OW + ox;
+        const I t = (bc * d.OH + oy) * d.OW + ox;
         if (bwd_mode == VCNN_POOLBWD_PAPER_NN) {
           acc += g[t];
         } else if (d.mode == VCNN_POOL_MAX) {
-          if ((int64_t)arg[t] == i) acc += g[t];
+          if ((I)arg[t] == i) acc += g[t];
         } else {
           acc += g[t] * scale;
         }
@@ -240,17 +249,18 @@ __global__ void act_bwd_kernel(int64_t n, int act, const float* __restrict__ y, 
 // loss_forward + loss_backward, softmax-CE (layers.hpp:402-459): one warp
 // per sample with shuffle max/sum; per-sample losses summed by thread 0 in
 // sample order (the reference's order), then / B.
-constexpr int kLossThreads = 512;
-__global__ void softmax_ce_kernel(int B, int units, const float* __restrict__ pred,
-                                  const int* __restrict__ cls, float* __restrict__ loss,
-                                  float* __restrict__ grad, int act_last, int* err) {
-  extern __shared__ float per_sample[];
+constexpr int kLossThreads = 1024;
+__global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(
+    int B, int units, const float* __restrict__ pred, const int* __restrict__ cls,
+    float* __restrict__ loss, float* __restrict__ grad, int act_last, int* err) {
+  __shared__ float red[kLossThreads];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const float inv_b = 1.0f / (float)B;
+  float mine = 0.f;  // lane 0: this warp's per-sample losses, in sample order
   for (int b = warp; b < B; b += nwarps) {
     const float* l = pred + (int64_t)b * units;
-    int c = cls[b];
+    const int c = cls[b];
     const bool bad = c < 0 || c >= units;
     if (bad && lane == 0 && err) atomicExch(err, 1);
     float m = -INFINITY;
@@ -262,25 +272,28 @@ __global__ void softmax_ce_kernel(int B, int units, const float* __restrict__ pr
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (grad) {
+      const float inv = inv_b / s;
       for (int u = lane; u < units; u += 32) {
-        float gv = expf(l[u] - m) / s * inv_b;
+        float gv = expf(l[u] - m) * inv;
         if (u == c) gv -= inv_b;
         if (act_last != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(act_last, l[u]);
         grad[(int64_t)b * units + u] = gv;
       }
     }
-    if (lane == 0) per_sample[b] = bad ? 0.f : (m + logf(s) - l[c]);
+    if (!bad) mine += m + logf(s) - l[c];
   }
+  // fixed-order tree over the warps' partial sums -> deterministic
+  red[threadIdx.x] = lane == 0 ? mine : 0.f;
   __syncthreads();
-  if (threadIdx.x == 0 && loss) {
-    float total = 0.f;
-    for (int b = 0; b < B; ++b) total += per_sample[b];
-    *loss = total / (float)B;
+  for (int st = kLossThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
   }
+  if (threadIdx.x == 0 && loss) *loss = red[0] / (float)B;
 }
 
 // MSE (layers.hpp:425-433, :461-467): loss = mean (p-t)^2, grad 2(p-t)/n
-__global__ void mse_kernel(int64_t n, const float* __restrict__ p, const float* __restrict__ t,
+__global__ void __launch_bounds__(kLossThreads) mse_kernel(int64_t n, const float* __restrict__ p, const float* __restrict__ t,
                            float* __restrict__ loss, float* __restrict__ grad, int act_last) {
   __shared__ float sh[kLossThreads];
   const float scale = 2.0f / (float)n;
@@ -545,7 +558,10 @@ int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st) 
 
 int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st,
                   const float* yprev, int act_prev) {
-  col2im_kernel<<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX, yprev, act_prev);
+  if (fits32(d.in_size()) && fits32(d.kd() * d.pixels()))
+    col2im_kernel<int><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX, yprev, act_prev);
+  else
+    col2im_kernel<int64_t><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX, yprev, act_prev);
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -565,7 +581,11 @@ int launch_pool_map(const PoolDesc& d, int64_t* src, int64_t* tgt, cudaStream_t 
 template <class IdxT>
 int launch_pool_fwd(const PoolDesc& d, const float* x, const float* bias, int act, float* y,
                     IdxT* arg, cudaStream_t st) {
-  pool_fwd_kernel<IdxT><<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, bias, act, y, arg);
+  if (fits32(d.in_size()))
+    pool_fwd_kernel<IdxT, int><<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, bias, act, y, arg);
+  else
+    pool_fwd_kernel<IdxT, int64_t><<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, bias, act, y,
+                                                                                arg);
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -577,8 +597,12 @@ template int launch_pool_fwd<int64_t>(const PoolDesc&, const float*, const float
 template <class IdxT>
 int launch_pool_bwd(const PoolDesc& d, int bwd_mode, const float* gpre, const IdxT* arg,
                     float* dx, const float* yprev, int act_prev, cudaStream_t st) {
-  pool_bwd_kernel<IdxT><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, bwd_mode, gpre, arg, dx,
-                                                                     yprev, act_prev);
+  if (fits32(d.in_size()))
+    pool_bwd_kernel<IdxT, int><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, bwd_mode, gpre, arg,
+                                                                           dx, yprev, act_prev);
+  else
+    pool_bwd_kernel<IdxT, int64_t><<<grid_for(d.in_size()), kThreads, 0, st>>>(
+        d, bwd_mode, gpre, arg, dx, yprev, act_prev);
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -610,14 +634,7 @@ int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
                 const float* values, float* loss, float* grad, int act_last, int* err,
                 cudaStream_t st) {
   if (kind == VCNN_LOSS_SOFTMAX_CE) {
-    const size_t smem = sizeof(float) * (size_t)B;
-    if (smem > 200 * 1024) return fail(VCNN_ESHAPE, "loss: batch too large for one block");
-    if (smem > 48 * 1024)
-      VCNN_CUDA_TRY(cudaFuncSetAttribute(softmax_ce_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
-    softmax_ce_kernel<<<1, kLossThreads, smem, st>>>(B, units, pred, cls, loss, grad, act_last,
-                                                      err);
+    softmax_ce_kernel<<<1, kLossThreads, 0, st>>>(B, units, pred, cls, loss, grad, act_last, err);
   } else {
     mse_kernel<<<1, kLossThreads, 0, st>>>((int64_t)B * units, pred, values, loss, grad,
                                            act_last);

@@ -16,7 +16,7 @@
 //     activation, the upstream activation derivative, or stores a split-K
 //     partial that a fixed-order reduce kernel finishes with the same fused
 //     epilogue -- deterministic, no float atomics.
-// Small problems split K so the grid covers the 148 SMs (2 CTAs/SM).  The
+// Small problems split K so the grid covers the 148 SMs (3 CTAs/SM).  The
 // bias gradient is folded into the wgrad GEMMs as one extra K-row / N-column
 // of ones.  Layers whose output is much smaller than their input (e.g. a 1x1
 // output) use the explicit dgrad W^T*G -> col2im instead of the implicit one,
@@ -35,7 +35,8 @@ namespace {
 constexpr int BM = 128;            // rows per tile == TMEM lanes
 constexpr int BK = 32;             // fp32 K per stage == one 128-B swizzle row
 constexpr int NT = 128;            // threads per CTA
-constexpr int TAB_MAX_INTS = 6144; // per-CTA K-offset tables (24 KB)
+constexpr int TAB_MAX_INTS = 4096; // per-CTA K-offset tables (16 KB)
+constexpr int CTAS_PER_SM = 3;     // smem sized for 3 resident CTAs / SM
 
 // Out-of-line activation helpers for the epilogues: the unrolled epilogue
 // would otherwise inline the transcendental branches 16x per TMEM load and
@@ -91,7 +92,7 @@ struct TileCfg {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int NS = SPLIT3 ? 2 : 1;
   static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * NS;
-  static constexpr int STAGES_RAW = (80 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (44 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 4 ? 4 : (STAGES_RAW < 2 ? 2 : STAGES_RAW);
   static constexpr int TAB_OFF = STAGES * STAGE_BYTES;
   static constexpr int SMEM_MAX = TAB_OFF + TAB_MAX_INTS * 4 + 1024;
@@ -659,7 +660,7 @@ struct Plan {
   size_t tab_bytes() const { return sizeof(int) * (size_t)tables * kb_per * BK; }
 };
 
-// Split K so that tiles * splits covers ~2 CTAs per SM, with >= min_kb K
+// Split K so that tiles * splits covers <= 3 CTAs per SM (one wave), with >= min_kb K
 // blocks per split (the partial write + reduce must pay for itself) and
 // <= the K blocks whose offset tables fit in shared memory.
 Plan make_plan(int64_t M, int64_t N, int64_t K, int tables, int min_kb = 2) {
@@ -673,10 +674,10 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int tables, int min_kb = 2) {
   p.kb_total = (int)cdiv(K, BK);
   if (p.kb_total < 1) p.kb_total = 1;
   const int64_t tiles = p.mt * p.nt;
-  const int64_t target = 2 * (int64_t)sm_count();
+  const int64_t target = CTAS_PER_SM * (int64_t)sm_count();
   int64_t splits = 1;
   if (tiles < target) {
-    splits = cdiv(target, tiles);
+    splits = target / tiles;  // floor: never spill a near-empty extra wave
     int64_t cap = p.kb_total / min_kb;
     if (cap < 1) cap = 1;
     if (splits > cap) splits = cap;
