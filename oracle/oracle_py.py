@@ -360,6 +360,9 @@ def ref():
         L.ref_net_train_steps.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                           C.c_int, C.c_void_p]
+        L.ref_net_train_steps_f32.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p, C.c_double, C.c_double,
+                                              C.c_int, C.c_void_p]
         L.ref_synth_bench_data.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
         _ref = L
@@ -400,4 +403,19 @@ def ref_net_train_steps(spec, params, x, cls, values, lr, mom, steps):
     losses = np.empty(steps)
     _chk(ref().ref_net_train_steps(C.byref(n), B, _dp(p), _dp(x), _dp(c), _dp(v), lr, mom, steps,
                                    _dp(losses)), "ref_net_train_steps")
+    return p, losses
+
+
+def ref_net_train_steps_f32(spec, params, x, cls, values, lr, mom, steps):
+    """The reference's own float Executor<float>(imp6) + sgd_step trajectory."""
+    n = make_net(spec)
+    B = x.shape[0]
+    p = np.ascontiguousarray(params, dtype=np.float32).copy()
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    c = np.ascontiguousarray(cls, dtype=np.int32) if cls is not None else None
+    v = np.ascontiguousarray(values, dtype=np.float32) if values is not None else None
+    losses = np.empty(steps)
+    _chk(ref().ref_net_train_steps_f32(C.byref(n), B, p.ctypes.data, x.ctypes.data,
+                                       _dp(c), None if v is None else v.ctypes.data, lr, mom,
+                                       steps, _dp(losses)), "ref_net_train_steps_f32")
     return p, losses

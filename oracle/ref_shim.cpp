@@ -259,6 +259,36 @@ int ref_net_train_steps(const orc_net* n, int B, double* params, const double* x
   }
 }
 
+// the reference's own float path (Executor<float>(imp6) + sgd_step): used to
+// measure how far an fp32 trajectory legitimately drifts from the f64 one
+// (near-tie argmax / ReLU decisions), which sets the N-step tolerances
+int ref_net_train_steps_f32(const orc_net* n, int B, float* params, const float* x,
+                            const int* cls, const float* values, double lr, double mom,
+                            int steps, double* losses) {
+  try {
+    NetworkSpec spec = spec_of(n);
+    Network<float> net = build_network<float>(spec);
+    flat_to_params(net, params);
+    Tensor<float> xb(Shape::hwcn(n->in_h, n->in_w, n->in_c, B));
+    std::memcpy(xb.data.data(), x, sizeof(float) * xb.data.size());
+    Targets<float> t = targets_of<float>(spec, B, cls, values);
+    Executor<float> exec(Variant::imp6);
+    TrainConfig cfg;
+    cfg.lr = lr;
+    cfg.momentum = mom;
+    Velocity<float> vel;
+    for (int s = 0; s < steps; ++s) {
+      RunResult<float> r = exec.run_batch(net, xb, &t);
+      losses[s] = r.loss;
+      sgd_step(net, r.grads, cfg, vel);
+    }
+    params_to_flat(net, params);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 int ref_im2col(int B, int C, int H, int W, int kh, int kw, int s, const double* x, double* P) {
   try {
     Tensor<double> f(Shape::hwcn(H, W, C, B));

@@ -17,7 +17,7 @@ from paper_1501_07338_b200.engine import Executor, Network, Trainer, predict_cla
 from paper_1501_07338_b200.errors import BoundsError, ShapeError, TrainingError
 from paper_1501_07338_b200.spec import Precision
 
-from .util import ALL_PREC, TOL, act_grad_np, act_np, assert_close, f32, normwise
+from .util import ALL_PREC, TOL, TOL_STEPS, act_grad_np, act_np, assert_close, ref_f32_drift, f32, normwise
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -144,9 +144,13 @@ def test_net_vs_reference_fixture(path, prec):
         net.train_step(B, float(d["lr"]), float(d["mom"]))
     p = net.get_params()
     p0 = d["params0"]
-    assert_close(p, d["params_after"], tol, "weights after N steps")
+    is_ce = spec.loss == S.LossKind.softmax_ce
+    drift, udrift = ref_f32_drift(spec, p0, x, cls if is_ce else None, None if is_ce else vals,
+                                  float(d["lr"]), float(d["mom"]), int(d["steps"]))
+    assert_close(p, d["params_after"], max(TOL_STEPS[prec], 2 * drift), "weights after N steps")
     if strict:
-        assert_close(p - p0, d["params_after"] - p0, 20 * tol, "update after N steps")
+        assert_close(p - p0, d["params_after"] - p0, max(20 * tol, 2 * udrift),
+                     "update after N steps")
     net.close()
 
 
@@ -196,9 +200,12 @@ def test_net_vs_oracle_10_steps(name, prec):
         g = O.net_run_batch(spec, p, f32(x), **_targets(spec, cls, vals))["grads"]
         O.sgd_step(p, v, g, 0.01, 0.9)
     pg = net.get_params()
-    assert_close(pg, p, tol, "weights after 10 steps")
+    is_ce = spec.loss == S.LossKind.softmax_ce
+    drift, udrift = ref_f32_drift(spec, p0, x, cls if is_ce else None, None if is_ce else vals,
+                                  0.01, 0.9, 10)
+    assert_close(pg, p, max(TOL_STEPS[prec], 2 * drift), "weights after 10 steps")
     if strict:
-        assert_close(pg - p0, p - p0, 20 * tol, "update after 10 steps")
+        assert_close(pg - p0, p - p0, max(20 * tol, 2 * udrift), "update after 10 steps")
     else:  # TF32: decision flips allowed, the update direction must agree
         du, dr = (pg - p0).ravel(), (p - p0).ravel()
         assert float(du @ dr) / (np.linalg.norm(du) * np.linalg.norm(dr)) > 0.98
