@@ -30,3 +30,11 @@ clean:
 	rm -rf build $(LIB)
 
 .PHONY: all lib oracle clean
+
+# debug build with clock64 phase stamps in the tcgen05 kernel (scripts/phase_timing.py)
+DBG_LIB := build/libvcnn_cuda_phase.so
+phase: $(SRCS) $(HDRS)
+	@mkdir -p build/objdbg
+	for f in $(SRCS); do $(NVCC) $(NVFLAGS) -DVCNN_PHASE_TIMING -c $$f -o build/objdbg/$$(basename $$f .cu).o || exit 1; done
+	$(NVCC) $(ARCH) -shared -o $(DBG_LIB) build/objdbg/*.o
+.PHONY: phase

@@ -238,6 +238,14 @@ int vcnn_net_set_stream(vcnn_net* net, void* stream);
 /* Executor::set_pool_backward_mode (variants.hpp:342) */
 int vcnn_net_set_pool_backward_mode(vcnn_net* net, int mode);
 int vcnn_net_set_precision(vcnn_net* net, int precision);
+/* conv -> max-pool fusion (default on, TF32): the
+ * pool runs in the conv epilogue and its backward is routed inside the conv's
+ * wgrad / dgrad.  Results are bit-identical with it off. */
+int vcnn_net_set_fusion(vcnn_net* net, int enable);
+/* keep the whole forward trace (every layer output) and every layer's
+ * pre-activation gradient in device memory, as the reference's LayerTrace
+ * does (variants.hpp:305-323); disables fusion.  Default off. */
+int vcnn_net_set_trace(vcnn_net* net, int keep);
 /* host <-> device parameter / gradient / velocity transfers (synchronous) */
 int vcnn_net_get_params(vcnn_net* net, float* host);
 int vcnn_net_set_params(vcnn_net* net, const float* host);

@@ -10,7 +10,9 @@ import os
 from .errors import STATUS_TO_ERROR, VcnnError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvcnn_cuda.so")
+# VCNN_LIB_PATH: an alternative in-tree build (e.g. the phase-timing build of
+# scripts/phase_timing.py); default the product library
+LIB_PATH = os.environ.get("VCNN_LIB_PATH") or os.path.join(_HERE, "libvcnn_cuda.so")
 
 c_int = C.c_int
 c_i64 = C.c_int64
@@ -94,6 +96,8 @@ _SIGS = {
     "vcnn_net_set_stream": [c_vp, c_vp],
     "vcnn_net_set_pool_backward_mode": [c_vp, c_int],
     "vcnn_net_set_precision": [c_vp, c_int],
+    "vcnn_net_set_fusion": [c_vp, c_int],
+    "vcnn_net_set_trace": [c_vp, c_int],
     "vcnn_net_get_params": [c_vp, c_vp],
     "vcnn_net_set_params": [c_vp, c_vp],
     "vcnn_net_get_grads": [c_vp, c_vp],

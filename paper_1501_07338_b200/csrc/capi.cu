@@ -290,7 +290,22 @@ int vcnn_conv_forward(const vcnn_conv_geometry* g, int maps, const float* x, con
   TRY(require_device());
   cudaStream_t st = as_stream(stream);
   WORKSPACE(ws, conv_workspace(d, precision));
-  return launch_conv_fwd(d, x, w, bias, act, y, precision, ws, st);
+  // TF32: the direct (shifted-view) kernel with prepacked weights, else the
+  // slab kernel with a tf32-rounded weight copy
+  Scratch wp(st);
+  const float* wf = nullptr;
+  if (precision == VCNN_PREC_TF32 && direct::fwd_ok(d, 0)) {
+    TRY(wp.alloc(sizeof(float) * direct::pack_floats(d, 0)));
+    float* pk = static_cast<float*>(wp.p);
+    TRY(direct::pack_weights(d, 0, w, pk, st));
+    return direct::conv_fwd(d, x, pk, bias, act, y, PoolFuse{}, st);
+  }
+  if (precision == VCNN_PREC_TF32 && tc::slab_fwd_ok(d, 0)) {
+    TRY(wp.alloc(sizeof(float) * tc::prep_floats_f(d)));
+    wf = static_cast<float*>(wp.p);
+    TRY(tc::prep_weights(d, w, static_cast<float*>(wp.p), nullptr, st));
+  }
+  return launch_conv_fwd(d, x, w, bias, act, y, precision, ws, st, wf);
 }
 
 int vcnn_conv_backward(const vcnn_conv_geometry* g, int maps, const float* x, const float* w,
@@ -312,7 +327,26 @@ int vcnn_conv_backward(const vcnn_conv_geometry* g, int maps, const float* x, co
   }
   WORKSPACE(ws, conv_workspace(d, precision));
   TRY(launch_conv_wgrad(d, x, gpre, dw, db, precision, ws, st));
-  if (dx) TRY(launch_conv_dgrad(d, gpre, w, dx, nullptr, VCNN_ACT_IDENTITY, precision, ws, st));
+  if (!dx) return VCNN_OK;
+  // TF32: tf32-rounded transposed weights for the slab dgrad
+  Scratch wp(st);
+  const float* wt = nullptr;
+  if (precision == VCNN_PREC_TF32 && direct::dgrad_ok(d)) {
+    TRY(wp.alloc(sizeof(float) * direct::pack_floats(d, 1)));
+    float* pk = static_cast<float*>(wp.p);
+    TRY(direct::pack_weights(d, 1, w, pk, st));
+    GradSrc gs;
+    gs.g = gpre;
+    return direct::conv_dgrad(d, gs, pk, dx, nullptr, VCNN_ACT_IDENTITY, st);
+  }
+  if (precision == VCNN_PREC_TF32 && tc::slab_dgrad_ok(d)) {
+    const size_t nf = tc::prep_floats_f(d);
+    TRY(wp.alloc(sizeof(float) * (nf + tc::prep_floats_t(d))));
+    float* wf = static_cast<float*>(wp.p);
+    wt = wf + nf;
+    TRY(tc::prep_weights(d, w, wf, wf + nf, st));
+  }
+  TRY(launch_conv_dgrad(d, gpre, w, dx, nullptr, VCNN_ACT_IDENTITY, precision, ws, st, wt));
   return VCNN_OK;
 }
 

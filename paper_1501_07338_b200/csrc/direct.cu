@@ -1,0 +1,542 @@
+// direct.cu -- stride-1 convolution forward and data-gradient as "shifted
+// view" implicit GEMMs on the sm_100a tensor cores (tcgen05, TF32).
+//
+// Output positions of a tile are R rows of a super-grid of width Wg (the
+// input width for the forward, W+kw-1 for dgrad), i.e. 128 consecutive
+// linear positions q.  For a kernel offset (ky,kx) the A operand of the
+// GEMM -- A[q][c] = in[c][q + ky*Wg + kx] -- is the staged input slab
+// itself: the slab is laid out [channel group of 8][half][position][4
+// channels], 16 bytes per position, and read through a no-swizzle K-major
+// descriptor whose 8-row core matrices are 8 consecutive positions (SBO =
+// 128 B) and whose two K halves are LBO apart.  A shift of the view by
+// ky*Wg+kx positions is just +16 bytes per position on the start address.
+// B (weights, K-major, 8 channels per MMA) arrives prepacked in exactly its
+// shared-memory image (pack_weights) with one TMA bulk copy.  No im2col is
+// ever built: after staging, ONE thread issues kh*kw*ceil(C/8) MMAs
+// (M=128, N=BN, K=8) back to back into a TMEM accumulator.
+//
+// Positions whose column is past the valid output width (x >= OW) are
+// computed and discarded -- the price of a uniform descriptor stride.
+//
+// Forward epilogue: bias + activation, NCHW store, optional fused
+// non-overlapping max pool (window == stride; strict >, ties -> lowest
+// index; int32 global argmax) -- conv_forward + pool_forward,
+// layers.hpp:139-149, vectorize.hpp:197-210, tensor.hpp:271-289.
+// dgrad: dX = conv(Gpad, flip(W)^T) over the zero-padded gradient; the
+// gradient may be routed on the fly from a fused pool (GradSrc), epilogue
+// multiplies the upstream activation derivative -- conv_backward_core dX
+// (layers.hpp:179) + apply_activation_grad (layers.hpp:57-61).
+#include <string>
+#include <type_traits>
+
+#include "kernels.cuh"
+#include "tc_ptx.cuh"
+
+namespace vcnn_b200 {
+namespace direct {
+
+namespace {
+
+constexpr int NT = 128;
+constexpr int BM = 128;
+constexpr size_t kSmemOptin = 227 * 1024;
+
+struct Geo {
+  int mode;                // 0 forward, 1 dgrad
+  int B;
+  int Cin, Hin, Win;       // staged planes: fwd x [B][C][H][W]; dgrad G [B][K][OH][OW]
+  int Cout;                // GEMM N: fwd K maps; dgrad C channels
+  int kh, kw;
+  int Wg;                  // super-grid row width
+  int Hout, Wout;          // valid outputs per image
+  int pad_y, pad_x;        // input origin inside the super-grid
+  int R, tpi;              // output rows per tile, tiles per image
+  int CG, NP;              // channel groups of 8; staged positions
+  int BN, nblk;            // N tile, N blocks
+  int off_b, off_raw, off_win, off_a, smem;  // shared-memory layout (bytes)
+  int raw_n, win_n;        // floats: raw input image, window scratch (routed dgrad)
+};
+
+// pack layout per N block: [s = ky*kw+kx][cg][BN/8][2][8][4] (K-major
+// no-swizzle core matrices: LBO = 128 B between the two 4-channel halves,
+// SBO = 256 B between 8-row groups)
+__host__ __device__ inline int64_t pack_floats_per_block(const Geo& g) {
+  return (int64_t)g.kh * g.kw * g.CG * g.BN * 8;
+}
+
+bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
+  g = Geo{};
+  if (d.s != 1) return false;
+  g.mode = mode;
+  g.B = d.B;
+  g.kh = d.kh;
+  g.kw = d.kw;
+  if (mode == 0) {
+    g.Cin = d.C, g.Hin = d.H, g.Win = d.W, g.Cout = d.K;
+    g.Wg = d.W, g.Hout = d.OH, g.Wout = d.OW, g.pad_y = 0, g.pad_x = 0;
+  } else {
+    g.Cin = d.K, g.Hin = d.OH, g.Win = d.OW, g.Cout = d.C;
+    g.Wg = d.W + d.kw - 1, g.Hout = d.H, g.Wout = d.W, g.pad_y = d.kh - 1, g.pad_x = d.kw - 1;
+  }
+  if (g.Wg > BM || g.Hout < 1) return false;
+  int R = BM / g.Wg;
+  if (R > g.Hout) R = g.Hout;
+  if (pool) {
+    R = (R / pool) * pool;
+    if (R < 1) return false;
+  } else {
+    R = (int)cdiv(g.Hout, cdiv(g.Hout, R));  // balanced row blocks
+  }
+  g.R = R;
+  g.tpi = (int)cdiv(g.Hout, R);
+  g.CG = (int)cdiv(g.Cin, 8);
+  const int maxsh = (g.kh - 1) * g.Wg + g.kw - 1;
+  g.NP = (int)cdiv(maxsh + BM, 8) * 8;
+  // the input image and the window arrays go in with single bulk copies
+  if ((g.Cin * g.Hin * g.Win) % 4 != 0) return false;
+  if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
+  g.raw_n = g.Cin * g.Hin * g.Win;
+  // dgrad always reserves window scratch for a >= 2x2 pool, so the routed
+  // and unrouted plans (and the weight pack) share one BN
+  if (mode == 1) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
+  const int a_bytes = g.CG * 2 * g.NP * 16 + 4 * g.NP;  // slab + position table
+  const int raw_bytes = 4 * g.raw_n;
+  const int win_bytes = 2 * 4 * g.win_n;
+  if (raw_bytes > 96 * 1024) return false;
+  for (int bn = g.Cout > 128 ? 128 : (int)((g.Cout + 15) / 16 * 16); bn >= 16; bn -= 16) {
+    const int b_bytes = g.kh * g.kw * g.CG * bn * 32;
+    // the epilogue tile [bn][128] reuses raw + window + A (all dead by then)
+    const int ep_bytes = bn * BM * 4;
+    const int tail = raw_bytes + win_bytes + a_bytes > ep_bytes ? raw_bytes + win_bytes + a_bytes
+                                                                : ep_bytes;
+    const int total = b_bytes + tail + 1024;
+    if ((size_t)total + 512 <= kSmemOptin) {
+      g.BN = bn;
+      g.nblk = (int)cdiv(g.Cout, bn);
+      g.off_b = 0;
+      g.off_raw = b_bytes;
+      g.off_win = g.off_raw + raw_bytes;
+      g.off_a = g.off_win + win_bytes;
+      g.smem = total;
+      return (int64_t)g.B * g.tpi < (1 << 24);
+    }
+  }
+  return false;
+}
+
+__global__ void pack_kernel(Geo g, int mode, const float* __restrict__ w, float* __restrict__ pk) {
+  // w: [K][C][kh][kw] (conv weights).  fwd rows = maps n, channels = c;
+  // dgrad rows = channels c, channels = maps n, kernel flipped.
+  const int64_t per = pack_floats_per_block(g), total = per * g.nblk;
+  const int Cch = mode == 0 ? g.Cin : g.Cout;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int nb = (int)(i / per);
+    int64_t r = i - nb * per;
+    const int k4 = (int)(r & 3), r8 = (int)((r >> 2) & 7), kh2 = (int)((r >> 5) & 1);
+    r >>= 6;
+    const int rg = (int)(r % (g.BN / 8));
+    r /= (g.BN / 8);
+    const int cg = (int)(r % g.CG);
+    const int s = (int)(r / g.CG);
+    const int row = nb * g.BN + rg * 8 + r8;  // GEMM N index
+    const int ch = cg * 8 + kh2 * 4 + k4;     // GEMM K index (input channel of the view)
+    float v = 0.f;
+    if (row < g.Cout && ch < g.Cin) {
+      const int ky = s / g.kw, kx = s - (s / g.kw) * g.kw;
+      const int n = mode == 0 ? row : ch, c = mode == 0 ? ch : row;
+      const int wy = mode == 0 ? ky : g.kh - 1 - ky, wx = mode == 0 ? kx : g.kw - 1 - kx;
+      v = ptx::to_tf32(w[(((int64_t)n * Cch + c) * g.kh + wy) * g.kw + wx]);
+    }
+    pk[i] = v;
+  }
+}
+
+template <int ACT>
+__device__ __forceinline__ float actf(float x) {
+  if (ACT == VCNN_ACT_RELU) return x > 0.f ? x : 0.f;
+  if (ACT == VCNN_ACT_SIGMOID) return 1.f / (1.f + expf(-x));
+  if (ACT == VCNN_ACT_TANH) return tanhf(x);
+  return x;
+}
+
+struct FwdEpi {
+  const float* bias;
+  int act;
+  float* y;  // nullable when pooled
+  int pool, POH, POW;
+  float* py;
+  int32_t* parg;
+};
+struct BwdEpi {
+  float* dx;
+  const float* yprev;
+  int act_prev;
+};
+
+struct Args {
+  Geo g;
+  const float* in;     // x (fwd) or materialised G (dgrad), NCHW
+  GradSrc gs;          // dgrad: routed gradient (gs.pool)
+  const float* pack;   // prepacked B
+  FwdEpi fe;
+  BwdEpi be;
+};
+
+// Epilogues read the accumulator tile ep[n][128] (position m = r*Wg + x) from
+// shared memory.  Work is spread warp = output row, lane = column, loop =
+// map, so no thread divides by a runtime extent; stores along a row are
+// coalesced.
+template <int ACT>
+__device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) {
+  const Geo& g = a.g;
+  const FwdEpi& e = a.fe;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nr = g.Hout - r0 < g.R ? g.Hout - r0 : g.R;
+  const int nmaps = g.Cout - n0 < g.BN ? g.Cout - n0 : g.BN;
+  const int64_t ohw = (int64_t)g.Hout * g.Wout;
+  const int64_t plane0 = (int64_t)b * g.Cout + n0;
+  if (e.y) {
+    for (int r = warp; r < nr; r += NT / 32)
+      for (int x = lane; x < g.Wout; x += 32) {
+        float* yp = e.y + plane0 * ohw + (int64_t)(r0 + r) * g.Wout + x;
+        const uint32_t ep = eb + 4u * (r * g.Wg + x);
+        for (int n = 0; n < nmaps; ++n)
+          yp[n * ohw] = actf<ACT>(ptx::lds_f32(ep + 4u * (n * BM)) + __ldg(e.bias + n0 + n));
+      }
+  }
+  if (e.pool) {
+    const int p = e.pool;
+    int nwr = (r0 + nr) / p - r0 / p;  // complete window rows of this tile
+    if (r0 / p + nwr > e.POH) nwr = e.POH - r0 / p;
+    const int64_t pplane = (int64_t)e.POH * e.POW;
+    for (int wr = warp; wr < nwr; wr += NT / 32)
+      for (int wc = lane; wc < e.POW; wc += 32) {
+        const int ry = wr * p, cx = wc * p;
+        const int64_t o0 = plane0 * pplane + (int64_t)(r0 / p + wr) * e.POW + wc;
+        for (int n = 0; n < nmaps; ++n) {
+          const float bn_ = __ldg(e.bias + n0 + n);
+          const uint32_t en = eb + 4u * (n * BM);
+          float best = actf<ACT>(ptx::lds_f32(en + 4u * (ry * g.Wg + cx)) + bn_);
+          int by = 0, bx = 0;
+          for (int u = 0; u < p; ++u)
+            for (int v = 0; v < p; ++v) {
+              const float val = actf<ACT>(ptx::lds_f32(en + 4u * ((ry + u) * g.Wg + cx + v)) + bn_);
+              if (val > best) {
+                best = val;
+                by = u;
+                bx = v;
+              }
+            }
+          e.py[o0 + n * pplane] = best;
+          e.parg[o0 + n * pplane] =
+              (int32_t)((plane0 + n) * ohw + (int64_t)(r0 + ry + by) * g.Wout + cx + bx);
+        }
+      }
+  }
+}
+
+template <int ACT>
+__device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) {
+  const Geo& g = a.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nr = g.Hout - r0 < g.R ? g.Hout - r0 : g.R;
+  const int nch = g.Cout - n0 < g.BN ? g.Cout - n0 : g.BN;
+  const int64_t hw = (int64_t)g.Hout * g.Wout;
+  const int64_t plane0 = (int64_t)b * g.Cout + n0;
+  for (int r = warp; r < nr; r += NT / 32)
+    for (int x = lane; x < g.Wout; x += 32) {
+      const int64_t o = plane0 * hw + (int64_t)(r0 + r) * g.Wout + x;
+      const uint32_t ep = eb + 4u * (r * g.Wg + x);
+      for (int c = 0; c < nch; ++c) {
+        float v = ptx::lds_f32(ep + 4u * (c * BM));
+        if (a.be.yprev) {
+          const float yv = a.be.yprev[o + c * hw];
+          if (ACT == VCNN_ACT_RELU) v *= yv > 0.f ? 1.f : 0.f;
+          else if (ACT == VCNN_ACT_SIGMOID) v *= yv * (1.f - yv);
+          else if (ACT == VCNN_ACT_TANH) v *= 1.f - yv * yv;
+        }
+        a.be.dx[o + c * hw] = v;
+      }
+    }
+}
+
+template <class F>
+__device__ __forceinline__ void with_act(int act, F&& f) {
+  switch (act) {
+    case VCNN_ACT_RELU: f(std::integral_constant<int, VCNN_ACT_RELU>{}); break;
+    case VCNN_ACT_SIGMOID: f(std::integral_constant<int, VCNN_ACT_SIGMOID>{}); break;
+    case VCNN_ACT_TANH: f(std::integral_constant<int, VCNN_ACT_TANH>{}); break;
+    default: f(std::integral_constant<int, VCNN_ACT_IDENTITY>{});
+  }
+}
+
+#ifdef VCNN_PHASE_TIMING
+__device__ float g_dump[4][256];
+__device__ unsigned long long g_dphase[8][8];
+#define DPHASE(i)                                                                        \
+  do {                                                                                   \
+    if (threadIdx.x == 0 && blockIdx.x + blockIdx.y < 8) g_dphase[blockIdx.x + blockIdx.y][i] = clock64(); \
+  } while (0)
+#else
+#define DPHASE(i) \
+  do {            \
+  } while (0)
+#endif
+
+template <int TMEM_COLS>
+__global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
+  const Geo& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t load_bar, done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tile = blockIdx.x, nb = blockIdx.y;
+  const int b = tile / g.tpi, r0 = (tile - b * g.tpi) * g.R;
+  const int n0 = nb * g.BN;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t s_b = sbase + g.off_b, s_raw = sbase + g.off_raw, s_win = sbase + g.off_win,
+                 s_a = sbase + g.off_a;
+  DPHASE(0);
+
+  if (warp == 0) {
+    ptx::tmem_alloc(&tmem_base_sh, TMEM_COLS);
+    ptx::tmem_relinquish();
+  }
+  // ---- TMA bulk loads: prepacked B, the input image (or routed windows) ----
+  const int64_t pk_per = pack_floats_per_block(g);
+  const bool routed = g.mode == 1 && a.gs.pool;
+  const int wsz = routed ? a.gs.POH * a.gs.POW * g.Cin : 0;
+  if (tid == 0) {
+    ptx::mbar_init(&load_bar, 1);
+    ptx::mbar_init(&done_bar, 1);
+    ptx::fence_mbar_init();
+    uint32_t bytes = (uint32_t)(pk_per * 4);
+    ptx::mbar_expect_tx(&load_bar, bytes);
+    ptx::bulk_g2s(s_b, a.pack + nb * pk_per, bytes, &load_bar);
+    if (!routed) {
+      const uint32_t rb = 4u * (uint32_t)(g.Cin * g.Hin * g.Win);
+      ptx::mbar_expect_tx(&load_bar, rb);
+      ptx::bulk_g2s(s_raw, a.in + (int64_t)b * g.Cin * g.Hin * g.Win, rb, &load_bar);
+    } else {
+      const uint32_t wb = 4u * (uint32_t)wsz;
+      ptx::mbar_expect_tx(&load_bar, 2 * wb);
+      ptx::bulk_g2s(s_win, a.gs.dP + (int64_t)b * wsz, wb, &load_bar);
+      ptx::bulk_g2s(s_win + 4u * g.win_n, a.gs.parg + (int64_t)b * wsz, wb, &load_bar);
+    }
+    ptx::mbar_arrive(&load_bar);
+  }
+  __syncthreads();
+  DPHASE(1);
+  if (routed) {  // zero the gradient image while the windows land
+    for (int i = tid; i < g.raw_n; i += NT) ptx::sts_f32(s_raw + 4u * i, 0.f);
+  }
+  ptx::mbar_wait(&load_bar, 0);
+  DPHASE(2);
+  if (routed) {  // scatter dP (already * act') to the argmax positions
+    __syncthreads();
+    const int hw = g.Hin * g.Win;
+    const int base = (int)((int64_t)b * g.Cin * hw);
+    for (int i = tid; i < wsz; i += NT) {
+      const int at = ptx::lds_s32(s_win + 4u * (g.win_n + i)) - base;
+      ptx::sts_f32(s_raw + 4u * at, ptx::lds_f32(s_win + 4u * i));
+    }
+    __syncthreads();
+  }
+  // ---- build the tf32-rounded [cg][half][position][4] slab ----
+  // position -> offset in the staged image (-1 outside it), one division per
+  // position; then thread -> (position, channel%4), 8 positions x 16 B per
+  // 128-byte warp store (conflict-free)
+  {
+    int* pos_off = reinterpret_cast<int*>(smem + g.off_a) + g.CG * 2 * g.NP * 4;
+    for (int P = tid; P < g.NP; P += NT) {
+      const int yy = r0 + P / g.Wg - g.pad_y, xx = P % g.Wg - g.pad_x;
+      pos_off[P] = (yy >= 0 && yy < g.Hin && xx >= 0 && xx < g.Win) ? yy * g.Win + xx : -1;
+    }
+    __syncthreads();
+    const uint32_t s_pos = ptx::smem_u32(pos_off);
+    const int hw = g.Hin * g.Win;
+    for (int ch = 0; ch < 2 * g.CG; ++ch) {  // ch = cg*2 + half: channels ch*4 .. ch*4+3
+      const uint32_t dst = s_a + (uint32_t)ch * (uint32_t)g.NP * 16u;
+      for (int j = tid; j < 4 * g.NP; j += NT) {
+        const int c = ch * 4 + (j & 3);
+        const int off = ptx::lds_s32(s_pos + 4u * (j >> 2));
+        float v = 0.f;
+        if (c < g.Cin && off >= 0) v = ptx::to_tf32(ptx::lds_f32(s_raw + 4u * (c * hw + off)));
+        ptx::sts_f32(dst + 4u * j, v);
+      }
+    }
+  }
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+#ifdef VCNN_PHASE_TIMING
+  if (blockIdx.x == 0 && blockIdx.y == 0) {
+    for (int i = tid; i < 256; i += NT) {
+      g_dump[0][i] = ptx::lds_f32(s_raw + 4u * i);
+      g_dump[1][i] = ptx::lds_f32(s_a + 4u * i);
+      g_dump[2][i] = ptx::lds_f32(s_b + 4u * i);
+    }
+  }
+#endif
+
+  DPHASE(3);
+  // ---- one thread issues every MMA ----
+  if (tid == 0) {
+    const uint32_t idesc = ptx::idesc_tf32(BM, g.BN);  // both operands K-major
+    const uint32_t half = (uint32_t)g.NP * 16u;          // LBO: the two 4-channel halves
+    // descriptors advance by plain additions on the start-address field
+    // (16-byte units): A by the shift and the channel group, B by its block
+    const uint64_t a0 = ptx::interleave_desc(s_a, half, 128u);
+    const uint64_t b0 = ptx::interleave_desc(s_b, 128u, 256u);
+    const uint64_t a_cg = (uint64_t)(2u * half >> 4), b_blk = (uint64_t)(g.BN * 32 >> 4);
+    uint64_t bd = b0;
+    uint32_t acc = 0;
+    for (int ky = 0; ky < g.kh; ++ky) {
+      for (int kx = 0; kx < g.kw; ++kx) {
+        uint64_t ad = a0 + (uint64_t)(ky * g.Wg + kx);
+        for (int cg = 0; cg < g.CG; ++cg) {
+          ptx::mma_tf32(tmem, ad, bd, idesc, acc);
+          acc = 1;
+          ad += a_cg;
+          bd += b_blk;
+        }
+      }
+    }
+    ptx::mma_commit(&done_bar);
+  }
+  if (warp == 0) ptx::mbar_wait(&done_bar, 0);  // the other warps park at the barrier
+  __syncthreads();
+  ptx::tc_fence_after();
+  DPHASE(4);
+
+  // ---- epilogue: TMEM -> smem [n][128] (over raw / window / slab) -> stores ----
+  {
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const int row = warp * 32 + lane;
+    for (int c = 0; c < g.BN; c += 16) {
+      uint32_t r[16];
+      ptx::tmem_ld16(trow + (uint32_t)c, r);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int jj = 0; jj < 16; ++jj)
+        ptx::sts_f32(s_raw + 4u * ((c + jj) * BM + row), __uint_as_float(r[jj]));
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+#ifdef VCNN_PHASE_TIMING
+  if (blockIdx.x == 0 && blockIdx.y == 0)
+    for (int i = tid; i < 256; i += NT) g_dump[3][i] = ptx::lds_f32(s_raw + 4u * i);
+#endif
+  if (g.mode == 0)
+    with_act(a.fe.act, [&](auto A) { fwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0); });
+  else
+    with_act(a.be.act_prev,
+             [&](auto A) { bwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0); });
+  DPHASE(5);
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc(tmem, TMEM_COLS);
+  DPHASE(6);
+}
+
+int launch(const Args& a, cudaStream_t st) {
+  const Geo& g = a.g;
+  dim3 grid((unsigned)(g.B * g.tpi), (unsigned)g.nblk);
+  const size_t smem = (size_t)g.smem;
+  auto go = [&](auto kern, size_t& configured) -> int {
+    if (smem > configured) {
+      VCNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      configured = smem;
+    }
+    kern<<<grid, NT, smem, st>>>(a);
+    VCNN_LAUNCHED();
+    return VCNN_OK;
+  };
+  static size_t cfg32 = 0, cfg64 = 0, cfg128 = 0;
+  if (g.BN <= 32) return go(direct_conv_kernel<32>, cfg32);
+  if (g.BN <= 64) return go(direct_conv_kernel<64>, cfg64);
+  return go(direct_conv_kernel<128>, cfg128);
+}
+
+}  // namespace
+
+bool fwd_ok(const ConvDesc& d, int pool) {
+  Geo g;
+  return plan(d, 0, pool, 0, 0, g);
+}
+bool dgrad_ok(const ConvDesc& d, int pool, int POH, int POW) {
+  Geo g;
+  return plan(d, 1, pool, POH, POW, g);
+}
+size_t pack_floats(const ConvDesc& d, int mode) {
+  Geo g;
+  if (!plan(d, mode, 0, 0, 0, g)) return 0;
+  return (size_t)(pack_floats_per_block(g) * g.nblk);
+}
+
+int pack_weights(const ConvDesc& d, int mode, const float* w, float* pk, cudaStream_t st) {
+  Geo g;
+  if (!plan(d, mode, 0, 0, 0, g)) return fail(VCNN_ESHAPE, "direct conv: geometry not supported");
+  const int64_t n = pack_floats_per_block(g) * g.nblk;
+  int64_t blocks = cdiv(n, 256);
+  if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
+  pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, mode, w, pk);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bias, int act,
+             float* y, const PoolFuse& pf, cudaStream_t st) {
+  Args a{};
+  if (!plan(d, 0, pf.pool, pf.POH, pf.POW, a.g))
+    return fail(VCNN_ESHAPE, "direct conv forward: geometry not supported");
+  a.in = x;
+  a.pack = pk;
+  a.fe.bias = bias;
+  a.fe.act = act;
+  a.fe.y = y;
+  a.fe.pool = pf.pool;
+  a.fe.POH = pf.POH;
+  a.fe.POW = pf.POW;
+  a.fe.py = pf.y;
+  a.fe.parg = pf.arg;
+  return launch(a, st);
+}
+
+int conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* pk, float* dx,
+               const float* yprev, int act_prev, cudaStream_t st) {
+  Args a{};
+  if (!plan(d, 1, gs.pool, gs.POH, gs.POW, a.g))
+    return fail(VCNN_ESHAPE, "direct conv dgrad: geometry not supported");
+  a.in = gs.g;
+  a.gs = gs;
+  a.pack = pk;
+  a.be.dx = dx;
+  a.be.yprev = yprev;
+  a.be.act_prev = act_prev;
+  return launch(a, st);
+}
+
+}  // namespace direct
+}  // namespace vcnn_b200
+
+#ifdef VCNN_PHASE_TIMING
+extern "C" int vcnn_debug_dphases(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_dphase, sizeof(unsigned long long) * 64) ==
+                 cudaSuccess
+             ? 0
+             : 4;
+}
+extern "C" int vcnn_debug_dump(float* out) {
+  return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_dump, sizeof(float) * 1024) ==
+                 cudaSuccess
+             ? 0
+             : 4;
+}
+#endif

@@ -72,21 +72,34 @@ size_t matmul_workspace(int64_t m, int64_t k, int64_t n, int prec) {
 }
 
 int launch_conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
-                    float* y, int prec, const Workspace& ws, cudaStream_t st) {
+                    float* y, int prec, const Workspace& ws, cudaStream_t st, const float* wf) {
   if (prec == VCNN_PREC_FP32) return simt::conv_fwd(d, x, w, b, act, y, st);
+  // TF32 stride-1 convs whose input window fits shared memory: slab kernel
+  if (prec == VCNN_PREC_TF32 && wf && tc::slab_fwd_ok(d, 0))
+    return tc::slab_conv_fwd(d, x, wf, b, act, y, PoolFuse{}, st);
   return tc::conv_fwd(d, x, w, b, act, y, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw,
                       float* db, int prec, const Workspace& ws, cudaStream_t st) {
   if (prec == VCNN_PREC_FP32) return simt::conv_wgrad(d, x, gpre, dw, db, st);
+  if (prec == VCNN_PREC_TF32 && tc::slab_wgrad_ok(d)) {
+    GradSrc gs;
+    gs.g = gpre;
+    return tc::slab_conv_wgrad(d, x, gs, dw, db, ws, st);
+  }
   return tc::conv_wgrad(d, x, gpre, dw, db, prec == VCNN_PREC_3XTF32, ws, st);
 }
 
 int launch_conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
                       const float* yprev, int act_prev, int prec, const Workspace& ws,
-                      cudaStream_t st) {
+                      cudaStream_t st, const float* wt) {
   if (prec == VCNN_PREC_FP32) return simt::conv_dgrad(d, gpre, w, dx, yprev, act_prev, st);
+  if (prec == VCNN_PREC_TF32 && wt && tc::slab_dgrad_ok(d)) {
+    GradSrc gs;
+    gs.g = gpre;
+    return tc::slab_conv_dgrad(d, gs, wt, dx, yprev, act_prev, st);
+  }
   return tc::conv_dgrad(d, gpre, w, dx, yprev, act_prev, prec == VCNN_PREC_3XTF32, ws, st);
 }
 

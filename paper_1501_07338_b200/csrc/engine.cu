@@ -36,6 +36,13 @@ struct LayerRt {
   float* out = nullptr;
   float* gpre = nullptr;
   int32_t* arg = nullptr;
+  // conv: tf32-rounded weight copies for the slab kernels (prep_weights),
+  // refreshed after every parameter update
+  float* wf = nullptr;
+  float* wt = nullptr;
+  // direct (shifted-view) kernels: prepacked tf32 weights, fwd and dgrad
+  float* pf = nullptr;
+  float* pd = nullptr;
 };
 
 // host Rng identical to the reference (common.hpp:51-66): mt19937_64 with
@@ -82,6 +89,10 @@ struct vcnn_net {
   int max_batch = 0;
   int precision = VCNN_PREC_TF32;
   int pool_bwd_mode = VCNN_POOLBWD_EXACT;
+  // fast path: slab kernels + conv->max-pool fusion (TF32); keep_trace forces
+  // every layer output / pre-activation gradient to be materialised
+  bool fuse = true;
+  bool keep_trace = false;
   int64_t nparams = 0;
   float* params = nullptr;
   float* grads = nullptr;
@@ -187,6 +198,66 @@ struct Mark {
   }
 };
 
+// a conv layer whose whole output is one patch (OH = OW = 1, the kernel
+// covers the input) is a fully connected layer over the flattened input:
+// im2col rows (c,ky,kx) == the (c,y,x) flatten order (layers.hpp:224-228)
+bool conv_is_dense(const LayerRt& l) {
+  return l.spec.kind == VCNN_LAYER_CONV && l.out_h == 1 && l.out_w == 1 &&
+         l.spec.kh == l.in_h && l.spec.kw == l.in_w;
+}
+
+
+// conv layer i followed by a max pool that its forward epilogue can compute
+// (non-overlapping windows, no pool bias, identity act, exact backward), with
+// a backward that can route the pool gradient on the fly
+int fused_pool_of(const vcnn_net* n, size_t i, int B) {
+  if (!n->fuse || n->keep_trace || n->precision != VCNN_PREC_TF32 ||
+      n->pool_bwd_mode != VCNN_POOLBWD_EXACT)
+    return 0;
+  if (i + 1 >= n->L.size()) return 0;
+  const LayerRt& l = n->L[i];
+  const LayerRt& p = n->L[i + 1];
+  if (l.spec.kind != VCNN_LAYER_CONV || conv_is_dense(l)) return 0;
+  if (p.spec.kind != VCNN_LAYER_POOL || p.spec.pool_mode != VCNN_POOL_MAX || p.b_len ||
+      p.spec.act != VCNN_ACT_IDENTITY || p.spec.kh != p.spec.kw || p.spec.kh != p.spec.stride ||
+      p.spec.kh < 1)
+    return 0;
+  if (i + 2 >= n->L.size()) return 0;  // the layer above applies the conv act' for the pool
+  const ConvDesc d = conv_of(l, B);
+  const int pz = p.spec.kh;
+  const bool fwd = (l.pf && direct::fwd_ok(d, pz)) || tc::slab_fwd_ok(d, pz);
+  const bool dg = i == 0 || (l.pd && direct::dgrad_ok(d, pz, p.out_h, p.out_w)) ||
+                  tc::slab_dgrad_ok(d, pz, p.out_w);
+  if (!fwd || !dg || !tc::slab_wgrad_ok(d, pz, p.out_h, p.out_w)) return 0;
+  return pz;
+}
+
+int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
+  const cudaStream_t st = n->stream;
+  LayerRt& l = n->L[i];
+  const float* W = n->params + l.w_off;
+  const float* b = n->params + l.b_off;
+  const ConvDesc d = conv_of(l, B);
+  if (conv_is_dense(l))
+    return launch_full_fwd(B, (int)l.in_per, l.spec.units, in, W, b, l.spec.act, l.out,
+                           n->precision, n->ws, st);
+  if (fpool) {
+    LayerRt& p = n->L[i + 1];
+    PoolFuse pf;
+    pf.pool = fpool;
+    pf.POH = p.out_h;
+    pf.POW = p.out_w;
+    pf.y = p.out;
+    pf.arg = p.arg;
+    if (l.pf && direct::fwd_ok(d, fpool))
+      return direct::conv_fwd(d, in, l.pf, b, l.spec.act, nullptr, pf, st);
+    return tc::slab_conv_fwd(d, in, l.wf, b, l.spec.act, nullptr, pf, st);
+  }
+  if (n->precision == VCNN_PREC_TF32 && l.pf && direct::fwd_ok(d, 0))
+    return direct::conv_fwd(d, in, l.pf, b, l.spec.act, l.out, PoolFuse{}, st);
+  return launch_conv_fwd(d, in, W, b, l.spec.act, l.out, n->precision, n->ws, st, l.wf);
+}
+
 int run_forward(vcnn_net* n, int B) {
   const cudaStream_t st = n->stream;
   for (size_t i = 0; i < n->L.size(); ++i) {
@@ -195,8 +266,10 @@ int run_forward(vcnn_net* n, int B) {
     const float* W = n->params + l.w_off;
     const float* b = n->params + l.b_off;
     if (l.spec.kind == VCNN_LAYER_CONV) {
+      const int fpool = fused_pool_of(n, i, B);
       Mark m(n, CONV_F, (int)i, OP_FWD);
-      TRY(launch_conv_fwd(conv_of(l, B), in, W, b, l.spec.act, l.out, n->precision, n->ws, st));
+      TRY(conv_forward(n, i, B, in, fpool));
+      if (fpool) ++i;  // the pool layer ran in the conv epilogue
     } else if (l.spec.kind == VCNN_LAYER_POOL) {
       Mark m(n, POOL_F, (int)i, OP_FWD);
       PoolDesc d = pool_of(l, B);
@@ -223,22 +296,58 @@ int run_backward(vcnn_net* n, int B) {
     LayerRt& l = n->L[i];
     const float* in = i == 0 ? n->x : n->L[i - 1].out;
     const float* yprev = i > 0 ? n->L[i - 1].out : nullptr;
-    const int act_prev = i > 0 ? n->L[i - 1].spec.act : VCNN_ACT_IDENTITY;
+    int act_prev = i > 0 ? n->L[i - 1].spec.act : VCNN_ACT_IDENTITY;
+    // below is a pool fused into its conv: hand down dP * conv_act'(pooled)
+    // (the pooled value is the conv output at the argmax), which the conv's
+    // backward routes through the argmax
+    if (i > 1 && fused_pool_of(n, (size_t)(i - 2), B)) act_prev = n->L[i - 2].spec.act;
     float* gprev = i > 0 ? n->L[i - 1].gpre : nullptr;
     const float* W = n->params + l.w_off;
     float* gW = n->grads + l.w_off;
     float* gB = n->grads + l.b_off;
     if (l.spec.kind == VCNN_LAYER_CONV) {
       ConvDesc d = conv_of(l, B);
+      const int fpool = fused_pool_of(n, (size_t)i, B);
+      GradSrc gs;
+      if (fpool) {  // route the fused pool's gradient on the fly
+        const LayerRt& p = n->L[i + 1];
+        gs.dP = p.gpre;
+        gs.parg = p.arg;
+        gs.pool = fpool;
+        gs.POH = p.out_h;
+        gs.POW = p.out_w;
+      } else {
+        gs.g = l.gpre;
+      }
+      const bool dense = conv_is_dense(l);
       {
         Mark m(n, CONV_B, i, OP_WGRAD);
-        TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, n->ws, st));
+        if (dense)
+          TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
+                                n->ws, st));
+        else if (fpool)
+          TRY(tc::slab_conv_wgrad(d, in, gs, gW, gB, n->ws, st));
+        else
+          TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, n->ws, st));
       }
       if (gprev) {
         Mark m(n, CONV_B, i, OP_DGRAD);
-        TRY(launch_conv_dgrad(d, l.gpre, W, gprev, yprev, act_prev, n->precision, n->ws, st));
+        if (dense)
+          TRY(launch_full_dgrad(B, (int)l.in_per, l.spec.units, l.gpre, W, gprev, yprev, act_prev,
+                                n->precision, n->ws, st));
+        else if (n->precision == VCNN_PREC_TF32 && l.pd &&
+                 direct::dgrad_ok(d, gs.pool, gs.POH, gs.POW))
+          TRY(direct::conv_dgrad(d, gs, l.pd, gprev, yprev, act_prev, st));
+        else if (fpool)
+          TRY(tc::slab_conv_dgrad(d, gs, l.wt, gprev, yprev, act_prev, st));
+        else
+          TRY(launch_conv_dgrad(d, l.gpre, W, gprev, yprev, act_prev, n->precision, n->ws, st,
+                                l.wt));
       }
     } else if (l.spec.kind == VCNN_LAYER_POOL) {
+      // a pool fused into the conv below: its gradient is routed by that
+      // conv's backward (no pool-backward kernel)
+      if (i > 0 && fused_pool_of(n, (size_t)(i - 1), B)) continue;
       PoolDesc d = pool_of(l, B);
       if (l.b_len) {
         Mark m(n, POOL_B, i, OP_WGRAD);
@@ -265,9 +374,22 @@ int run_backward(vcnn_net* n, int B) {
   return VCNN_OK;
 }
 
+// refresh the slab kernels' tf32 weight copies from params
+int prep_weights(vcnn_net* n) {
+  for (LayerRt& l : n->L) {
+    const ConvDesc d = conv_of(l, 1);
+    const float* w = n->params + l.w_off;
+    if (l.wf) TRY(tc::prep_weights(d, w, l.wf, l.wt, n->stream));
+    if (l.pf) TRY(direct::pack_weights(d, 0, w, l.pf, n->stream));
+    if (l.pd) TRY(direct::pack_weights(d, 1, w, l.pd, n->stream));
+  }
+  return VCNN_OK;
+}
+
 int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   Mark m(n, OTHER_B, -1, OP_SGD);
-  return launch_sgd(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, n->stream);
+  TRY(launch_sgd(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, n->stream));
+  return prep_weights(n);
 }
 
 int check_batch(vcnn_net* n, int batch) {
@@ -496,6 +618,20 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
     s = s ? s : dalloc((void**)&l.gpre, ob);
     if (l.spec.kind == VCNN_LAYER_POOL && l.spec.pool_mode == VCNN_POOL_MAX)
       s = s ? s : dalloc((void**)&l.arg, sizeof(int32_t) * (size_t)(l.out_per * max_batch));
+    if (l.spec.kind == VCNN_LAYER_CONV && !conv_is_dense(l)) {
+      // tf32 weight copies: the direct kernels' packs where the geometry
+      // allows, else the slab kernels' plain copies
+      const ConvDesc d1 = conv_of(l, 1);
+      const size_t nf = direct::pack_floats(d1, 0);
+      const bool first = &l == &n->L[0];  // layer 0 has no data gradient
+      const size_t nd = first ? 0 : direct::pack_floats(d1, 1);
+      if (nf) s = s ? s : dalloc((void**)&l.pf, sizeof(float) * nf);
+      if (nd) s = s ? s : dalloc((void**)&l.pd, sizeof(float) * nd);
+      if (!nf || (!first && !nd)) {
+        s = s ? s : dalloc((void**)&l.wf, sizeof(float) * tc::prep_floats_f(d1));
+        s = s ? s : dalloc((void**)&l.wt, sizeof(float) * tc::prep_floats_t(d1));
+      }
+    }
     // scratch (split-K partials, explicit-dgrad dP) for every batch size the
     // net may run -- the split plan depends on the batch
     for (int B = 1; B <= max_batch; ++B) {
@@ -521,6 +657,11 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
         cudaMemset(n->err, 0, sizeof(int) * 4) != cudaSuccess)
       s = fail(VCNN_ECUDA, "net_create: initial upload failed");
   }
+  if (!s) {
+    s = prep_weights(n);
+    if (!s && cudaStreamSynchronize(n->stream) != cudaSuccess)
+      s = fail(VCNN_ECUDA, "net_create: weight preparation failed");
+  }
   if (s) {
     vcnn_net_destroy(n);
     return s;
@@ -538,6 +679,10 @@ int vcnn_net_destroy(vcnn_net* n) {
     cudaFree(l.out);
     cudaFree(l.gpre);
     cudaFree(l.arg);
+    cudaFree(l.wf);
+    cudaFree(l.wt);
+    cudaFree(l.pf);
+    cudaFree(l.pd);
   }
   cudaFree(n->params);
   cudaFree(n->grads);
@@ -600,11 +745,28 @@ int vcnn_net_set_precision(vcnn_net* n, int precision) {
   return VCNN_OK;
 }
 
+int vcnn_net_set_fusion(vcnn_net* n, int enable) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if ((enable != 0) != n->fuse) drop_graph(n);
+  n->fuse = enable != 0;
+  return VCNN_OK;
+}
+
+int vcnn_net_set_trace(vcnn_net* n, int keep) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if ((keep != 0) != n->keep_trace) drop_graph(n);
+  n->keep_trace = keep != 0;
+  return VCNN_OK;
+}
+
 int vcnn_net_get_params(vcnn_net* n, float* host) {
   return copy_out(n, host, n->params, sizeof(float) * n->nparams);
 }
 int vcnn_net_set_params(vcnn_net* n, const float* host) {
-  return copy_in(n, n->params, host, sizeof(float) * n->nparams);
+  TRY(copy_in(n, n->params, host, sizeof(float) * n->nparams));
+  TRY(prep_weights(n));
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  return VCNN_OK;
 }
 int vcnn_net_get_grads(vcnn_net* n, float* host) {
   return copy_out(n, host, n->grads, sizeof(float) * n->nparams);

@@ -68,15 +68,18 @@ int launch_accumulate(const float* values, const int64_t* source, const int64_t*
                       cudaStream_t st);
 
 // ---- GEMM-shaped kernels: SIMT fp32 reference (simt.cu) or tcgen05 (tc.cu) ----
+// wf / wt: prepared weights (tc::prep_weights) enabling the TF32 slab
+// kernels; nullptr -> generic kernels
 int launch_conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
-                    float* y, int prec, const Workspace& ws, cudaStream_t st);
+                    float* y, int prec, const Workspace& ws, cudaStream_t st,
+                    const float* wf = nullptr);
 // dw [K][kd], db [K] from the pre-activation gradient gpre [B][K][OH][OW]
 int launch_conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw,
                       float* db, int prec, const Workspace& ws, cudaStream_t st);
 // dx [B][C][H][W] = col2im(W^T gpre) * act_prev'(yprev)
 int launch_conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
                       const float* yprev, int act_prev, int prec, const Workspace& ws,
-                      cudaStream_t st);
+                      cudaStream_t st, const float* wt = nullptr);
 int launch_full_fwd(int B, int in, int out, const float* x, const float* w, const float* b,
                     int act, float* y, int prec, const Workspace& ws, cudaStream_t st);
 int launch_full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw,
@@ -111,8 +114,62 @@ int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, floa
            bool transB, cudaStream_t st);
 }  // namespace simt
 
+// Source of a conv layer's pre-activation output gradient G [B][K][OH][OW]:
+// materialised (g), or routed on the fly from a fused non-overlapping max
+// pool (pool = window == stride): dP = the pool-output gradient ALREADY
+// multiplied by the conv activation derivative at the argmax (the producer
+// applies it with yprev = pool output, act_prev = conv act), parg = int32
+// global argmax into [B][K][OH][OW].  G = dP at the argmax, 0 elsewhere.
+struct GradSrc {
+  const float* g = nullptr;
+  const float* dP = nullptr;
+  const int32_t* parg = nullptr;
+  int pool = 0;
+  int POH = 0, POW = 0;
+};
+
+// fused max pool written by the conv-forward epilogue
+struct PoolFuse {
+  int pool = 0;  // window == stride; 0 = none
+  int POH = 0, POW = 0;
+  float* y = nullptr;
+  int32_t* arg = nullptr;
+};
+
+// ---- direct (shifted-view) stride-1 conv forward / dgrad (direct.cu, TF32) ----
+namespace direct {
+bool fwd_ok(const ConvDesc& d, int pool);
+bool dgrad_ok(const ConvDesc& d, int pool = 0, int POH = 0, int POW = 0);
+// prepacked tf32 weights: mode 0 forward, 1 dgrad (0 floats: not supported)
+size_t pack_floats(const ConvDesc& d, int mode);
+int pack_weights(const ConvDesc& d, int mode, const float* w, float* pk, cudaStream_t st);
+int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bias, int act,
+             float* y, const PoolFuse& pf, cudaStream_t st);
+int conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* pk, float* dx,
+               const float* yprev, int act_prev, cudaStream_t st);
+}  // namespace direct
+
 // ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----
 namespace tc {
+// Slab kernels (TF32, stride 1): the CTA stages its input window in shared
+// memory once (cp.async), gathers the implicit-GEMM operands from there.
+// *_ok() says whether a geometry fits (else use the generic kernels below).
+// They read PREPARED weights (prep_weights: tf32-rounded, wf = [K][kd4]
+// zero-padded for the forward, wt = [C][K*kh*kw] transposed for dgrad).
+bool slab_fwd_ok(const ConvDesc& d, int pool);
+bool slab_wgrad_ok(const ConvDesc& d, int pool = 0, int POH = 0, int POW = 0);
+bool slab_dgrad_ok(const ConvDesc& d, int pool = 0, int POW = 0);
+size_t slab_wgrad_workspace(const ConvDesc& d);
+size_t prep_floats_f(const ConvDesc& d);
+size_t prep_floats_t(const ConvDesc& d);
+int prep_weights(const ConvDesc& d, const float* w, float* wf, float* wt, cudaStream_t st);
+// y (nullable when pf.pool) = act(conv(x) + b); pf: fused max pool
+int slab_conv_fwd(const ConvDesc& d, const float* x, const float* wf, const float* b, int act,
+                  float* y, const PoolFuse& pf, cudaStream_t st);
+int slab_conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
+                    const Workspace& ws, cudaStream_t st);
+int slab_conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* wt, float* dx,
+                    const float* yprev, int act_prev, cudaStream_t st);
 int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
              float* y, bool split3, const Workspace& ws, cudaStream_t st);
 int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,

@@ -85,6 +85,15 @@ class Network:
         self.precision = Precision(precision)
         check(lib().vcnn_net_set_precision(self._h, int(precision)))
 
+    def set_fusion(self, on=True):
+        """TF32 slab kernels + conv->max-pool fusion (default on)."""
+        check(lib().vcnn_net_set_fusion(self._h, int(bool(on))))
+
+    def set_trace(self, keep=True):
+        """Materialise every layer output / pre-activation gradient (the
+        reference's LayerTrace, variants.hpp:305-323); disables fusion."""
+        check(lib().vcnn_net_set_trace(self._h, int(bool(keep))))
+
     def set_pool_backward_mode(self, mode):
         """Executor::set_pool_backward_mode (variants.hpp:342)."""
         check(lib().vcnn_net_set_pool_backward_mode(self._h, int(mode)))

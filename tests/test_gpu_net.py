@@ -113,6 +113,7 @@ def test_net_vs_reference_fixture(path, prec):
     spec, B = _fixture_nets()[name]
     d = np.load(path)
     net = Network(spec, B, prec)
+    net.set_trace(True)  # per-layer checks read the whole trace
     x, cls, vals = d["x"], d["cls"], d["values"]
     _load(net, spec, x, cls, vals)
     net.forward_backward(B)
@@ -139,7 +140,8 @@ def test_net_vs_reference_fixture(path, prec):
     else:
         assert normwise(net.get_grads(), d["grads_paper_nn"]) < 0.3
     net.set_pool_backward_mode(S.PoolBackwardMode.exact)
-    # N steps, weights after
+    # N steps on the production path (fusion on), weights after
+    net.set_trace(False)
     for _ in range(int(d["steps"])):
         net.train_step(B, float(d["lr"]), float(d["mom"]))
     p = net.get_params()
@@ -177,6 +179,7 @@ def test_net_vs_oracle_10_steps(name, prec):
     spec, B = PARITY_NETS[name]
     x, cls, vals = O.synth_bench_data(spec, B, 8)
     net = Network(spec, B, prec)
+    net.set_trace(True)
     _load(net, spec, x, cls, vals)
     net.forward_backward(B)
     p0 = net.get_params().astype(np.float64)
@@ -193,7 +196,8 @@ def test_net_vs_oracle_10_steps(name, prec):
     if strict:
         assert_close(net.get_grads(), r["grads"], 5 * tol, "grads")
     teacher_forced(net, spec, x, B, tol)
-    # 10 steps
+    # 10 steps on the production path (fusion on)
+    net.set_trace(False)
     p, v = p0.copy(), np.zeros_like(p0)
     for _ in range(10):
         net.train_step(B, 0.01, 0.9)
@@ -218,6 +222,7 @@ def test_pool_argmax_bit_exact_in_net():
     B = 8
     x, cls, _ = O.synth_bench_data(spec, B, 8)
     net = Network(spec, B, Precision.fp32)
+    net.set_trace(True)
     _load(net, spec, x, cls, None)
     net.forward(B)
     # feed each pool the GPU's own conv output so the comparison isolates pooling
@@ -349,6 +354,7 @@ def test_full_size_step_vs_oracle(name, B):
     spec = S.PRESETS[name]()
     x, cls, _ = O.synth_bench_data(spec, B, 8)
     net = Network(spec, B, Precision.tf32)
+    net.set_trace(True)
     _load(net, spec, x, cls, None)
     net.forward_backward(B)
     r = O.net_run_batch(spec, net.get_params().astype(np.float64), f32(x), cls=cls)
@@ -377,3 +383,30 @@ def test_big_batch_and_presets_run():
         net.forward_backward(B)
         assert net.loss() < l0, name
         net.close()
+
+
+@pytest.mark.parametrize("name,B", [("cifar3", 128), ("cifar3", 37), ("lenet-caffe", 100),
+                                    ("scale1-analog", 8)])
+def test_fused_path_bitwise_equals_trace_path(name, B):
+    """conv->max-pool fusion (pool in the conv epilogue, pool backward routed
+    inside the conv's wgrad / dgrad) changes no bit: loss, output, every
+    gradient and the weights after 3 SGD steps equal the unfused trace path,
+    whose layers are checked against the oracle above."""
+    spec = S.PRESETS[name]() if name in S.PRESETS else PARITY_NETS[name][0]
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    res = []
+    for trace in (True, False):
+        net = Network(spec, B, Precision.tf32)
+        net.set_trace(trace)
+        _load(net, spec, x, cls, None)
+        net.forward_backward(B)
+        out, loss, g = net.output(B), net.loss(), net.get_grads()
+        for _ in range(3):
+            net.train_step(B, 0.01, 0.9)
+        res.append((out, loss, g, net.get_params(), net.kernels_per_step()))
+        net.close()
+    (o0, l0, g0, p0, k0), (o1, l1, g1, p1, k1) = res
+    assert np.array_equal(o0, o1) and l0 == l1
+    assert np.array_equal(g0, g1)
+    assert np.array_equal(p0, p1)
+    assert k1 < k0, (k1, k0)  # the fused step launches fewer kernels
