@@ -39,6 +39,7 @@ namespace {
 
 constexpr int NT = 128;
 constexpr int BM = 128;
+constexpr int EPS = BM + 1;  // epilogue tile row stride (floats): conflict-free per-map reads
 constexpr size_t kSmemOptin = 227 * 1024;
 
 struct Geo {
@@ -106,7 +107,7 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   for (int bn = g.Cout > 128 ? 128 : (int)((g.Cout + 15) / 16 * 16); bn >= 16; bn -= 16) {
     const int b_bytes = g.kh * g.kw * g.CG * bn * 32;
     // the epilogue tile [bn][128] reuses raw + window + A (all dead by then)
-    const int ep_bytes = bn * BM * 4;
+    const int ep_bytes = bn * EPS * 4;
     const int tail = raw_bytes + win_bytes + a_bytes > ep_bytes ? raw_bytes + win_bytes + a_bytes
                                                                 : ep_bytes;
     const int total = b_bytes + tail + 1024;
@@ -202,7 +203,7 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
         float* yp = e.y + plane0 * ohw + (int64_t)(r0 + r) * g.Wout + x;
         const uint32_t ep = eb + 4u * (r * g.Wg + x);
         for (int n = 0; n < nmaps; ++n)
-          yp[n * ohw] = actf<ACT>(ptx::lds_f32(ep + 4u * (n * BM)) + __ldg(e.bias + n0 + n));
+          yp[n * ohw] = actf<ACT>(ptx::lds_f32(ep + 4u * (n * EPS)) + __ldg(e.bias + n0 + n));
       }
   }
   if (e.pool) {
@@ -210,13 +211,20 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
     int nwr = (r0 + nr) / p - r0 / p;  // complete window rows of this tile
     if (r0 / p + nwr > e.POH) nwr = e.POH - r0 / p;
     const int64_t pplane = (int64_t)e.POH * e.POW;
-    for (int wr = warp; wr < nwr; wr += NT / 32)
-      for (int wc = lane; wc < e.POW; wc += 32) {
-        const int ry = wr * p, cx = wc * p;
-        const int64_t o0 = plane0 * pplane + (int64_t)(r0 / p + wr) * e.POW + wc;
-        for (int n = 0; n < nmaps; ++n) {
-          const float bn_ = __ldg(e.bias + n0 + n);
-          const uint32_t en = eb + 4u * (n * BM);
+    // lane = map (window loop per warp): all lanes busy for narrow pools
+    const int nwin = nwr * e.POW;
+    for (int n = lane; n < nmaps; n += 32) {
+      const float bn_ = __ldg(e.bias + n0 + n);
+      const uint32_t en = eb + 4u * (n * EPS);
+      int wr = 0, wc = warp;
+      while (wc >= e.POW) {
+        wc -= e.POW;
+        ++wr;
+      }
+      for (int w = warp; w < nwin; w += NT / 32) {
+        {
+          const int ry = wr * p, cx = wc * p;
+          const int64_t o0 = plane0 * pplane + (int64_t)(r0 / p + wr) * e.POW + wc;
           float best = actf<ACT>(ptx::lds_f32(en + 4u * (ry * g.Wg + cx)) + bn_);
           int by = 0, bx = 0;
           for (int u = 0; u < p; ++u)
@@ -232,33 +240,54 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
           e.parg[o0 + n * pplane] =
               (int32_t)((plane0 + n) * ohw + (int64_t)(r0 + ry + by) * g.Wout + cx + bx);
         }
+        wc += NT / 32;  // next window of this warp (row-major over the tile's windows)
+        while (wc >= e.POW) {
+          wc -= e.POW;
+          ++wr;
+        }
       }
+    }
   }
 }
 
+// dgrad epilogue: lane = output position of the tile (coalesced along x),
+// warp = channel slice; the yprev loads of 16 (position, channel) pairs are
+// in flight together (read-only path).
 template <int ACT>
 __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) {
   const Geo& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nr = g.Hout - r0 < g.R ? g.Hout - r0 : g.R;
   const int nch = g.Cout - n0 < g.BN ? g.Cout - n0 : g.BN;
+  const int npix = nr * g.Wout;
   const int64_t hw = (int64_t)g.Hout * g.Wout;
   const int64_t plane0 = (int64_t)b * g.Cout + n0;
-  for (int r = warp; r < nr; r += NT / 32)
-    for (int x = lane; x < g.Wout; x += 32) {
-      const int64_t o = plane0 * hw + (int64_t)(r0 + r) * g.Wout + x;
-      const uint32_t ep = eb + 4u * (r * g.Wg + x);
-      for (int c = 0; c < nch; ++c) {
-        float v = ptx::lds_f32(ep + 4u * (c * BM));
-        if (a.be.yprev) {
-          const float yv = a.be.yprev[o + c * hw];
-          if (ACT == VCNN_ACT_RELU) v *= yv > 0.f ? 1.f : 0.f;
-          else if (ACT == VCNN_ACT_SIGMOID) v *= yv * (1.f - yv);
-          else if (ACT == VCNN_ACT_TANH) v *= 1.f - yv * yv;
+  const float* yp = a.be.yprev;
+  for (int p = lane; p < npix; p += 32) {
+    const int r = p / g.Wout, x = p - r * g.Wout;
+    const int64_t o = plane0 * hw + (int64_t)(r0 + r) * g.Wout + x;
+    const uint32_t ep = eb + 4u * (r * g.Wg + x);
+    for (int c0 = warp; c0 < nch; c0 += 4 * 16) {
+      float yv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int c = c0 + 4 * u;
+        yv[u] = (yp && c < nch) ? __ldg(yp + o + c * hw) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int c = c0 + 4 * u;
+        if (c >= nch) break;
+        float v = ptx::lds_f32(ep + 4u * (c * EPS));
+        if (yp) {
+          if (ACT == VCNN_ACT_RELU) v *= yv[u] > 0.f ? 1.f : 0.f;
+          else if (ACT == VCNN_ACT_SIGMOID) v *= yv[u] * (1.f - yv[u]);
+          else if (ACT == VCNN_ACT_TANH) v *= 1.f - yv[u] * yv[u];
         }
         a.be.dx[o + c * hw] = v;
       }
     }
+  }
 }
 
 template <class F>
@@ -358,14 +387,28 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
     __syncthreads();
     const uint32_t s_pos = ptx::smem_u32(pos_off);
     const int hw = g.Hin * g.Win;
-    for (int ch = 0; ch < 2 * g.CG; ++ch) {  // ch = cg*2 + half: channels ch*4 .. ch*4+3
-      const uint32_t dst = s_a + (uint32_t)ch * (uint32_t)g.NP * 16u;
-      for (int j = tid; j < 4 * g.NP; j += NT) {
-        const int c = ch * 4 + (j & 3);
-        const int off = ptx::lds_s32(s_pos + 4u * (j >> 2));
-        float v = 0.f;
-        if (c < g.Cin && off >= 0) v = ptx::to_tf32(ptx::lds_f32(s_raw + 4u * (c * hw + off)));
-        ptx::sts_f32(dst + 4u * j, v);
+    const uint32_t hstride = (uint32_t)g.NP * 16u;  // bytes per (cg, half) block
+    // j = (position, channel%4); the channel-group loop inside keeps 4
+    // independent loads in flight per thread
+    for (int j = tid; j < 4 * g.NP; j += NT) {
+      const int off = ptx::lds_s32(s_pos + 4u * (j >> 2));
+      const int c4 = j & 3;
+      const uint32_t dst = s_a + 4u * j;
+      int ch = 0;
+      for (; ch + 3 < 2 * g.CG; ch += 4) {
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = (ch + u) * 4 + c4;
+          v[u] = (c < g.Cin && off >= 0) ? ptx::lds_f32(s_raw + 4u * (c * hw + off)) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ptx::sts_f32(dst + (uint32_t)(ch + u) * hstride, ptx::to_tf32(v[u]));
+      }
+      for (; ch < 2 * g.CG; ++ch) {
+        const int c = ch * 4 + c4;
+        const float v = (c < g.Cin && off >= 0) ? ptx::lds_f32(s_raw + 4u * (c * hw + off)) : 0.f;
+        ptx::sts_f32(dst + (uint32_t)ch * hstride, ptx::to_tf32(v));
       }
     }
   }
@@ -385,8 +428,9 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
 #endif
 
   DPHASE(3);
-  // ---- one thread issues every MMA ----
-  if (tid == 0) {
+  // ---- one elected lane of warp 0 issues every MMA (converged warp: the
+  // tcgen05 issue stays on the uniform datapath) ----
+  if (warp == 0 && ptx::elect_one()) {
     const uint32_t idesc = ptx::idesc_tf32(BM, g.BN);  // both operands K-major
     const uint32_t half = (uint32_t)g.NP * 16u;          // LBO: the two 4-channel halves
     // descriptors advance by plain additions on the start-address field
@@ -409,6 +453,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
     }
     ptx::mma_commit(&done_bar);
   }
+  __syncwarp();
   if (warp == 0) ptx::mbar_wait(&done_bar, 0);  // the other warps park at the barrier
   __syncthreads();
   ptx::tc_fence_after();
@@ -424,7 +469,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
       ptx::tmem_wait_ld();
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj)
-        ptx::sts_f32(s_raw + 4u * ((c + jj) * BM + row), __uint_as_float(r[jj]));
+        ptx::sts_f32(s_raw + 4u * ((c + jj) * EPS + row), __uint_as_float(r[jj]));
     }
   }
   ptx::tc_fence_before();

@@ -253,7 +253,7 @@ constexpr int kLossThreads = 1024;
 __global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(
     int B, int units, const float* __restrict__ pred, const int* __restrict__ cls,
     float* __restrict__ loss, float* __restrict__ grad, int act_last, int* err) {
-  __shared__ float red[kLossThreads];
+  __shared__ float red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
   const float inv_b = 1.0f / (float)B;
@@ -282,14 +282,15 @@ __global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(
     }
     if (!bad) mine += m + logf(s) - l[c];
   }
-  // fixed-order tree over the warps' partial sums -> deterministic
-  red[threadIdx.x] = lane == 0 ? mine : 0.f;
+  // fixed-order reduction of the warps' partial sums -> deterministic
+  if (lane == 0) red[warp] = mine;
   __syncthreads();
-  for (int st = kLossThreads / 2; st > 0; st >>= 1) {
-    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
-    __syncthreads();
+  if (warp == 0) {
+    float v = lane < nwarps ? red[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && loss) *loss = v / (float)B;
   }
-  if (threadIdx.x == 0 && loss) *loss = red[0] / (float)B;
 }
 
 // MSE (layers.hpp:425-433, :461-467): loss = mean (p-t)^2, grad 2(p-t)/n
@@ -489,9 +490,19 @@ __global__ void full_fwd_simt(int B, int in, int out, const float* __restrict__ 
     const int64_t bb = i / out;
     const float* xr = x + bb * in;
     const float* wr = w + (int64_t)o * in;
-    float acc = 0.f;
-    for (int k = 0; k < in; ++k) acc += xr[k] * wr[k];
-    y[i] = act_fwd(act, acc + b[o]);
+    // 4 independent partial sums (loads of 4 iterations in flight), fixed
+    // combination order -> deterministic
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int k = 0;
+#pragma unroll 2
+    for (; k + 3 < in; k += 4) {
+      a0 += xr[k] * wr[k];
+      a1 += xr[k + 1] * wr[k + 1];
+      a2 += xr[k + 2] * wr[k + 2];
+      a3 += xr[k + 3] * wr[k + 3];
+    }
+    for (; k < in; ++k) a0 += xr[k] * wr[k];
+    y[i] = act_fwd(act, ((a0 + a1) + (a2 + a3)) + b[o]);
   }
 }
 
@@ -504,13 +515,28 @@ __global__ void full_wgrad_simt(int B, int in, int out, const float* __restrict_
        t += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(t % (in + 1));
     const int o = (int)(t / (in + 1));
-    float acc = 0.f;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int bb = 0;
     if (i < in) {
-      for (int bb = 0; bb < B; ++bb) acc += g[(int64_t)bb * out + o] * x[(int64_t)bb * in + i];
-      dw[(int64_t)o * in + i] = acc;
+#pragma unroll 2
+      for (; bb + 3 < B; bb += 4) {
+        a0 += g[(int64_t)bb * out + o] * x[(int64_t)bb * in + i];
+        a1 += g[(int64_t)(bb + 1) * out + o] * x[(int64_t)(bb + 1) * in + i];
+        a2 += g[(int64_t)(bb + 2) * out + o] * x[(int64_t)(bb + 2) * in + i];
+        a3 += g[(int64_t)(bb + 3) * out + o] * x[(int64_t)(bb + 3) * in + i];
+      }
+      for (; bb < B; ++bb) a0 += g[(int64_t)bb * out + o] * x[(int64_t)bb * in + i];
+      dw[(int64_t)o * in + i] = (a0 + a1) + (a2 + a3);
     } else {
-      for (int bb = 0; bb < B; ++bb) acc += g[(int64_t)bb * out + o];
-      db[o] = acc;
+#pragma unroll 2
+      for (; bb + 3 < B; bb += 4) {
+        a0 += g[(int64_t)bb * out + o];
+        a1 += g[(int64_t)(bb + 1) * out + o];
+        a2 += g[(int64_t)(bb + 2) * out + o];
+        a3 += g[(int64_t)(bb + 3) * out + o];
+      }
+      for (; bb < B; ++bb) a0 += g[(int64_t)bb * out + o];
+      db[o] = (a0 + a1) + (a2 + a3);
     }
   }
 }
@@ -523,8 +549,17 @@ __global__ void full_dgrad_simt(int B, int in, int out, const float* __restrict_
        t += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(t % in);
     const int64_t bb = t / in;
-    float acc = 0.f;
-    for (int o = 0; o < out; ++o) acc += g[bb * out + o] * w[(int64_t)o * in + i];
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int o = 0;
+#pragma unroll 2
+    for (; o + 3 < out; o += 4) {
+      a0 += g[bb * out + o] * w[(int64_t)o * in + i];
+      a1 += g[bb * out + o + 1] * w[(int64_t)(o + 1) * in + i];
+      a2 += g[bb * out + o + 2] * w[(int64_t)(o + 2) * in + i];
+      a3 += g[bb * out + o + 3] * w[(int64_t)(o + 3) * in + i];
+    }
+    for (; o < out; ++o) a0 += g[bb * out + o] * w[(int64_t)o * in + i];
+    float acc = (a0 + a1) + (a2 + a3);
     if (yprev) acc *= act_grad_from_out(act_prev, yprev[t]);
     dx[t] = acc;
   }

@@ -235,8 +235,9 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
   constexpr uint32_t IDESC = ptx::idesc_tf32(BM, BN);
 
   if (warp == 4) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (one elected lane of a converged warp, so
+    // the tcgen05 issue stays on the uniform datapath) ----------------
+    if (ptx::elect_one()) {
       PHASE_ACC_DECL
       for (int it = 0; it < nkb; ++it) {
         const int s = it % S;
@@ -670,7 +671,7 @@ struct ConvDgradProb : KRange {
   __device__ __forceinline__ void store(int64_t ec, int c, float v) const {
     if (ec < 0 || c >= d.C) return;
     const int64_t i = ec + (int64_t)c * d.H * d.W;
-    if (yprev) v *= epi_dact(act_prev, yprev[i]);
+    if (yprev) v *= epi_dact(act_prev, __ldg(yprev + i));
     dx[i] = v;
   }
 };
@@ -1158,7 +1159,7 @@ struct SlabDgradProb : KRange {
   __device__ __forceinline__ void store(int64_t ec, int c, float v) const {
     if (ec < 0 || c >= d.C) return;
     const int64_t i = ec + (int64_t)c * d.H * d.W;
-    if (yprev) v *= epi_dact(act_prev, yprev[i]);
+    if (yprev) v *= epi_dact(act_prev, __ldg(yprev + i));
     dx[i] = v;
   }
 };
@@ -1229,7 +1230,7 @@ struct DenseProb : KRange {
       case EPI_BIAS_ACT: c[m * ldc + n] = epi_act(act, v + bias[n]); break;
       case EPI_DACT: {
         const int64_t i = m * ldc + n;
-        c[i] = yprev ? v * epi_dact(act, yprev[i]) : v;
+        c[i] = yprev ? v * epi_dact(act, __ldg(yprev + i)) : v;
         break;
       }
       case EPI_WGRAD:
@@ -1275,6 +1276,9 @@ Plan make_plan(int64_t M, int64_t N, int64_t K, int tables, int min_kb = 2) {
   p.N = N;
   p.tables = tables;
   p.bn = pick_bn(N);
+  // few M tiles and a wide N: narrower N tiles spread the work over more
+  // CTAs (a BN=256 tile is 4x the gather work of one SM at BN=64)
+  while (p.bn > 32 && cdiv(M, BM) * cdiv(N, p.bn) < sm_count() / 2) p.bn /= 2;
   p.mt = cdiv(M, BM);
   p.nt = cdiv(N, p.bn);
   p.kb_total = (int)cdiv(K, BK);

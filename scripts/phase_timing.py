@@ -75,3 +75,13 @@ for name, (C_, H, K, k) in {"conv1": (3, 32, 32, 5), "conv2": (32, 14, 32, 5)}.i
     phases(f"{name} wgrad", lambda: ops.conv_backward(x, w, y, dy, k, k, need_dx=False))
     if name == "conv2":
         dphases(f"{name} dgrad", lambda: ops.conv_backward(x, w, y, dy, k, k))
+
+# the routed dgrad inside a CIFAR-3 training step (last direct launch of backward)
+from paper_1501_07338_b200 import spec as S  # noqa: E402
+from paper_1501_07338_b200.engine import Network  # noqa: E402
+
+net = Network(S.cifar3(), 128)
+xb = torch.rand(128, 3 * 32 * 32, device="cuda")
+cb = torch.randint(0, 10, (128,), device="cuda", dtype=torch.int32)
+net.load_batch(xb, cls=cb)
+dphases("cifar3 conv2 dgrad (routed, in net)", lambda: net.forward_backward(128))
