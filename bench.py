@@ -275,10 +275,13 @@ def main():
         def step():
             net.train_step(B, lr, mom)
     else:
+        from paper_1501_07338_b200.dp import DataParallel
+        dp = DataParallel(net)
+
         def eager_step():
-            net.forward_backward(B)
-            dist.all_reduce(grads)           # NCCL over NVLink, fp32 sum
-            net.sgd_step(lr, mom, 1.0 / world)
+            # run_batch(shard) -> NCCL all-reduce over NVLink (fp32 sum of the
+            # one flat gradient buffer) -> replicated sgd_step(grad_scale 1/N)
+            dp.step(B, B * world, lr, mom)
         step = eager_step
         if not args.no_graph:
             try:

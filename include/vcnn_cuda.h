@@ -107,6 +107,9 @@ const char* vcnn_last_error(void);
 int vcnn_device_info(int* sm_count, int* cc_major, int* cc_minor);
 /* kernels launched by this library since load (gpu_launches evidence) */
 int64_t vcnn_launch_count(void);
+/* synchronous host -> device copy (lets C / C++ hosts stage batches without
+ * CUDA headers); VCNN_ECUDA without a device */
+int vcnn_copy_h2d(void* dev, const void* host, size_t bytes);
 
 /* ------------------------------------------------------------------------ */
 /* geometry (host only, no device needed)                                    */

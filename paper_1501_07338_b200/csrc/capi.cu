@@ -94,6 +94,12 @@ struct Scratch {
 
 extern "C" {
 
+int vcnn_copy_h2d(void* dev, const void* host, size_t bytes) {
+  TRY(require_device());
+  VCNN_CUDA_TRY(cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice));
+  return VCNN_OK;
+}
+
 int vcnn_abi_version(void) { return VCNN_ABI_VERSION; }
 const char* vcnn_last_error(void) { return last_error(); }
 int64_t vcnn_launch_count(void) { return g_launches.load(); }

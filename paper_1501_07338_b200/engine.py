@@ -140,6 +140,11 @@ class Network:
         mk = lambda q: torch.as_tensor(_DevBuf(q.value, (self.nparams,), "<f4"), device="cuda")
         return mk(p), mk(g), mk(v)
 
+    def grads_tensor(self):
+        """The flat gradient buffer (NetGrads order) as a torch CUDA view:
+        the one buffer a data-parallel step all-reduces (dp.DataParallel)."""
+        return self.device_tensors()[1]
+
     def input_tensors(self):
         """(x [max_batch, in], cls [max_batch], values [max_batch, units]) views."""
         x, c, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
