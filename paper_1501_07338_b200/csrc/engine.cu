@@ -104,6 +104,13 @@ struct vcnn_net {
   float* loss = nullptr;
   int* err = nullptr;
   Workspace ws;
+  // backward runs weight gradients on a side stream, concurrently with the
+  // data-gradient chain (separate split-K workspace); per-layer fork events
+  // and one join event.  Captured into the graph as parallel branches.
+  cudaStream_t side = nullptr;
+  Workspace ws2;
+  std::vector<cudaEvent_t> fork_ev;
+  cudaEvent_t join_ev = nullptr;
   cudaStream_t stream = nullptr;
   // graph replay
   bool use_graph = false;
@@ -292,8 +299,17 @@ int run_backward(vcnn_net* n, int B) {
     TRY(launch_loss(n->spec.loss, B, (int)n->out_units, last.out, n->cls, n->values, n->loss,
                     last.gpre, last.spec.act, n->err, st));
   }
+  // weight gradients on the side stream (not in breakdown mode, whose
+  // per-op events live on the main stream)
+  const bool par = n->side && !n->breakdown;
+  const cudaStream_t sw = par ? n->side : st;
+  const Workspace& wsw = par ? n->ws2 : n->ws;
   for (int i = (int)n->L.size() - 1; i >= 0; --i) {
     LayerRt& l = n->L[i];
+    if (par) {  // this layer's gradient inputs are ready on the main stream
+      VCNN_CUDA_TRY(cudaEventRecord(n->fork_ev[i], st));
+      VCNN_CUDA_TRY(cudaStreamWaitEvent(n->side, n->fork_ev[i], 0));
+    }
     const float* in = i == 0 ? n->x : n->L[i - 1].out;
     const float* yprev = i > 0 ? n->L[i - 1].out : nullptr;
     int act_prev = i > 0 ? n->L[i - 1].spec.act : VCNN_ACT_IDENTITY;
@@ -324,11 +340,11 @@ int run_backward(vcnn_net* n, int B) {
         Mark m(n, CONV_B, i, OP_WGRAD);
         if (dense)
           TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
-                                n->ws, st));
+                                wsw, sw));
         else if (fpool)
-          TRY(tc::slab_conv_wgrad(d, in, gs, gW, gB, n->ws, st));
+          TRY(tc::slab_conv_wgrad(d, in, gs, gW, gB, wsw, sw));
         else
-          TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, n->ws, st));
+          TRY(launch_conv_wgrad(d, in, l.gpre, gW, gB, n->precision, wsw, sw));
       }
       if (gprev) {
         Mark m(n, CONV_B, i, OP_DGRAD);
@@ -351,7 +367,7 @@ int run_backward(vcnn_net* n, int B) {
       PoolDesc d = pool_of(l, B);
       if (l.b_len) {
         Mark m(n, POOL_B, i, OP_WGRAD);
-        TRY(launch_pool_bias_grad(d, l.gpre, gB, st));
+        TRY(launch_pool_bias_grad(d, l.gpre, gB, sw));
       }
       if (gprev) {
         Mark m(n, POOL_B, i, OP_DGRAD);
@@ -362,7 +378,7 @@ int run_backward(vcnn_net* n, int B) {
       {
         Mark m(n, FULL_B, i, OP_WGRAD);
         TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
-                              n->ws, st));
+                              wsw, sw));
       }
       if (gprev) {
         Mark m(n, FULL_B, i, OP_DGRAD);
@@ -370,6 +386,10 @@ int run_backward(vcnn_net* n, int B) {
                               n->precision, n->ws, st));
       }
     }
+  }
+  if (par) {  // join: the update (and any host read) sees every gradient
+    VCNN_CUDA_TRY(cudaEventRecord(n->join_ev, n->side));
+    VCNN_CUDA_TRY(cudaStreamWaitEvent(st, n->join_ev, 0));
   }
   return VCNN_OK;
 }
@@ -646,6 +666,17 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
   if (wsb) {
     s = s ? s : dalloc((void**)&n->ws.ptr, wsb);
     n->ws.bytes = wsb;
+    s = s ? s : dalloc((void**)&n->ws2.ptr, wsb);
+    n->ws2.bytes = wsb;
+  }
+  if (!s) {
+    n->fork_ev.assign(n->L.size(), nullptr);
+    for (auto& e : n->fork_ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+        s = fail(VCNN_ECUDA, "net_create: event");
+    if (!s && (cudaEventCreateWithFlags(&n->join_ev, cudaEventDisableTiming) != cudaSuccess ||
+               cudaStreamCreateWithFlags(&n->side, cudaStreamNonBlocking) != cudaSuccess))
+      s = fail(VCNN_ECUDA, "net_create: side stream");
   }
   if (!s) {
     if (cudaMemcpy(n->params, hp.data(), sizeof(float) * (size_t)n->nparams,
@@ -693,6 +724,11 @@ int vcnn_net_destroy(vcnn_net* n) {
   cudaFree(n->loss);
   cudaFree(n->err);
   cudaFree(n->ws.ptr);
+  cudaFree(n->ws2.ptr);
+  for (cudaEvent_t e : n->fork_ev)
+    if (e) cudaEventDestroy(e);
+  if (n->join_ev) cudaEventDestroy(n->join_ev);
+  if (n->side) cudaStreamDestroy(n->side);
   if (n->cap_stream) cudaStreamDestroy(n->cap_stream);
   for (cudaEvent_t e : n->event_pool) cudaEventDestroy(e);
   delete n;
