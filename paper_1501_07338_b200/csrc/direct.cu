@@ -28,6 +28,7 @@
 // (layers.hpp:179) + apply_activation_grad (layers.hpp:57-61).
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
@@ -532,6 +533,78 @@ int pack_weights(const ConvDesc& d, int mode, const float* w, float* pk, cudaStr
   int64_t blocks = cdiv(n, 256);
   if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
   pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, mode, w, pk);
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+// ---- fused SGD + weight packing: one launch per update ---------------------
+namespace {
+constexpr int kMaxPackLayers = 8;
+struct PackLayer {
+  int64_t w_off, w_len;  // the layer's weight range in the flat params
+  Geo gf, gd;            // fwd / dgrad pack geometry (BN, CG, nblk, ...)
+  float* pf;
+  float* pd;
+  int K, C, kh, kw;
+};
+struct PackTable {
+  int n;
+  PackLayer L[kMaxPackLayers];
+};
+
+// offset of (row = GEMM N index, ch = GEMM K index, s = ky*kw+kx) in a pack
+__device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int s) {
+  const int nb = row / g.BN, r = row - nb * g.BN, cg = ch >> 3, kk = ch & 7;
+  return ((((int64_t)nb * g.kh * g.kw + s) * g.CG + cg) * (g.BN / 8) + (r >> 3)) * 64 +
+         (kk >> 2) * 32 + (r & 7) * 4 + (kk & 3);
+}
+
+// sgd_step (network.hpp:242-273): v = mom*v + scale*g; w -= lr*v; and the
+// updated conv weights are written straight into the direct kernels' packs
+// (fwd: row n, channel c, s = ky*kw+kx; dgrad: row c, channel n, flipped s)
+__global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
+                                const float* __restrict__ g, float lr, float mom, float scale,
+                                const PackTable t) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float vi = mom * v[i] + scale * g[i];
+    const float wi = w[i] - lr * vi;
+    v[i] = vi;
+    w[i] = wi;
+    for (int l = 0; l < t.n; ++l) {
+      const PackLayer& L = t.L[l];
+      const int64_t k = i - L.w_off;
+      if (k < 0 || k >= L.w_len) continue;
+      const int khw = L.kh * L.kw, kd = L.C * khw;
+      const int nn = (int)(k / kd), rem = (int)(k - (int64_t)nn * kd);
+      const int c = rem / khw, s = rem - c * khw;
+      const float q = ptx::to_tf32(wi);
+      if (L.pf) L.pf[pack_index(L.gf, nn, c, s)] = q;
+      if (L.pd) L.pd[pack_index(L.gd, c, nn, khw - 1 - s)] = q;
+    }
+  }
+}
+}  // namespace
+
+int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+             const std::vector<PackSpec>& layers, cudaStream_t st) {
+  PackTable t{};
+  for (const PackSpec& p : layers) {
+    if (!p.pf && !p.pd) continue;
+    if (t.n == kMaxPackLayers) return fail(VCNN_ECONFIG, "sgd_pack: too many conv layers");
+    PackLayer& L = t.L[t.n++];
+    L.w_off = p.w_off;
+    L.w_len = p.d.kd() * p.d.K;
+    L.pf = p.pf;
+    L.pd = p.pd;
+    L.K = p.d.K, L.C = p.d.C, L.kh = p.d.kh, L.kw = p.d.kw;
+    if (p.pf && !plan(p.d, 0, 0, 0, 0, L.gf)) return fail(VCNN_ESHAPE, "sgd_pack: fwd plan");
+    if (p.pd && !plan(p.d, 1, 0, 0, 0, L.gd)) return fail(VCNN_ESHAPE, "sgd_pack: dgrad plan");
+  }
+  int64_t blocks = cdiv(n, 256);
+  if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
+  if (blocks < 1) blocks = 1;
+  sgd_pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, w, v, g, lr, mom, scale, t);
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

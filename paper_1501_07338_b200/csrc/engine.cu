@@ -408,8 +408,20 @@ int prep_weights(vcnn_net* n) {
 
 int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   Mark m(n, OTHER_B, -1, OP_SGD);
-  TRY(launch_sgd(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, n->stream));
-  return prep_weights(n);
+  // one launch: the update + the direct kernels' weight packs; only layers
+  // on the slab fallback still need their plain tf32 copies refreshed
+  std::vector<direct::PackSpec> packs;
+  bool slab_copies = false;
+  for (LayerRt& l : n->L) {
+    if (l.pf || l.pd) packs.push_back({conv_of(l, 1), l.w_off, l.pf, l.pd});
+    slab_copies = slab_copies || l.wf;
+  }
+  TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
+                       n->stream));
+  if (!slab_copies) return VCNN_OK;
+  for (LayerRt& l : n->L)
+    if (l.wf) TRY(tc::prep_weights(conv_of(l, 1), n->params + l.w_off, l.wf, l.wt, n->stream));
+  return VCNN_OK;
 }
 
 int check_batch(vcnn_net* n, int batch) {

@@ -5,6 +5,8 @@
 // into the kernel that produces the gradient (no standalone act' pass).
 #pragma once
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace vcnn_b200 {
@@ -147,6 +149,16 @@ int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bi
              float* y, const PoolFuse& pf, cudaStream_t st);
 int conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* pk, float* dx,
                const float* yprev, int act_prev, cudaStream_t st);
+// sgd_step fused with the refresh of the conv layers' packs (pf / pd may be
+// null); pack padding must already be zero (pack_weights at creation)
+struct PackSpec {
+  ConvDesc d;
+  int64_t w_off;
+  float* pf;
+  float* pd;
+};
+int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+             const std::vector<PackSpec>& layers, cudaStream_t st);
 }  // namespace direct
 
 // ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----
