@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "vcnn_cuda.h"
 
@@ -31,6 +32,39 @@ extern std::atomic<int64_t> g_launches;
     cudaError_t _e = cudaGetLastError();                                  \
     if (_e != cudaSuccess) return ::vcnn_b200::cuda_fail(_e, "launch");   \
   } while (0)
+
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// Every kernel is launched with programmatic stream serialisation: it lets
+// its dependents launch at once (launch_dependents at entry) and waits for
+// its predecessor's memory (griddepcontrol.wait) only after its own
+// data-independent prologue, so launch latency and setup (barrier init, TMEM
+// allocation) overlap the previous kernel's tail -- inside CUDA graphs too.
+// Without a programmatic predecessor the wait returns at once.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define PDL_ENTRY()             \
+  do {                          \
+    pdl_launch_dependents();    \
+    pdl_wait();                 \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // fails with VCNN_ECUDA unless an sm_100-class device is current
 int require_device();

@@ -56,6 +56,7 @@ struct Geo {
   int CG, NP;              // channel groups of 8; staged positions
   int BN, nblk;            // N tile, N blocks
   int off_b, off_raw, off_win, off_a, smem;  // shared-memory layout (bytes)
+  int off_yp;              // dgrad: the image's yprev planes (act' in the epilogue), -1: none
   int raw_n, win_n;        // floats: raw input image, window scratch (routed dgrad)
 };
 
@@ -105,13 +106,19 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   const int raw_bytes = 4 * g.raw_n;
   const int win_bytes = 2 * 4 * g.win_n;
   if (raw_bytes > 96 * 1024) return false;
+  // dgrad: stage the whole image's yprev (C x H x W) with one bulk copy so
+  // the epilogue's activation derivative reads shared memory
+  const int yp_floats = mode == 1 ? g.Cout * g.Hout * g.Wout : 0;
+  const int yp_bytes = (yp_floats % 4 == 0 && 4 * yp_floats <= 48 * 1024) ? 4 * yp_floats : 0;
   for (int bn = g.Cout > 128 ? 128 : (int)((g.Cout + 15) / 16 * 16); bn >= 16; bn -= 16) {
     const int b_bytes = g.kh * g.kw * g.CG * bn * 32;
     // the epilogue tile [bn][128] reuses raw + window + A (all dead by then)
     const int ep_bytes = bn * EPS * 4;
     const int tail = raw_bytes + win_bytes + a_bytes > ep_bytes ? raw_bytes + win_bytes + a_bytes
                                                                 : ep_bytes;
-    const int total = b_bytes + tail + 1024;
+    int total = b_bytes + tail + 1024;
+    const bool stage_yp = yp_bytes && (size_t)(total + yp_bytes) + 512 <= kSmemOptin;
+    if (stage_yp) total += yp_bytes;
     if ((size_t)total + 512 <= kSmemOptin) {
       g.BN = bn;
       g.nblk = (int)cdiv(g.Cout, bn);
@@ -119,6 +126,7 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
       g.off_raw = b_bytes;
       g.off_win = g.off_raw + raw_bytes;
       g.off_a = g.off_win + win_bytes;
+      g.off_yp = stage_yp ? b_bytes + tail : -1;
       g.smem = total;
       return (int64_t)g.B * g.tpi < (1 << 24);
     }
@@ -127,6 +135,7 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
 }
 
 __global__ void pack_kernel(Geo g, int mode, const float* __restrict__ w, float* __restrict__ pk) {
+  PDL_ENTRY();
   // w: [K][C][kh][kw] (conv weights).  fwd rows = maps n, channels = c;
   // dgrad rows = channels c, channels = maps n, kernel flipped.
   const int64_t per = pack_floats_per_block(g), total = per * g.nblk;
@@ -264,16 +273,23 @@ __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
   const int64_t hw = (int64_t)g.Hout * g.Wout;
   const int64_t plane0 = (int64_t)b * g.Cout + n0;
   const float* yp = a.be.yprev;
+  // yprev staged in shared memory (whole image) when the plan had room
+  const bool ys = yp && g.off_yp >= 0;
+  const uint32_t s_yp = eb - (uint32_t)g.off_raw + (uint32_t)(g.off_yp < 0 ? 0 : g.off_yp);
   for (int p = lane; p < npix; p += 32) {
     const int r = p / g.Wout, x = p - r * g.Wout;
     const int64_t o = plane0 * hw + (int64_t)(r0 + r) * g.Wout + x;
     const uint32_t ep = eb + 4u * (r * g.Wg + x);
+    const int lo = (r0 + r) * g.Wout + x;  // offset inside one channel plane
     for (int c0 = warp; c0 < nch; c0 += 4 * 16) {
       float yv[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int c = c0 + 4 * u;
-        yv[u] = (yp && c < nch) ? __ldg(yp + o + c * hw) : 0.f;
+        yv[u] = (yp && c < nch)
+                    ? (ys ? ptx::lds_f32(s_yp + 4u * (uint32_t)((n0 + c) * (int)hw + lo))
+                          : __ldg(yp + o + c * hw))
+                    : 0.f;
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
@@ -316,6 +332,7 @@ __device__ unsigned long long g_dphase[8][8];
 
 template <int TMEM_COLS>
 __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
+  pdl_launch_dependents();
   const Geo& g = a.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -335,6 +352,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
     ptx::tmem_alloc(&tmem_base_sh, TMEM_COLS);
     ptx::tmem_relinquish();
   }
+  pdl_wait();  // TMEM allocation above overlapped the previous kernel
   // ---- TMA bulk loads: prepacked B, the input image (or routed windows) ----
   const int64_t pk_per = pack_floats_per_block(g);
   const bool routed = g.mode == 1 && a.gs.pool;
@@ -346,6 +364,12 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
     uint32_t bytes = (uint32_t)(pk_per * 4);
     ptx::mbar_expect_tx(&load_bar, bytes);
     ptx::bulk_g2s(s_b, a.pack + nb * pk_per, bytes, &load_bar);
+    if (g.off_yp >= 0 && a.be.yprev) {
+      const uint32_t yb = 4u * (uint32_t)(g.Cout * g.Hout * g.Wout);
+      ptx::mbar_expect_tx(&load_bar, yb);
+      ptx::bulk_g2s(sbase + g.off_yp, a.be.yprev + (int64_t)b * g.Cout * g.Hout * g.Wout, yb,
+                    &load_bar);
+    }
     if (!routed) {
       const uint32_t rb = 4u * (uint32_t)(g.Cin * g.Hin * g.Win);
       ptx::mbar_expect_tx(&load_bar, rb);
@@ -500,7 +524,7 @@ int launch(const Args& a, cudaStream_t st) {
                                          (int)smem));
       configured = smem;
     }
-    kern<<<grid, NT, smem, st>>>(a);
+    VCNN_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(NT), smem, st, a));
     VCNN_LAUNCHED();
     return VCNN_OK;
   };
@@ -532,7 +556,7 @@ int pack_weights(const ConvDesc& d, int mode, const float* w, float* pk, cudaStr
   const int64_t n = pack_floats_per_block(g) * g.nblk;
   int64_t blocks = cdiv(n, 256);
   if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
-  pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(g, mode, w, pk);
+  VCNN_CUDA_TRY(launch_pdl(pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, g, mode, w, pk));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -565,6 +589,7 @@ __device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int
 __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
                                 const float* __restrict__ g, float lr, float mom, float scale,
                                 const PackTable t) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float vi = mom * v[i] + scale * g[i];
@@ -604,7 +629,7 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
   int64_t blocks = cdiv(n, 256);
   if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
   if (blocks < 1) blocks = 1;
-  sgd_pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, w, v, g, lr, mom, scale, t);
+  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, w, v, g, lr, mom, scale, t));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

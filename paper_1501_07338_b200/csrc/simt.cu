@@ -42,6 +42,7 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 // im2col (vectorize.hpp:54-79): one thread per patch cell, column fastest so
 // the patch-matrix writes are coalesced.
 __global__ void im2col_kernel(ConvDesc d, const float* __restrict__ x, float* __restrict__ P) {
+  PDL_ENTRY();
   const int64_t cols = d.pixels();
   const int64_t total = d.kd() * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -64,6 +65,7 @@ __global__ void im2col_kernel(ConvDesc d, const float* __restrict__ x, float* __
 template <class I>
 __global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* __restrict__ dX,
                               const float* __restrict__ yprev, int act_prev) {
+  PDL_ENTRY();
   const I cols = (I)d.pixels();
   const I total = (I)d.in_size();
   const I ohw = (I)d.ohw();
@@ -100,6 +102,7 @@ __global__ void col2im_kernel(ConvDesc d, const float* __restrict__ dP, float* _
 // (row=(c,ky,kx), b, oy, ox); its source is k itself.
 __global__ void col2im_map_kernel(ConvDesc d, int64_t* __restrict__ src,
                                   int64_t* __restrict__ tgt) {
+  PDL_ENTRY();
   const int64_t cols = d.pixels();
   const int64_t total = d.kd() * cols;
   const int64_t plane = (int64_t)d.H * d.W;
@@ -120,6 +123,7 @@ __global__ void col2im_map_kernel(ConvDesc d, int64_t* __restrict__ src,
 // build_pool_map (vectorize.hpp:167-191): pairs (b,c,oy,ox,py,px)
 __global__ void pool_map_kernel(PoolDesc d, int64_t* __restrict__ src,
                                 int64_t* __restrict__ tgt) {
+  PDL_ENTRY();
   const int64_t ws = (int64_t)d.ph * d.pw;
   const int64_t total = d.out_size() * ws;
   const int64_t plane = (int64_t)d.H * d.W;
@@ -141,6 +145,7 @@ template <class IdxT, class I>
 __global__ void pool_fwd_kernel(PoolDesc d, const float* __restrict__ x,
                                 const float* __restrict__ bias, int act, float* __restrict__ y,
                                 IdxT* __restrict__ arg) {
+  PDL_ENTRY();
   const I total = (I)d.out_size();
   const I plane = (I)d.H * d.W;
   for (I t = blockIdx.x * (I)blockDim.x + threadIdx.x; t < total; t += (I)gridDim.x * blockDim.x) {
@@ -183,6 +188,7 @@ template <class IdxT, class I>
 __global__ void pool_bwd_kernel(PoolDesc d, int bwd_mode, const float* __restrict__ g,
                                 const IdxT* __restrict__ arg, float* __restrict__ dx,
                                 const float* __restrict__ yprev, int act_prev) {
+  PDL_ENTRY();
   const I total = (I)d.in_size();
   const float scale = 1.0f / (float)(d.ph * d.pw);
   for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
@@ -219,6 +225,7 @@ __global__ void pool_bwd_kernel(PoolDesc d, int bwd_mode, const float* __restric
 // plane; one block per channel.
 __global__ void pool_bias_grad_kernel(PoolDesc d, const float* __restrict__ g,
                                       float* __restrict__ db) {
+  PDL_ENTRY();
   __shared__ float sh[kThreads];
   const int c = blockIdx.x;
   const int64_t plane = (int64_t)d.OH * d.OW;
@@ -234,6 +241,7 @@ __global__ void pool_bias_grad_kernel(PoolDesc d, const float* __restrict__ g,
 
 __global__ void act_fwd_kernel(int64_t n, int act, const float* __restrict__ x,
                                float* __restrict__ y) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = act_fwd(act, x[i]);
@@ -241,6 +249,7 @@ __global__ void act_fwd_kernel(int64_t n, int act, const float* __restrict__ x,
 
 __global__ void act_bwd_kernel(int64_t n, int act, const float* __restrict__ y, const float* dy,
                                float* g) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     g[i] = dy[i] * act_grad_from_out(act, y[i]);
@@ -253,6 +262,7 @@ constexpr int kLossThreads = 1024;
 __global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(
     int B, int units, const float* __restrict__ pred, const int* __restrict__ cls,
     float* __restrict__ loss, float* __restrict__ grad, int act_last, int* err) {
+  PDL_ENTRY();
   __shared__ float red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
@@ -296,6 +306,7 @@ __global__ void __launch_bounds__(kLossThreads) softmax_ce_kernel(
 // MSE (layers.hpp:425-433, :461-467): loss = mean (p-t)^2, grad 2(p-t)/n
 __global__ void __launch_bounds__(kLossThreads) mse_kernel(int64_t n, const float* __restrict__ p, const float* __restrict__ t,
                            float* __restrict__ loss, float* __restrict__ grad, int act_last) {
+  PDL_ENTRY();
   __shared__ float sh[kLossThreads];
   const float scale = 2.0f / (float)n;
   float acc = 0.f;
@@ -316,6 +327,7 @@ __global__ void __launch_bounds__(kLossThreads) mse_kernel(int64_t n, const floa
 __global__ void sgd_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
                            const float* __restrict__ g, float lr, float mom, float scale,
                            int vec) {
+  PDL_ENTRY();
   const int64_t n4 = vec ? (n >> 2) : 0;
   float4* w4 = reinterpret_cast<float4*>(w);
   float4* v4 = reinterpret_cast<float4*>(v);
@@ -350,6 +362,7 @@ __global__ void accumulate_kernel(const float* __restrict__ values,
                                   const int64_t* __restrict__ source, int64_t pairs,
                                   int64_t target_len, int reducer, float* __restrict__ out,
                                   int64_t* __restrict__ arg) {
+  PDL_ENTRY();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < target_len;
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = 0, hi = pairs;  // lower_bound(t)
@@ -384,6 +397,7 @@ __global__ void accumulate_kernel(const float* __restrict__ values,
 }
 
 __global__ void iota_kernel(int64_t n, int64_t* __restrict__ v) {
+  PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     v[i] = i;
@@ -396,6 +410,7 @@ __global__ void iota_kernel(int64_t n, int64_t* __restrict__ v) {
 __global__ void conv_fwd_simt(ConvDesc d, const float* __restrict__ x,
                               const float* __restrict__ w, const float* __restrict__ b, int act,
                               float* __restrict__ y) {
+  PDL_ENTRY();
   const int64_t total = d.out_size();
   const int64_t kd = d.kd();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -419,6 +434,7 @@ __global__ void conv_fwd_simt(ConvDesc d, const float* __restrict__ x,
 __global__ void conv_wgrad_simt(ConvDesc d, const float* __restrict__ x,
                                 const float* __restrict__ g, float* __restrict__ dw,
                                 float* __restrict__ db) {
+  PDL_ENTRY();
   __shared__ float sh[kThreads];
   const int64_t kd = d.kd();
   const int64_t k = blockIdx.x;  // 0..kd (kd = bias)
@@ -450,6 +466,7 @@ __global__ void conv_wgrad_simt(ConvDesc d, const float* __restrict__ x,
 __global__ void conv_dgrad_simt(ConvDesc d, const float* __restrict__ g,
                                 const float* __restrict__ w, float* __restrict__ dx,
                                 const float* __restrict__ yprev, int act_prev) {
+  PDL_ENTRY();
   const int64_t total = d.in_size();
   const int64_t kd = d.kd();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -483,6 +500,7 @@ __global__ void conv_dgrad_simt(ConvDesc d, const float* __restrict__ g,
 __global__ void full_fwd_simt(int B, int in, int out, const float* __restrict__ x,
                               const float* __restrict__ w, const float* __restrict__ b, int act,
                               float* __restrict__ y) {
+  PDL_ENTRY();
   const int64_t total = (int64_t)B * out;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -510,6 +528,7 @@ __global__ void full_fwd_simt(int B, int in, int out, const float* __restrict__ 
 __global__ void full_wgrad_simt(int B, int in, int out, const float* __restrict__ x,
                                 const float* __restrict__ g, float* __restrict__ dw,
                                 float* __restrict__ db) {
+  PDL_ENTRY();
   const int64_t total = (int64_t)out * (in + 1);
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -544,6 +563,7 @@ __global__ void full_wgrad_simt(int B, int in, int out, const float* __restrict_
 __global__ void full_dgrad_simt(int B, int in, int out, const float* __restrict__ g,
                                 const float* __restrict__ w, float* __restrict__ dx,
                                 const float* __restrict__ yprev, int act_prev) {
+  PDL_ENTRY();
   const int64_t total = (int64_t)B * in;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -567,6 +587,7 @@ __global__ void full_dgrad_simt(int B, int in, int out, const float* __restrict_
 
 __global__ void matmul_simt(int64_t m, int64_t k, int64_t n, const float* __restrict__ a,
                             const float* __restrict__ b, float* __restrict__ c, bool transB) {
+  PDL_ENTRY();
   const int64_t total = m * n;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -586,7 +607,7 @@ __global__ void matmul_simt(int64_t m, int64_t k, int64_t n, const float* __rest
 // launchers
 // ===========================================================================
 int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st) {
-  im2col_kernel<<<grid_for(d.kd() * d.pixels()), kThreads, 0, st>>>(d, x, P);
+  VCNN_CUDA_TRY(launch_pdl(im2col_kernel, dim3(grid_for(d.kd() * d.pixels())), dim3(kThreads), 0, st, d, x, P));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -594,21 +615,21 @@ int launch_im2col(const ConvDesc& d, const float* x, float* P, cudaStream_t st) 
 int launch_col2im(const ConvDesc& d, const float* dP, float* dX, cudaStream_t st,
                   const float* yprev, int act_prev) {
   if (fits32(d.in_size()) && fits32(d.kd() * d.pixels()))
-    col2im_kernel<int><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX, yprev, act_prev);
+    VCNN_CUDA_TRY(launch_pdl(col2im_kernel<int>, dim3(grid_for(d.in_size())), dim3(kThreads), 0, st, d, dP, dX, yprev, act_prev));
   else
-    col2im_kernel<int64_t><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, dP, dX, yprev, act_prev);
+    VCNN_CUDA_TRY(launch_pdl(col2im_kernel<int64_t>, dim3(grid_for(d.in_size())), dim3(kThreads), 0, st, d, dP, dX, yprev, act_prev));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int launch_col2im_map(const ConvDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st) {
-  col2im_map_kernel<<<grid_for(d.kd() * d.pixels()), kThreads, 0, st>>>(d, src, tgt);
+  VCNN_CUDA_TRY(launch_pdl(col2im_map_kernel, dim3(grid_for(d.kd() * d.pixels())), dim3(kThreads), 0, st, d, src, tgt));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int launch_pool_map(const PoolDesc& d, int64_t* src, int64_t* tgt, cudaStream_t st) {
-  pool_map_kernel<<<grid_for(d.out_size() * d.ph * d.pw), kThreads, 0, st>>>(d, src, tgt);
+  VCNN_CUDA_TRY(launch_pdl(pool_map_kernel, dim3(grid_for(d.out_size() * d.ph * d.pw)), dim3(kThreads), 0, st, d, src, tgt));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -617,10 +638,10 @@ template <class IdxT>
 int launch_pool_fwd(const PoolDesc& d, const float* x, const float* bias, int act, float* y,
                     IdxT* arg, cudaStream_t st) {
   if (fits32(d.in_size()))
-    pool_fwd_kernel<IdxT, int><<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, bias, act, y, arg);
+    VCNN_CUDA_TRY(launch_pdl(pool_fwd_kernel<IdxT, int>, dim3(grid_for(d.out_size())), dim3(kThreads), 0, st, d, x, bias, act, y, arg));
   else
-    pool_fwd_kernel<IdxT, int64_t><<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, bias, act, y,
-                                                                                arg);
+    VCNN_CUDA_TRY(launch_pdl(pool_fwd_kernel<IdxT, int64_t>, dim3(grid_for(d.out_size())), dim3(kThreads), 0, st, d, x, bias, act, y,
+                                                                                arg));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -633,11 +654,11 @@ template <class IdxT>
 int launch_pool_bwd(const PoolDesc& d, int bwd_mode, const float* gpre, const IdxT* arg,
                     float* dx, const float* yprev, int act_prev, cudaStream_t st) {
   if (fits32(d.in_size()))
-    pool_bwd_kernel<IdxT, int><<<grid_for(d.in_size()), kThreads, 0, st>>>(d, bwd_mode, gpre, arg,
-                                                                           dx, yprev, act_prev);
+    VCNN_CUDA_TRY(launch_pdl(pool_bwd_kernel<IdxT, int>, dim3(grid_for(d.in_size())), dim3(kThreads), 0, st, d, bwd_mode, gpre, arg,
+                                                                           dx, yprev, act_prev));
   else
-    pool_bwd_kernel<IdxT, int64_t><<<grid_for(d.in_size()), kThreads, 0, st>>>(
-        d, bwd_mode, gpre, arg, dx, yprev, act_prev);
+    VCNN_CUDA_TRY(launch_pdl(pool_bwd_kernel<IdxT, int64_t>, dim3(grid_for(d.in_size())), dim3(kThreads), 0, st, 
+        d, bwd_mode, gpre, arg, dx, yprev, act_prev));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -647,20 +668,20 @@ template int launch_pool_bwd<int64_t>(const PoolDesc&, int, const float*, const 
                                       const float*, int, cudaStream_t);
 
 int launch_pool_bias_grad(const PoolDesc& d, const float* gpre, float* dbias, cudaStream_t st) {
-  pool_bias_grad_kernel<<<d.C, kThreads, 0, st>>>(d, gpre, dbias);
+  VCNN_CUDA_TRY(launch_pdl(pool_bias_grad_kernel, dim3(d.C), dim3(kThreads), 0, st, d, gpre, dbias));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int launch_act_fwd(int64_t n, int act, const float* x, float* y, cudaStream_t st) {
-  act_fwd_kernel<<<grid_for(n), kThreads, 0, st>>>(n, act, x, y);
+  VCNN_CUDA_TRY(launch_pdl(act_fwd_kernel, dim3(grid_for(n)), dim3(kThreads), 0, st, n, act, x, y));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int launch_act_bwd(int64_t n, int act, const float* y, const float* dy, float* g,
                    cudaStream_t st) {
-  act_bwd_kernel<<<grid_for(n), kThreads, 0, st>>>(n, act, y, dy, g);
+  VCNN_CUDA_TRY(launch_pdl(act_bwd_kernel, dim3(grid_for(n)), dim3(kThreads), 0, st, n, act, y, dy, g));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -669,10 +690,10 @@ int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
                 const float* values, float* loss, float* grad, int act_last, int* err,
                 cudaStream_t st) {
   if (kind == VCNN_LOSS_SOFTMAX_CE) {
-    softmax_ce_kernel<<<1, kLossThreads, 0, st>>>(B, units, pred, cls, loss, grad, act_last, err);
+    VCNN_CUDA_TRY(launch_pdl(softmax_ce_kernel, dim3(1), dim3(kLossThreads), 0, st, B, units, pred, cls, loss, grad, act_last, err));
   } else {
-    mse_kernel<<<1, kLossThreads, 0, st>>>((int64_t)B * units, pred, values, loss, grad,
-                                           act_last);
+    VCNN_CUDA_TRY(launch_pdl(mse_kernel, dim3(1), dim3(kLossThreads), 0, st, (int64_t)B * units, pred, values, loss, grad,
+                                           act_last));
   }
   VCNN_LAUNCHED();
   return VCNN_OK;
@@ -685,7 +706,7 @@ int launch_sgd(int64_t n, float* w, float* v, const float* g, float lr, float mo
   const int64_t work = aligned ? ((n >> 2) > 0 ? (n >> 2) : 1) : n;
   unsigned grid = grid_for(work);
   if (grid > (unsigned)sm_count() * 8) grid = (unsigned)sm_count() * 8;
-  sgd_kernel<<<grid, kThreads, 0, st>>>(n, w, v, g, lr, mom, scale, aligned ? 1 : 0);
+  VCNN_CUDA_TRY(launch_pdl(sgd_kernel, dim3(grid), dim3(kThreads), 0, st, n, w, v, g, lr, mom, scale, aligned ? 1 : 0));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -701,7 +722,7 @@ int launch_accumulate(const float* values, const int64_t* source, const int64_t*
   VCNN_CUDA_TRY(cudaMallocAsync(&idx_in, sizeof(int64_t) * np, st));
   VCNN_CUDA_TRY(cudaMallocAsync(&idx_out, sizeof(int64_t) * np, st));
   if (pairs > 0) {
-    iota_kernel<<<grid_for(pairs), kThreads, 0, st>>>(pairs, idx_in);
+    VCNN_CUDA_TRY(launch_pdl(iota_kernel, dim3(grid_for(pairs)), dim3(kThreads), 0, st, pairs, idx_in));
     VCNN_LAUNCHED();
     // stable radix sort: equal targets keep their map order
     VCNN_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, target, keys_out, idx_in,
@@ -710,8 +731,8 @@ int launch_accumulate(const float* values, const int64_t* source, const int64_t*
     VCNN_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, target, keys_out, idx_in,
                                                   idx_out, pairs, 0, 64, st));
   }
-  accumulate_kernel<<<grid_for(target_len), kThreads, 0, st>>>(
-      values, keys_out, idx_out, source, pairs, target_len, reducer, out, arg);
+  VCNN_CUDA_TRY(launch_pdl(accumulate_kernel, dim3(grid_for(target_len)), dim3(kThreads), 0, st, 
+      values, keys_out, idx_out, source, pairs, target_len, reducer, out, arg));
   VCNN_LAUNCHED();
   if (temp) cudaFreeAsync(temp, st);
   cudaFreeAsync(keys_out, st);
@@ -724,7 +745,7 @@ namespace simt {
 
 int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, int act,
              float* y, cudaStream_t st) {
-  conv_fwd_simt<<<grid_for(d.out_size()), kThreads, 0, st>>>(d, x, w, b, act, y);
+  VCNN_CUDA_TRY(launch_pdl(conv_fwd_simt, dim3(grid_for(d.out_size())), dim3(kThreads), 0, st, d, x, w, b, act, y));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -732,44 +753,44 @@ int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* b, 
 int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
                cudaStream_t st) {
   dim3 grid((unsigned)(d.kd() + 1), (unsigned)d.K);
-  conv_wgrad_simt<<<grid, kThreads, 0, st>>>(d, x, gpre, dw, db);
+  VCNN_CUDA_TRY(launch_pdl(conv_wgrad_simt, dim3(grid), dim3(kThreads), 0, st, d, x, gpre, dw, db));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
                const float* yprev, int act_prev, cudaStream_t st) {
-  conv_dgrad_simt<<<grid_for(d.in_size()), kThreads, 0, st>>>(d, gpre, w, dx, yprev, act_prev);
+  VCNN_CUDA_TRY(launch_pdl(conv_dgrad_simt, dim3(grid_for(d.in_size())), dim3(kThreads), 0, st, d, gpre, w, dx, yprev, act_prev));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
              float* y, cudaStream_t st) {
-  full_fwd_simt<<<grid_for((int64_t)B * out), kThreads, 0, st>>>(B, in, out, x, w, b, act, y);
+  VCNN_CUDA_TRY(launch_pdl(full_fwd_simt, dim3(grid_for((int64_t)B * out)), dim3(kThreads), 0, st, B, in, out, x, w, b, act, y));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw, float* db,
                cudaStream_t st) {
-  full_wgrad_simt<<<grid_for((int64_t)out * (in + 1)), kThreads, 0, st>>>(B, in, out, x, gpre,
-                                                                          dw, db);
+  VCNN_CUDA_TRY(launch_pdl(full_wgrad_simt, dim3(grid_for((int64_t)out * (in + 1))), dim3(kThreads), 0, st, B, in, out, x, gpre,
+                                                                          dw, db));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float* dx,
                const float* yprev, int act_prev, cudaStream_t st) {
-  full_dgrad_simt<<<grid_for((int64_t)B * in), kThreads, 0, st>>>(B, in, out, gpre, w, dx,
-                                                                  yprev, act_prev);
+  VCNN_CUDA_TRY(launch_pdl(full_dgrad_simt, dim3(grid_for((int64_t)B * in)), dim3(kThreads), 0, st, B, in, out, gpre, w, dx,
+                                                                  yprev, act_prev));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
 
 int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
            bool transB, cudaStream_t st) {
-  matmul_simt<<<grid_for(m * n), kThreads, 0, st>>>(m, k, n, a, b, c, transB);
+  VCNN_CUDA_TRY(launch_pdl(matmul_simt, dim3(grid_for(m * n)), dim3(kThreads), 0, st, m, k, n, a, b, c, transB));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

@@ -160,6 +160,9 @@ struct KRange {
   // first pass (ta4/tb4), so all table loads of a stage are in flight before
   // the dependent operand loads
   static constexpr bool TWO_PHASE = false;
+  // A_ZERO_ROWS: a_zero(ctx) marks A rows that are identically zero (M
+  // padding); once every ring slot holds them they are not rewritten
+  static constexpr bool A_ZERO_ROWS = false;
   int kb_total = 0, kb_per = 0;
   float* part = nullptr;
   int part_m = 0, part_n = 0;
@@ -187,6 +190,7 @@ struct KRange {
 // inside the K loop.  Epilogue: warps 0-3, thread = TMEM lane = row.
 template <class Prob, int BN, bool SPLIT3>
 __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
+  pdl_launch_dependents();
   using C = TileCfg<BN, SPLIT3>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -219,6 +223,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
     ptx::mbar_init(&done_bar, 1);
     ptx::fence_mbar_init();
   }
+  pdl_wait();  // TMEM / barrier setup above overlapped the previous kernel
   const int tab_off = S * C::STAGE_BYTES;
   int* tabp = reinterpret_cast<int*>(smem + tab_off);
   float* slab = reinterpret_cast<float*>(smem + tab_off + p.slab_off);
@@ -339,6 +344,8 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
       for (int i = 0; i < C::PA; ++i) {
         int row, ch;
         slot_of<BM>(i, arm, row, ch);
+        if constexpr (Prob::A_ZERO_ROWS)
+          if (it >= S && p.a_zero(actx[i])) continue;  // still zero from the first pass
         store_chunk<SPLIT3, BM, !Prob::PRE_ROUNDED>(sa, row, ch, va[i]);
       }
 #pragma unroll
@@ -424,6 +431,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
 // Few splits: one thread per output, 4 independent accumulators.
 template <class Prob>
 __global__ void splitk_reduce_small(const Prob p, int splits) {
+  PDL_ENTRY();
   const int64_t M = p.part_m, N = p.part_n, total = M * N;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -446,6 +454,7 @@ __global__ void splitk_reduce_small(const Prob p, int splits) {
 // partial sums in warp order -- fixed order, deterministic.
 template <class Prob>
 __global__ void splitk_reduce_kernel(const Prob p, int splits) {
+  PDL_ENTRY();
   __shared__ float sh[8][33];
   const int64_t M = p.part_m, N = p.part_n, total = M * N;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
@@ -945,7 +954,7 @@ struct SlabFwdProb : KRange {
 // 0 four consecutive pixels are one aligned 16-byte G load (vecg).
 // Deterministic split-K reduce.
 struct SlabWgradProb : KRange {
-  static constexpr bool SLAB = true, PRE_ROUNDED = true, TWO_PHASE = true;
+  static constexpr bool SLAB = true, PRE_ROUNDED = true, TWO_PHASE = true, A_ZERO_ROWS = true;
   static constexpr int TABLES = 2;
   ConvDesc d;
   const float* x;
@@ -1005,6 +1014,7 @@ struct SlabWgradProb : KRange {
     const int c = k / khw, rem = k - c * khw, ky = rem / d.kw, kx = rem - ky * d.kw;
     return (c * d.H + ky) * d.W + kx;
   }
+  __device__ __forceinline__ bool a_zero(int ctx) const { return ctx == -3; }
   using BCtx = int;  // n * OH*OW, -1 past K
   __device__ __forceinline__ int b_ctx(int n) const { return n < d.K ? n * d.OH * d.OW : -1; }
   __device__ __forceinline__ int4 ta4(const Tab& tab, int pt) const { return tab.t4(pt); }
@@ -1168,6 +1178,7 @@ struct SlabDgradProb : KRange {
 // wf[n][kd4] = tf32(W[n][k]) zero-padded, wt[c][(n,ky,kx)] = tf32(W[n][c][ky][kx])
 __global__ void prep_weights_kernel(ConvDesc d, const float* __restrict__ w,
                                     float* __restrict__ wf, float* __restrict__ wt) {
+  PDL_ENTRY();
   const int Kd = (int)d.kd(), kd4 = round4(Kd), khw = d.kh * d.kw;
   const int nf = d.K * kd4;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
@@ -1324,7 +1335,7 @@ int launch_one(const Prob& p0, dim3 grid, size_t tab_bytes, size_t slab_bytes, c
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  tc_gemm_kernel<Prob, BN, SPLIT3><<<grid, NTH, smem, st>>>(p);
+  VCNN_CUDA_TRY(launch_pdl(tc_gemm_kernel<Prob, BN, SPLIT3>, dim3(grid), dim3(NTH), smem, st, p));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -1372,9 +1383,9 @@ int run(Prob p, const Plan& pl, bool split3, const Workspace& ws, cudaStream_t s
   if (pl.splits <= 16) {
     int64_t blocks = cdiv(pl.M * pl.N, 256);
     if (blocks > 8 * sm_count()) blocks = 8 * sm_count();
-    splitk_reduce_small<Prob><<<(unsigned)blocks, 256, 0, st>>>(p, pl.splits);
+    VCNN_CUDA_TRY(launch_pdl(splitk_reduce_small<Prob>, dim3((unsigned)blocks), dim3(256), 0, st, p, pl.splits));
   } else {
-    splitk_reduce_kernel<Prob><<<(unsigned)cdiv(pl.M * pl.N, 32), 256, 0, st>>>(p, pl.splits);
+    VCNN_CUDA_TRY(launch_pdl(splitk_reduce_kernel<Prob>, dim3((unsigned)cdiv(pl.M * pl.N, 32)), dim3(256), 0, st, p, pl.splits));
   }
   VCNN_LAUNCHED();
   return VCNN_OK;
@@ -1703,7 +1714,7 @@ int prep_weights(const ConvDesc& d, const float* w, float* wf, float* wt, cudaSt
   const int64_t n = (int64_t)prep_floats_f(d);
   int64_t blocks = cdiv(n, 256);
   if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
-  prep_weights_kernel<<<(unsigned)blocks, 256, 0, st>>>(d, w, wf, wt);
+  VCNN_CUDA_TRY(launch_pdl(prep_weights_kernel, dim3((unsigned)blocks), dim3(256), 0, st, d, w, wf, wt));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
