@@ -402,7 +402,17 @@ def main():
         else:
             roof = {"bound": "hbm", "achieved": top["gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": top["gbs"] / pk["hbm_gbs"]}
-        roof.update({"traffic": None, "kernel": f"layer{top['layer']}.{top['op']}",
+        # DRAM traffic per launch of that kernel from the committed ncu --set
+        # full capture (profiles/ncu_traffic.json), when there is one
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                t = json.load(f).get(f"layer{top['layer']}.{top['op']}")
+            if t and args.config == "cifar3" and B == 128:
+                traffic = t["dram_bytes"]
+        except (OSError, ValueError):
+            pass
+        roof.update({"traffic": traffic, "kernel": f"layer{top['layer']}.{top['op']}",
                      "share_of_step": top["share"], "us_per_launch": top["us"],
                      "peak_src": pk["tf32_src"] if top["bound"] == "tensor" else pk["src"]})
         step_roof_us = sum(r["roof_us"] for r in rows)
