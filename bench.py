@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-infer", action="store_true", help="skip the forward-only pass")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--details", default="", help="write per-op timing JSON here")
     return ap.parse_args()
@@ -422,6 +423,36 @@ def main():
             with open(args.details, "w") as f:
                 json.dump(details, f, indent=1)
 
+    # ---- test mode (paper Table 4): forward-only img/s, graph-replayed ----
+    infer = None
+    if rank == 0 and not args.no_infer:
+        fs = torch.cuda.Stream()
+        fs.wait_stream(stream)
+        with torch.cuda.stream(fs):
+            net.set_stream(fs)
+            for _ in range(3):
+                net.forward(B)
+            fg = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(fg, stream=fs):
+                net.forward(B)
+        net.set_stream(stream)
+        stream.wait_stream(fs)
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for i in range(args.warmup):
+            load(i)
+            fg.replay()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            fev[i][0].record(stream)
+            load(args.warmup + i)
+            fg.replay()
+            fev[i][1].record(stream)
+        torch.cuda.synchronize()
+        fsec = sum(a.elapsed_time(b) for a, b in fev) / 1e3
+        infer = {"metric": "test images/sec (forward only)", "value": B * args.steps / fsec,
+                 "unit": "img/s", "ms_per_batch": 1e3 * fsec / args.steps, "batch": B}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(spec, B, 3, 1, seconds=args.cpu_seconds)
@@ -447,6 +478,12 @@ def main():
             "gpu_launches": int(launches), "kernels_per_step": kps,
             "clocks": clk.result(),
             "step_roofline_us": details.get("step_roofline_us"),
+            # BreakdownTimer components (variants.hpp:249-274, paper Fig. 6):
+            # seconds per step from the event-timed eager pass
+            "breakdown_ms_per_step": (
+                {k: 1e3 * v / args.steps for k, v in details["breakdown_s"].items()}
+                if details.get("breakdown_s") else None),
+            "infer": infer,
         }
         print(json.dumps(line))
     net.close()
