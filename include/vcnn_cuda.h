@@ -277,6 +277,19 @@ int vcnn_net_train_step(vcnn_net* net, int batch, float lr, float mom);
  * H2D copy, train step, D2H loss; synchronous */
 int vcnn_net_train_step_host(vcnn_net* net, int batch, const float* x, const int* cls,
                              const float* values, float lr, float mom, float* loss_out);
+/* Trainer<T>::fit's inner loop for ONE epoch, device-resident
+ * (training.hpp:60-88, gather_batch network.hpp:165-176): the dataset
+ * (images [count][in], cls [count] or values [count][out]) lives in device
+ * memory, `order` is the epoch's permutation (device, count ints -- the
+ * reference's Rng::shuffle of 0..count-1, common.hpp:84-90), batches of
+ * `batch` rows with a smaller last batch.  Per batch: index-gather kernel +
+ * train step (CUDA-graph replayed when enabled); the batch loss lands in
+ * losses[b] (device, ceil(count/batch) floats).  Stream-ordered, no host
+ * synchronisation; class bounds are the caller's contract (checked on the
+ * host by the C++/Python Trainers when the dataset is uploaded). */
+int vcnn_net_train_epoch(vcnn_net* net, const float* images, const int* cls,
+                         const float* values, int count, const int* order, int batch, float lr,
+                         float mom, float* losses);
 /* end-to-end inference: HOST batch in, HOST output out; synchronous */
 int vcnn_net_forward_host(vcnn_net* net, int batch, const float* x, float* out);
 /* CUDA-graph capture of train_step (per batch size); 0 disables */

@@ -98,6 +98,7 @@ _SIGS = {
     "vcnn_net_set_precision": [c_vp, c_int],
     "vcnn_net_set_fusion": [c_vp, c_int],
     "vcnn_copy_h2d": [c_vp, c_vp, C.c_size_t],
+    "vcnn_net_train_epoch": [c_vp, c_vp, c_vp, c_vp, c_int, c_vp, c_int, c_float, c_float, c_vp],
     "vcnn_net_set_trace": [c_vp, c_int],
     "vcnn_net_get_params": [c_vp, c_vp],
     "vcnn_net_set_params": [c_vp, c_vp],

@@ -114,6 +114,15 @@ struct vcnn_net {
   cudaStream_t stream = nullptr;
   // graph replay
   bool use_graph = false;
+  // instantiated step graphs, one per (batch, lr, momentum) in use (a
+  // training epoch alternates full batches and one smaller last batch)
+  struct GraphEntry {
+    int batch;
+    float lr, mom;
+    cudaGraphExec_t exec;
+    int kernels;
+  };
+  std::vector<GraphEntry> graphs;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;  // capture needs a non-legacy stream
   int g_batch = -1;
@@ -438,7 +447,8 @@ int check_cfg(float lr, float mom) {
 }
 
 void drop_graph(vcnn_net* n) {
-  if (n->gexec) cudaGraphExecDestroy(n->gexec);
+  for (auto& e : n->graphs) cudaGraphExecDestroy(e.exec);
+  n->graphs.clear();
   n->gexec = nullptr;
   n->g_batch = -1;
 }
@@ -457,7 +467,19 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
   TRY(check_cfg(lr, mom));
   if (!n->use_graph || n->breakdown) return eager_step(n, batch, lr, mom);
   if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom) {
-    drop_graph(n);
+    n->gexec = nullptr;
+    for (auto& e : n->graphs)
+      if (e.batch == batch && e.lr == lr && e.mom == mom) {
+        n->gexec = e.exec;
+        n->kernels_per_step = e.kernels;
+      }
+  }
+  if (n->gexec) {
+    n->g_batch = batch;
+    n->g_lr = lr;
+    n->g_mom = mom;
+  } else {
+    if (n->graphs.size() >= 4) drop_graph(n);
     if (!n->cap_stream)
       VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&n->cap_stream, cudaStreamNonBlocking));
     // capture on a private stream (the caller's may be the legacy default
@@ -478,6 +500,7 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     e = cudaGraphInstantiate(&n->gexec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    n->graphs.push_back({batch, lr, mom, n->gexec, n->kernels_per_step});
     n->g_batch = batch;
     n->g_lr = lr;
     n->g_mom = mom;
@@ -906,6 +929,28 @@ int vcnn_net_train_step_host(vcnn_net* n, int batch, const float* x, const int* 
   float l = 0;
   TRY(copy_out(n, &l, n->loss, sizeof(float)));
   if (loss_out) *loss_out = l;
+  return VCNN_OK;
+}
+
+int vcnn_net_train_epoch(vcnn_net* n, const float* images, const int* cls, const float* values,
+                         int count, const int* order, int batch, float lr, float mom,
+                         float* losses) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (count < 1) return fail(VCNN_ETRAINING, "fit: empty dataset");
+  if (batch < 1 || batch > n->max_batch)
+    return fail(VCNN_ESHAPE, "epoch batch outside [1, max_batch]");
+  TRY(check_cfg(lr, mom));
+  const bool ce = n->spec.loss == VCNN_LOSS_SOFTMAX_CE;
+  if (ce ? !cls : !values) return fail(VCNN_ESHAPE, "train_epoch: targets required");
+  int bi = 0;
+  for (int start = 0; start < count; start += batch, ++bi) {
+    const int nb = count - start < batch ? count - start : batch;
+    TRY(launch_gather_rows(nb, n->in_per, images, order, start, n->x, n->out_units,
+                           ce ? cls : nullptr, n->cls, ce ? nullptr : values, n->values,
+                           n->stream));
+    TRY(train_step(n, nb, lr, mom));
+    TRY(launch_store_scalar(n->loss, losses + bi, n->stream));
+  }
   return VCNN_OK;
 }
 

@@ -65,6 +65,11 @@ int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
                 cudaStream_t st);
 int launch_sgd(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
                cudaStream_t st);
+// batch row j <- dataset row order[start + j] (+ class / value targets)
+int launch_gather_rows(int n, int64_t per, const float* src, const int* order, int start,
+                       float* dst, int64_t tper, const int* cls_src, int* cls_dst,
+                       const float* val_src, float* val_dst, cudaStream_t st);
+int launch_store_scalar(const float* src, float* dst, cudaStream_t st);
 int launch_accumulate(const float* values, const int64_t* source, const int64_t* target,
                       int64_t pairs, int64_t target_len, int reducer, float* out, int64_t* arg,
                       cudaStream_t st);

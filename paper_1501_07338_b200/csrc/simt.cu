@@ -699,6 +699,54 @@ int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
   return VCNN_OK;
 }
 
+// gather_batch (network.hpp:165-176) on the device: row j of the batch =
+// dataset sample order[start + j]; labels / value targets alongside
+__global__ void gather_rows_kernel(int n, int64_t per, const float* __restrict__ src,
+                                   const int* __restrict__ order, int start,
+                                   float* __restrict__ dst, int64_t tper,
+                                   const int* __restrict__ cls_src, int* __restrict__ cls_dst,
+                                   const float* __restrict__ val_src, float* __restrict__ val_dst) {
+  PDL_ENTRY();
+  const int j = blockIdx.y;
+  if (j >= n) return;
+  const int64_t id = order[start + j];
+  const float* s = src + id * per;
+  float* d = dst + (int64_t)j * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < per;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = s[i];
+  if (blockIdx.x == 0) {
+    if (cls_src && threadIdx.x == 0) cls_dst[j] = cls_src[id];
+    if (val_src)
+      for (int64_t i = threadIdx.x; i < tper; i += blockDim.x)
+        val_dst[(int64_t)j * tper + i] = val_src[id * tper + i];
+  }
+}
+
+int launch_gather_rows(int n, int64_t per, const float* src, const int* order, int start,
+                       float* dst, int64_t tper, const int* cls_src, int* cls_dst,
+                       const float* val_src, float* val_dst, cudaStream_t st) {
+  int64_t bx = cdiv(per, kThreads);
+  if (bx > 8) bx = 8;
+  VCNN_CUDA_TRY(launch_pdl(gather_rows_kernel, dim3((unsigned)bx, (unsigned)n), dim3(kThreads), 0,
+                           st, n, per, src, order, start, dst, tper, cls_src, cls_dst, val_src,
+                           val_dst));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+// losses[i] = *loss (device scalar copy into the epoch's loss history)
+__global__ void store_scalar_kernel(const float* __restrict__ src, float* __restrict__ dst) {
+  PDL_ENTRY();
+  if (threadIdx.x == 0) *dst = *src;
+}
+
+int launch_store_scalar(const float* src, float* dst, cudaStream_t st) {
+  VCNN_CUDA_TRY(launch_pdl(store_scalar_kernel, dim3(1), dim3(32), 0, st, src, dst));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
 int launch_sgd(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
                cudaStream_t st) {
   const bool aligned = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(v) |

@@ -339,11 +339,18 @@ class Trainer:
         self.precision = Precision(precision)
         self.use_graph = use_graph
 
-    def fit(self, net: Network, images, targets):
+    def fit(self, net: Network, images, targets, resident=False):
+        """resident=True: the dataset is uploaded once and every epoch runs on
+        the device (vcnn_net_train_epoch: permutation from the reference Rng,
+        index-gather kernel, graph-replayed steps, one D2H of the epoch's
+        losses).  The non-finite check then happens per epoch (the reference
+        stops after the offending batch, training.hpp:77-80)."""
         images = np.ascontiguousarray(images, dtype=np.float32)
         count = images.shape[0]
         if count < 1:
             raise TrainingError("fit: empty dataset")
+        if resident:
+            return self._fit_resident(net, images, targets)
         net.set_precision(self.precision)
         net.enable_graph(self.use_graph)
         rng = Rng(self.cfg.seed)
@@ -372,15 +379,64 @@ class Trainer:
             epoch_loss.append(loss_sum / batches)
         return epoch_loss
 
+    def _fit_resident(self, net: Network, images, targets):
+        count = images.shape[0]
+        is_ce = net.spec.loss == LossKind.softmax_ce
+        net.set_precision(self.precision)
+        net.enable_graph(self.use_graph)
+        dev = torch.device("cuda")
+        X = torch.from_numpy(images.reshape(count, -1)).to(dev)
+        tg = np.asarray(targets)
+        Ct = Vt = None
+        if is_ce:
+            cls = tg.astype(np.int32).reshape(count)
+            bad = (cls < 0) | (cls >= net.units)
+            if bad.any():  # layers.hpp:413-415, checked once at upload
+                raise BoundsError(f"loss: class index {int(cls[bad][0])} out of range "
+                                  f"[0,{net.units})")
+            Ct = torch.from_numpy(cls).to(dev)
+        else:
+            Vt = torch.from_numpy(tg.reshape(count, -1).astype(np.float32)).to(dev)
+        nb = -(-count // self.cfg.batch)
+        losses = torch.empty(nb, device=dev)
+        order_t = torch.empty(count, dtype=torch.int32, device=dev)
+        rng = Rng(self.cfg.seed)
+        order = list(range(count))
+        ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())
+        epoch_loss = []
+        for epoch in range(self.cfg.epochs):
+            rng.shuffle(order)  # Rng::shuffle (common.hpp:84-90), not reset between epochs
+            order_t.copy_(torch.tensor(order, dtype=torch.int32))
+            check(lib().vcnn_net_train_epoch(net._h, ptr(X), ptr(Ct), ptr(Vt), count,
+                                             ptr(order_t), self.cfg.batch, self.cfg.lr,
+                                             self.cfg.momentum, ptr(losses)))
+            ls = losses.cpu().numpy().astype(np.float64)
+            if not np.isfinite(ls).all():
+                k = int(np.argmin(np.isfinite(ls)))
+                ids = order[k * self.cfg.batch:(k + 1) * self.cfg.batch]
+                net.forward_host(images[ids])
+                raise TrainingError(
+                    f"non-finite loss at epoch {epoch}, batch {k}; first non-finite output at "
+                    f"{self._locate_nonfinite(net, len(ids))}")
+            epoch_loss.append(float(ls.mean()))
+        return epoch_loss
+
     @staticmethod
     def _locate_nonfinite(net: Network, B):
-        """locate_nonfinite (training.hpp:28-45): first layer whose output is not finite."""
-        for i, L in enumerate(net.spec.layers):
-            if not np.isfinite(net.layer_output(i, B)).all():
-                kind = type(L).__name__.replace("Spec", "").lower()
-                kind = {"conv": "conv", "pool": "pool", "full": "full"}.get(kind, kind)
-                return f"layer {i} ({kind})"
-        return "loss head"
+        """locate_nonfinite (training.hpp:28-45): first layer whose output is
+        not finite -- the staged batch is re-run with the full trace kept
+        (fused layers do not materialise their conv outputs)."""
+        net.set_trace(True)
+        try:
+            net.forward(B)
+            for i, L in enumerate(net.spec.layers):
+                if not np.isfinite(net.layer_output(i, B)).all():
+                    kind = type(L).__name__.replace("Spec", "").lower()
+                    kind = {"conv": "conv", "pool": "pool", "full": "full"}.get(kind, kind)
+                    return f"layer {i} ({kind})"
+            return "loss head"
+        finally:
+            net.set_trace(False)
 
     def evaluate_accuracy(self, net: Network, images, labels):
         images = np.ascontiguousarray(images, dtype=np.float32)

@@ -410,3 +410,28 @@ def test_fused_path_bitwise_equals_trace_path(name, B):
     assert np.array_equal(g0, g1)
     assert np.array_equal(p0, p1)
     assert k1 < k0, (k1, k0)  # the fused step launches fewer kernels
+
+
+def test_resident_epoch_loop_equals_host_loop():
+    """vcnn_net_train_epoch (dataset in HBM, index-gather kernel, graph
+    replay) trains bit-identically to the host-gather
+    Trainer: same Rng permutation, same batches incl. the smaller last one."""
+    rng = np.random.default_rng(5)
+    n = 70  # 2 full batches of 32 + one of 6
+    spec = S.cifar3()
+    imgs = rng.uniform(0, 1, (n, 3, 32, 32)).astype(np.float32)
+    labels = rng.integers(0, 10, n).astype(np.int32)
+    cfg = S.TrainConfig(lr=0.01, momentum=0.9, batch=32, epochs=2, seed=3)
+    res = []
+    for resident in (False, True):
+        net = Network(spec, 32)
+        hist = Trainer(cfg).fit(net, imgs, labels, resident=resident)
+        res.append((hist, net.get_params()))
+        net.close()
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.allclose(res[0][0], res[1][0], rtol=0, atol=1e-6)
+    net = Network(spec, 32)
+    bad = labels.copy()
+    bad[3] = 10
+    with pytest.raises(BoundsError):
+        Trainer(cfg).fit(net, imgs, bad, resident=True)
