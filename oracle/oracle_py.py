@@ -360,6 +360,8 @@ def ref():
         L.ref_net_train_steps.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                           C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                           C.c_int, C.c_void_p]
+        L.ref_save_model.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_char_p]
+        L.ref_load_model_f32.argtypes = [C.c_char_p, C.c_void_p, C.c_int64]
         L.ref_net_train_steps_f32.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                               C.c_void_p, C.c_void_p, C.c_double, C.c_double,
                                               C.c_int, C.c_void_p]
@@ -419,3 +421,18 @@ def ref_net_train_steps_f32(spec, params, x, cls, values, lr, mom, steps):
                                        _dp(c), None if v is None else v.ctypes.data, lr, mom,
                                        steps, _dp(losses)), "ref_net_train_steps_f32")
     return p, losses
+
+
+def ref_save_model(spec, params, path, f32=True):
+    """The reference's save_model(model_from_network(net)) (io.cpp:265-307)."""
+    n = make_net(spec)
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    _chk(ref().ref_save_model(C.byref(n), _dp(p), int(bool(f32)), path.encode()),
+         "ref_save_model")
+
+
+def ref_load_model_f32(path, count):
+    """The reference's load_model + network_from_model<float> (io.cpp:309-404)."""
+    out = np.empty(count, dtype=np.float32)
+    _chk(ref().ref_load_model_f32(path.encode(), out.ctypes.data, count), "ref_load_model")
+    return out

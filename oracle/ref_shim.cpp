@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include "vcnn/io.hpp"
 #include "vcnn/training.hpp"
 #include "../oracle/vcnn_oracle.h"
 
@@ -283,6 +284,58 @@ int ref_net_train_steps_f32(const orc_net* n, int B, float* params, const float*
       sgd_step(net, r.grads, cfg, vel);
     }
     params_to_flat(net, params);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+// the reference's own ModelFile v1 writer / reader (io.cpp:265-404):
+// parameters (flat, NetGrads order) <-> file, f32 or f64 networks
+int ref_save_model(const orc_net* n, const double* params, int f32, const char* path) {
+  try {
+    NetworkSpec spec = spec_of(n);
+    if (f32) {
+      Network<float> net = build_network<float>(spec);
+      size_t count = 0;
+      for (auto& layer : net.layers)
+        std::visit(
+            [&](const auto& l) {
+              using L = std::decay_t<decltype(l)>;
+              if constexpr (!std::is_same_v<L, PoolLayer<float>>) count += l.weights.data.size();
+              count += l.bias.size();
+            },
+            layer);
+      std::vector<float> pf(params, params + count);
+      flat_to_params(net, pf.data());
+      save_model(path, model_from_network(net));
+    } else {
+      Network<double> net = build_network<double>(spec);
+      flat_to_params(net, params);
+      save_model(path, model_from_network(net));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
+int ref_load_model_f32(const char* path, float* params, int64_t cap) {
+  try {
+    ModelFile m = load_model(path);
+    Network<float> net = network_from_model<float>(m);
+    std::vector<float> flat;
+    for (auto& layer : net.layers)
+      std::visit(
+          [&](const auto& l) {
+            using L = std::decay_t<decltype(l)>;
+            if constexpr (!std::is_same_v<L, PoolLayer<float>>)
+              flat.insert(flat.end(), l.weights.data.begin(), l.weights.data.end());
+            flat.insert(flat.end(), l.bias.begin(), l.bias.end());
+          },
+          layer);
+    if ((int64_t)flat.size() > cap) return 99;
+    std::memcpy(params, flat.data(), sizeof(float) * flat.size());
     return 0;
   } catch (const std::exception& e) {
     return status_of(e);

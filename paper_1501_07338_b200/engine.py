@@ -85,6 +85,21 @@ class Network:
         self.precision = Precision(precision)
         check(lib().vcnn_net_set_precision(self._h, int(precision)))
 
+    # ---- ModelFile v1 (io.cpp:265-404), SURVEY 8f row 4 ----
+    def save_model(self, path, dtype="f32"):
+        """Write the device parameters in the reference's model format."""
+        from .modelfile import save_model
+        save_model(path, self.spec, self.get_params(), dtype)
+
+    @classmethod
+    def from_model(cls, path, max_batch, precision=Precision.tf32, stream=None):
+        """A device network initialised from a reference model file."""
+        from .modelfile import load_model
+        spec, params, _ = load_model(path)
+        net = cls(spec, max_batch, precision, stream)
+        net.set_params(params.astype(np.float32))
+        return net
+
     def set_fusion(self, on=True):
         """TF32 slab kernels + conv->max-pool fusion (default on)."""
         check(lib().vcnn_net_set_fusion(self._h, int(bool(on))))

@@ -435,3 +435,27 @@ def test_resident_epoch_loop_equals_host_loop():
     bad[3] = 10
     with pytest.raises(BoundsError):
         Trainer(cfg).fit(net, imgs, bad, resident=True)
+
+
+def test_model_export_reference_predicts_the_same(tmp_path):
+    """Device-trained weights -> ModelFile v1 -> the reference's own loader
+    (io.cpp) -> the reference forward agrees with the device forward; and
+    Network.from_model restores the parameters bit for bit."""
+    spec = S.cifar3()
+    B = 16
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    net = Network(spec, B)
+    _load(net, spec, x, cls, None)
+    for _ in range(3):
+        net.train_step(B, 0.01, 0.9)
+    f = str(tmp_path / "trained.vcnn")
+    net.save_model(f)
+    p_ref = O.ref_load_model_f32(f, net.nparams)
+    assert np.array_equal(p_ref, net.get_params())
+    out_ref = O.ref_net_run_batch(spec, p_ref.astype(np.float64), f32(x), grads=False)["out"]
+    out = net.forward_host(x)
+    assert_close(out, out_ref, TOL[Precision.tf32], "reference forward of exported weights")
+    net2 = Network.from_model(f, B)
+    assert np.array_equal(net2.get_params(), net.get_params())
+    net.close()
+    net2.close()
