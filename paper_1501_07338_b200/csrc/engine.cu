@@ -274,9 +274,17 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
   return launch_conv_fwd(d, in, W, b, l.spec.act, l.out, n->precision, n->ws, st, l.wf);
 }
 
-int run_forward(vcnn_net* n, int B) {
+// the last layer is a small full layer: its forward, the loss and its
+// backward run as one kernel in training steps (launch_head)
+bool head_fused(const vcnn_net* n, int B) {
+  const LayerRt& l = n->L.back();
+  return l.spec.kind == VCNN_LAYER_FULL && head_fusable(B, (int)l.in_per, l.spec.units);
+}
+
+int run_forward(vcnn_net* n, int B, bool skip_head = false) {
   const cudaStream_t st = n->stream;
-  for (size_t i = 0; i < n->L.size(); ++i) {
+  const size_t nl = skip_head ? n->L.size() - 1 : n->L.size();
+  for (size_t i = 0; i < nl; ++i) {
     LayerRt& l = n->L[i];
     const float* in = i == 0 ? n->x : n->L[i - 1].out;
     const float* W = n->params + l.w_off;
@@ -300,11 +308,23 @@ int run_forward(vcnn_net* n, int B) {
   return VCNN_OK;
 }
 
-int run_backward(vcnn_net* n, int B) {
+int run_backward(vcnn_net* n, int B, bool head = false) {
   const cudaStream_t st = n->stream;
   LayerRt& last = n->L.back();
-  {
-    Mark m(n, OTHER_F, (int)n->L.size() - 1, OP_LOSS);
+  const int nl = (int)n->L.size();
+  if (head) {  // last full layer fwd + loss + its backward, one kernel
+    Mark m(n, OTHER_F, nl - 1, OP_LOSS);
+    const LayerRt* prev = nl > 1 ? &n->L[nl - 2] : nullptr;
+    int act_prev = prev ? prev->spec.act : VCNN_ACT_IDENTITY;
+    // below a pool fused into its conv: hand down dP * conv_act'(pooled)
+    if (nl > 2 && fused_pool_of(n, (size_t)(nl - 3), B)) act_prev = n->L[nl - 3].spec.act;
+    TRY(launch_head(B, (int)last.in_per, last.spec.units, prev ? prev->out : n->x,
+                    n->params + last.w_off, n->params + last.b_off, last.spec.act, last.out,
+                    n->spec.loss, n->cls, n->values, n->loss, last.gpre, n->grads + last.w_off,
+                    n->grads + last.b_off, prev ? prev->gpre : nullptr, act_prev, n->err,
+                    st));
+  } else {
+    Mark m(n, OTHER_F, nl - 1, OP_LOSS);
     TRY(launch_loss(n->spec.loss, B, (int)n->out_units, last.out, n->cls, n->values, n->loss,
                     last.gpre, last.spec.act, n->err, st));
   }
@@ -313,7 +333,7 @@ int run_backward(vcnn_net* n, int B) {
   const bool par = n->side && !n->breakdown;
   const cudaStream_t sw = par ? n->side : st;
   const Workspace& wsw = par ? n->ws2 : n->ws;
-  for (int i = (int)n->L.size() - 1; i >= 0; --i) {
+  for (int i = head ? nl - 2 : nl - 1; i >= 0; --i) {
     LayerRt& l = n->L[i];
     if (par) {  // this layer's gradient inputs are ready on the main stream
       VCNN_CUDA_TRY(cudaEventRecord(n->fork_ev[i], st));
@@ -455,8 +475,9 @@ void drop_graph(vcnn_net* n) {
 
 int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   const int64_t before = g_launches.load();
-  TRY(run_forward(n, batch));
-  TRY(run_backward(n, batch));
+  const bool head = head_fused(n, batch);
+  TRY(run_forward(n, batch, head));
+  TRY(run_backward(n, batch, head));
   TRY(run_sgd(n, lr, mom, 1.0f));
   n->kernels_per_step = (int)(g_launches.load() - before);
   return VCNN_OK;
@@ -883,8 +904,9 @@ int vcnn_net_set_batch_device(vcnn_net* n, int batch, const float* x, const int*
 int vcnn_net_forward_backward(vcnn_net* n, int batch) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
   TRY(check_batch(n, batch));
-  TRY(run_forward(n, batch));
-  return run_backward(n, batch);
+  const bool head = head_fused(n, batch);
+  TRY(run_forward(n, batch, head));
+  return run_backward(n, batch, head);
 }
 
 int vcnn_net_forward(vcnn_net* n, int batch) {

@@ -70,6 +70,13 @@ int launch_gather_rows(int n, int64_t per, const float* src, const int* order, i
                        float* dst, int64_t tper, const int* cls_src, int* cls_dst,
                        const float* val_src, float* val_dst, cudaStream_t st);
 int launch_store_scalar(const float* src, float* dst, cudaStream_t st);
+// the network head fused: last full layer fwd + loss fwd/bwd + its
+// dW / db / dX (dX * act_prev'(x)); one CTA, fp32
+bool head_fusable(int B, int in, int out);
+int launch_head(int B, int in, int out, const float* x, const float* W, const float* bias,
+                int act, float* y, int loss_kind, const int* cls, const float* values,
+                float* loss, float* gpre, float* dW, float* db, float* dx, int act_prev, int* err,
+                cudaStream_t st);
 int launch_accumulate(const float* values, const int64_t* source, const int64_t* target,
                       int64_t pairs, int64_t target_len, int reducer, float* out, int64_t* arg,
                       cudaStream_t st);

@@ -5,6 +5,7 @@
 // per-thread partials + a fixed shared-memory tree), scatters of the
 // reference (col2im, pool_backward) are rewritten as gathers so no float
 // atomics are needed.  Reference paths: /root/reference/proj/include/vcnn.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -695,6 +696,203 @@ int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
     VCNN_CUDA_TRY(launch_pdl(mse_kernel, dim3(1), dim3(kLossThreads), 0, st, (int64_t)B * units, pred, values, loss, grad,
                                            act_last));
   }
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+// The network head in ONE kernel: the last full layer forward, the loss
+// forward + backward, and the layer's weight / bias / data gradients
+// (full_forward + loss_forward/backward + full_backward_core, layers.hpp:
+// 230-267, :402-468), replacing 4 launches on the critical path.  One thread-
+// block cluster: CTA r owns batch rows [r*R, (r+1)*R) for the forward, the
+// loss and dx; its partial dW/db over those rows stays in its shared memory
+// and, after a cluster barrier, CTA r reduces slice r of dW/db over the
+// cluster's CTAs through distributed shared memory in rank order (CTA 0 also
+// the loss).  fp32 throughout, every reduction in a fixed order.
+constexpr int kHeadThreads = 256;
+constexpr int kHeadCluster = 8;
+
+__global__ void __launch_bounds__(kHeadThreads) head_kernel(
+    int B, int in, int out, const float* __restrict__ x, const float* __restrict__ W,
+    const float* __restrict__ bias, int act, float* __restrict__ y, int loss_kind,
+    const int* __restrict__ cls, const float* __restrict__ values, float* __restrict__ loss,
+    float* __restrict__ gpre, float* __restrict__ dW, float* __restrict__ db,
+    float* __restrict__ dx, int act_prev, int* __restrict__ err) {
+  PDL_ENTRY();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+  const int R = (B + C - 1) / C;
+  const int r0 = rank * R < B ? rank * R : B;
+  const int nr = (r0 + R <= B ? R : B - r0);
+  const int ld = in + 1;  // padded rows: conflict-free strided reads
+  const int np = out * ld;  // dW row o = [dW[o][0..in), db[o]]
+  extern __shared__ float hs[];
+  float* part = hs;                  // [out][ld] partial dW | db over my rows
+  float* ws = part + np;             // [out][ld]
+  float* xs = ws + np;               // [R][ld]
+  float* gs = xs + (size_t)R * ld;   // [R][out]: y, then the gradient
+  __shared__ float red[32];
+  __shared__ float loss_part;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const float* xg = x + (size_t)r0 * in;
+  for (int i = tid; i < nr * in; i += nt) xs[i + i / in] = xg[i];
+  for (int i = tid; i < out * in; i += nt) ws[i + i / in] = W[i];
+  __syncthreads();
+  // forward: y = act(x W^T + b)
+  for (int t = tid; t < nr * out; t += nt) {
+    const int bb = t / out, o = t - bb * out;
+    const float* xr = xs + (size_t)bb * ld;
+    const float* wr = ws + (size_t)o * ld;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    int k = 0;
+    for (; k + 3 < in; k += 4) {
+      a0 += xr[k] * wr[k];
+      a1 += xr[k + 1] * wr[k + 1];
+      a2 += xr[k + 2] * wr[k + 2];
+      a3 += xr[k + 3] * wr[k + 3];
+    }
+    for (; k < in; ++k) a0 += xr[k] * wr[k];
+    const float v = act_fwd(act, ((a0 + a1) + (a2 + a3)) + bias[o]);
+    gs[t] = v;
+    y[(size_t)r0 * out + t] = v;
+  }
+  __syncthreads();
+  // loss + dL/dy * act'(y): one thread per sample (softmax-CE) or element (MSE)
+  float mine = 0.f;
+  if (loss_kind == VCNN_LOSS_SOFTMAX_CE) {
+    const float inv_b = 1.0f / (float)B;
+    for (int bb = tid; bb < nr; bb += nt) {
+      float* l = gs + (size_t)bb * out;
+      const int c = cls[r0 + bb];
+      const bool bad = c < 0 || c >= out;
+      if (bad && err) atomicExch(err, 1);
+      float m = l[0];
+      for (int u = 1; u < out; ++u) m = fmaxf(m, l[u]);
+      float sum = 0.f;
+      for (int u = 0; u < out; ++u) sum += expf(l[u] - m);
+      if (!bad) mine += m + logf(sum) - l[c];
+      const float inv = inv_b / sum;
+      for (int u = 0; u < out; ++u) {
+        const float yv = l[u];
+        float gv = expf(yv - m) * inv;
+        if (u == c) gv -= inv_b;
+        if (act != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(act, yv);
+        l[u] = gv;
+      }
+    }
+  } else {
+    const float scale = 2.0f / (float)(B * out);
+    const float* vg = values + (size_t)r0 * out;
+    for (int t = tid; t < nr * out; t += nt) {
+      const float yv = gs[t], dd = yv - vg[t];
+      mine += dd * dd;
+      float gv = scale * dd;
+      if (act != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(act, yv);
+      gs[t] = gv;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((tid & 31) == 0) red[tid >> 5] = mine;
+  __syncthreads();
+  if (tid < 32) {
+    float v = tid < (nt >> 5) ? red[tid] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (tid == 0) loss_part = v;
+  }
+  for (int t = tid; t < nr * out; t += nt) gpre[(size_t)r0 * out + t] = gs[t];
+  // partial dW[o][i] = sum_{my b} g[b][o] x[b][i]; db[o] = sum_{my b} g[b][o]
+  for (int t = tid; t < np; t += nt) {
+    const int o = t / ld, i = t - o * ld;
+    float a0 = 0.f, a1 = 0.f;
+    int bb = 0;
+    if (i < in) {
+      for (; bb + 1 < nr; bb += 2) {
+        a0 += gs[bb * out + o] * xs[(size_t)bb * ld + i];
+        a1 += gs[(bb + 1) * out + o] * xs[(size_t)(bb + 1) * ld + i];
+      }
+      for (; bb < nr; ++bb) a0 += gs[bb * out + o] * xs[(size_t)bb * ld + i];
+    } else {
+      for (; bb + 1 < nr; bb += 2) {
+        a0 += gs[bb * out + o];
+        a1 += gs[(bb + 1) * out + o];
+      }
+      for (; bb < nr; ++bb) a0 += gs[bb * out + o];
+    }
+    part[t] = a0 + a1;
+  }
+  // dx[b][i] = (sum_o g[b][o] W[o][i]) * act_prev'(x[b][i])
+  if (dx) {
+    float* dxg = dx + (size_t)r0 * in;
+    for (int t = tid; t < nr * in; t += nt) {
+      const int bb = t / in, i = t - bb * in;
+      float acc = 0.f;
+      for (int o = 0; o < out; ++o) acc += gs[bb * out + o] * ws[(size_t)o * ld + i];
+      if (act_prev != VCNN_ACT_IDENTITY)
+        acc *= act_grad_from_out(act_prev, xs[(size_t)bb * ld + i]);
+      dxg[t] = acc;
+    }
+  }
+  cluster.sync();  // every CTA's partials are visible cluster-wide
+  const int per = (np + C - 1) / C;
+  const int e0 = rank * per, e1 = e0 + per < np ? e0 + per : np;
+  for (int e = e0 + tid; e < e1; e += nt) {
+    float acc = 0.f;
+    for (int c = 0; c < C; ++c) acc += *cluster.map_shared_rank(part + e, c);
+    const int o = e / ld, i = e - o * ld;
+    if (i < in) dW[(size_t)o * in + i] = acc;
+    else db[o] = acc;
+  }
+  if (rank == 0 && tid == 0 && loss) {
+    float v = 0.f;
+    for (int c = 0; c < C; ++c) v += *cluster.map_shared_rank(&loss_part, c);
+    *loss = loss_kind == VCNN_LOSS_SOFTMAX_CE ? v / (float)B : v / (float)(B * out);
+  }
+  cluster.sync();  // no CTA leaves while its shared memory is being read
+}
+
+static int head_cluster(int B) { return B < kHeadCluster ? (B > 0 ? B : 1) : kHeadCluster; }
+
+size_t head_smem_floats(int B, int in, int out) {
+  const int C = head_cluster(B), R = (B + C - 1) / C;
+  return 2 * (size_t)out * (in + 1) + (size_t)R * (in + 1) + (size_t)R * out;
+}
+
+bool head_fusable(int B, int in, int out) {
+  return head_smem_floats(B, in, out) * sizeof(float) <= 160 * 1024 &&
+         (int64_t)B * in * out <= (1 << 20);
+}
+
+int launch_head(int B, int in, int out, const float* x, const float* W, const float* bias,
+                int act, float* y, int loss_kind, const int* cls, const float* values,
+                float* loss, float* gpre, float* dW, float* db, float* dx, int act_prev, int* err,
+                cudaStream_t st) {
+  const size_t smem = sizeof(float) * head_smem_floats(B, in, out);
+  static size_t configured = 0;
+  if (smem > configured) {
+    VCNN_CUDA_TRY(cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    configured = smem;
+  }
+  const int C = head_cluster(B);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kHeadThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = C;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  VCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, head_kernel, B, in, out, x, W, bias, act, y, loss_kind,
+                                   cls, values, loss, gpre, dW, db, dx, act_prev, err));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
