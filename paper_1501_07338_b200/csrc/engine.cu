@@ -274,16 +274,26 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
   return launch_conv_fwd(d, in, W, b, l.spec.act, l.out, n->precision, n->ws, st, l.wf);
 }
 
-// the last layer is a small full layer: its forward, the loss and its
-// backward run as one kernel in training steps (launch_head)
-bool head_fused(const vcnn_net* n, int B) {
+// How many top layers run fused with the loss in training steps: 2 when the
+// last two are small full layers (or a dense conv under a full layer;
+// launch_mlp_head), 1 when the last is a small full layer (launch_head),
+// else 0 (separate forward / loss / backward kernels).
+int tail_fused(const vcnn_net* n, int B) {
+  const size_t nl = n->L.size();
   const LayerRt& l = n->L.back();
-  return l.spec.kind == VCNN_LAYER_FULL && head_fusable(B, (int)l.in_per, l.spec.units);
+  if (l.spec.kind != VCNN_LAYER_FULL) return 0;
+  if (nl >= 2) {
+    const LayerRt& hl = n->L[nl - 2];
+    if ((hl.spec.kind == VCNN_LAYER_FULL || conv_is_dense(hl)) &&
+        mlp_head_fusable(B, (int)hl.in_per, hl.spec.units, l.spec.units))
+      return 2;
+  }
+  return head_fusable(B, (int)l.in_per, l.spec.units) ? 1 : 0;
 }
 
-int run_forward(vcnn_net* n, int B, bool skip_head = false) {
+int run_forward(vcnn_net* n, int B, int skip_top = 0) {
   const cudaStream_t st = n->stream;
-  const size_t nl = skip_head ? n->L.size() - 1 : n->L.size();
+  const size_t nl = n->L.size() - (size_t)skip_top;
   for (size_t i = 0; i < nl; ++i) {
     LayerRt& l = n->L[i];
     const float* in = i == 0 ? n->x : n->L[i - 1].out;
@@ -308,11 +318,24 @@ int run_forward(vcnn_net* n, int B, bool skip_head = false) {
   return VCNN_OK;
 }
 
-int run_backward(vcnn_net* n, int B, bool head = false) {
+int run_backward(vcnn_net* n, int B, int tail = 0) {
   const cudaStream_t st = n->stream;
   LayerRt& last = n->L.back();
   const int nl = (int)n->L.size();
-  if (head) {  // last full layer fwd + loss + its backward, one kernel
+  if (tail == 2) {  // last two layers fwd + loss + their backward, one kernel
+    Mark m(n, OTHER_F, nl - 1, OP_LOSS);
+    LayerRt& hl = n->L[nl - 2];
+    const LayerRt* prev = nl > 2 ? &n->L[nl - 3] : nullptr;
+    int act_prev = prev ? prev->spec.act : VCNN_ACT_IDENTITY;
+    if (nl > 3 && fused_pool_of(n, (size_t)(nl - 4), B)) act_prev = n->L[nl - 4].spec.act;
+    TRY(launch_mlp_head(B, (int)hl.in_per, hl.spec.units, last.spec.units,
+                        prev ? prev->out : n->x, n->params + hl.w_off, n->params + hl.b_off,
+                        hl.spec.act, n->params + last.w_off, n->params + last.b_off,
+                        last.spec.act, hl.out, last.out, n->spec.loss, n->cls, n->values,
+                        n->loss, n->err, hl.gpre, last.gpre, n->grads + hl.w_off,
+                        n->grads + hl.b_off, n->grads + last.w_off, n->grads + last.b_off,
+                        prev ? prev->gpre : nullptr, act_prev, st));
+  } else if (tail == 1) {  // last full layer fwd + loss + its backward, one kernel
     Mark m(n, OTHER_F, nl - 1, OP_LOSS);
     const LayerRt* prev = nl > 1 ? &n->L[nl - 2] : nullptr;
     int act_prev = prev ? prev->spec.act : VCNN_ACT_IDENTITY;
@@ -333,7 +356,7 @@ int run_backward(vcnn_net* n, int B, bool head = false) {
   const bool par = n->side && !n->breakdown;
   const cudaStream_t sw = par ? n->side : st;
   const Workspace& wsw = par ? n->ws2 : n->ws;
-  for (int i = head ? nl - 2 : nl - 1; i >= 0; --i) {
+  for (int i = nl - 1 - (tail ? tail : 0); i >= 0; --i) {
     LayerRt& l = n->L[i];
     if (par) {  // this layer's gradient inputs are ready on the main stream
       VCNN_CUDA_TRY(cudaEventRecord(n->fork_ev[i], st));
@@ -475,9 +498,9 @@ void drop_graph(vcnn_net* n) {
 
 int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   const int64_t before = g_launches.load();
-  const bool head = head_fused(n, batch);
-  TRY(run_forward(n, batch, head));
-  TRY(run_backward(n, batch, head));
+  const int tail = tail_fused(n, batch);
+  TRY(run_forward(n, batch, tail));
+  TRY(run_backward(n, batch, tail));
   TRY(run_sgd(n, lr, mom, 1.0f));
   n->kernels_per_step = (int)(g_launches.load() - before);
   return VCNN_OK;
@@ -904,9 +927,9 @@ int vcnn_net_set_batch_device(vcnn_net* n, int batch, const float* x, const int*
 int vcnn_net_forward_backward(vcnn_net* n, int batch) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
   TRY(check_batch(n, batch));
-  const bool head = head_fused(n, batch);
-  TRY(run_forward(n, batch, head));
-  return run_backward(n, batch, head);
+  const int tail = tail_fused(n, batch);
+  TRY(run_forward(n, batch, tail));
+  return run_backward(n, batch, tail);
 }
 
 int vcnn_net_forward(vcnn_net* n, int batch) {

@@ -71,12 +71,20 @@ int launch_gather_rows(int n, int64_t per, const float* src, const int* order, i
                        const float* val_src, float* val_dst, cudaStream_t st);
 int launch_store_scalar(const float* src, float* dst, cudaStream_t st);
 // the network head fused: last full layer fwd + loss fwd/bwd + its
-// dW / db / dX (dX * act_prev'(x)); one CTA, fp32
+// dW / db / dX (dX * act_prev'(x)); one cluster, fp32
 bool head_fusable(int B, int in, int out);
 int launch_head(int B, int in, int out, const float* x, const float* W, const float* bias,
                 int act, float* y, int loss_kind, const int* cls, const float* values,
                 float* loss, float* gpre, float* dW, float* db, float* dx, int act_prev, int* err,
                 cudaStream_t st);
+// the two-layer tail fused (head.cu): small full layer H + last full layer O
+// fwd, loss fwd/bwd, both layers' dW / db and dX; one 16-CTA cluster
+bool mlp_head_fusable(int B, int in, int h, int out);
+int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* WH,
+                    const float* bH, int actH, const float* WO, const float* bO, int actO,
+                    float* yH, float* yO, int loss_kind, const int* cls, const float* values,
+                    float* loss, int* err, float* gH, float* gO, float* dWH, float* dbH,
+                    float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st);
 int launch_accumulate(const float* values, const int64_t* source, const int64_t* target,
                       int64_t pairs, int64_t target_len, int reducer, float* out, int64_t* arg,
                       cudaStream_t st);
