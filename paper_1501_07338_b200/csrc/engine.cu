@@ -282,7 +282,7 @@ int tail_fused(const vcnn_net* n, int B) {
   const size_t nl = n->L.size();
   const LayerRt& l = n->L.back();
   if (l.spec.kind != VCNN_LAYER_FULL) return 0;
-  if (nl >= 2) {
+  if (nl >= 2 && n->precision == VCNN_PREC_TF32) {  // its GEMMs run in TF32
     const LayerRt& hl = n->L[nl - 2];
     if ((hl.spec.kind == VCNN_LAYER_FULL || conv_is_dense(hl)) &&
         mlp_head_fusable(B, (int)hl.in_per, hl.spec.units, l.spec.units))

@@ -30,36 +30,47 @@ constexpr int kThreadsM = 512;
 
 struct Dims {
   int B, in, h, out;
-  int R, Kc;                  // rows / input columns per CTA
-  int Bp, Hp, Kp;             // padded to multiples of 4
-  int sB, sK;                 // strides of the [k][b] / [b][k] tiles
+  int R, Kc;                  // batch rows / input columns per CTA (Kc % 4 == 0)
+  int Bp, Hp, Kp;             // padded: Bp, Hp to 16 (mma M), Kp to 8 (mma K / N)
+  int sK, sH;                 // row strides: multiples of 4 floats, odd in 16B units
+  int per5;                   // dW_O | db_O elements reduced per CTA
   // smem offsets (floats)
-  int oxT, owT, oxr, owr, oP, ogT, oW5, ohs, og5, ogl, op5;
+  int oxr, owr, oPs, oG, oW5, ohs, og5, ogl, op5, obH, obO, oy5, otg;
   int total;
 };
 
 __host__ __device__ inline int up4(int v) { return (v + 3) & ~3; }
+__host__ __device__ inline int up8(int v) { return (v + 7) & ~7; }
+__host__ __device__ inline int up16(int v) { return (v + 15) & ~15; }
+// a row stride of v floats (v % 4 == 0) whose 16-byte units are odd: float4
+// accesses of 8 consecutive rows, and mma fragment loads (8 rows x 4 columns)
+// hit distinct banks
+__host__ __device__ inline int odd16(int v) { return (v >> 2) & 1 ? v : v + 4; }
 
 __host__ __device__ inline Dims dims_of(int B, int in, int h, int out) {
   Dims d;
   d.B = B; d.in = in; d.h = h; d.out = out;
   d.R = (B + kC - 1) / kC;
-  d.Kc = (in + kC - 1) / kC;
-  d.Bp = up4(B); d.Hp = up4(h); d.Kp = up4(d.Kc);
-  d.sB = d.Bp + 4;            // 16B-aligned rows, staggered banks
-  d.sK = d.Kp + 4;
+  d.Kc = up4((in + kC - 1) / kC);
+  d.Bp = up16(B); d.Hp = up16(h); d.Kp = up8(d.Kc);
+  d.sK = odd16(d.Kp);
+  d.sH = odd16(d.Hp);
+  d.per5 = (out * (h + 1) + kC - 1) / kC;
   int o = 0;
-  d.oxT = o; o += d.Kp * d.sB;        // x^T  [Kp][sB]
-  d.owT = o; o += d.Kp * (d.Hp + 4);  // W_H^T [Kp][Hp+4]
-  d.oxr = o; o += d.Bp * d.sK;        // x    [Bp][sK]
-  d.owr = o; o += d.Hp * d.sK;        // W_H  [Hp][sK]
-  d.oP = o;  o += d.Bp * d.Hp;        // partial x W_H^T [Bp][Hp]; later gH [Bp][Hp]
-  d.ogT = o; o += d.Hp * d.sB;        // gH^T [Hp][sB]
-  d.oW5 = o; o += out * (h + 1);      // W_O  [out][h+1]
+  d.oxr = o; o += d.Bp * d.sK;        // x[:, mine]   [Bp][sK]
+  d.owr = o; o += d.Hp * d.sK;        // W_H[:, mine] [Hp][sK]
+  d.oPs = o; o += kC * d.R * d.sH;    // pushed partials of my rows [src rank][R][sH]
+  d.oG = o;  o += d.Bp * d.sH;        // gH, all rows (pushed by the row owners) [Bp][sH]
+  d.oW5 = o; o += out * (h + 1);      // W_O [out][h+1]
   d.ohs = o; o += d.R * (h + 1);      // h rows [R][h+1]
   d.og5 = o; o += d.R * out;          // y / gO rows [R][out]
-  d.ogl = o; o += d.R * d.Hp;         // gH rows [R][Hp] (all-gathered by the cluster)
-  d.op5 = o; o += out * (h + 1);      // partial dW_O | db_O [out][h+1]
+  o = up4(o);
+  d.ogl = o; o += d.R * d.sH;         // my gH rows [R][sH] (float4 pushes)
+  d.op5 = o; o += kC * d.per5;        // pushed dW_O | db_O partials [src rank][per5]
+  d.obH = o; o += h;                  // b_H
+  d.obO = o; o += out;                // b_O
+  d.oy5 = o; o += d.R * out;          // y rows (stored after the exchange)
+  d.otg = o; o += d.R * out;          // my rows' targets (class ids or values)
   d.total = o;
   return d;
 }
@@ -74,88 +85,222 @@ struct MlpArgs {
   float* gH; float* gO;       // dL/d(pre-activation) of each layer
   float* dWH; float* dbH; float* dWO; float* dbO;
   float* dx; int act_prev;    // dx * act_prev'(x); null for the first layer
+  int vec;                    // x / W_H rows 16B aligned: float4 staging
 };
 
+#ifdef VCNN_PHASE_TIMING
+__device__ unsigned long long g_hphase[kC][16];
+#define HPHASE(i)                                                   \
+  do {                                                              \
+    if (threadIdx.x == 0) g_hphase[blockIdx.x % kC][i] = clock64(); \
+  } while (0)
+#else
+#define HPHASE(i) \
+  do {            \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t tf32(float f) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+  return r;
+}
+
+// One warp's m16 x (NG x n8) tile of C += A B over ksteps k8 steps with
+// mma.sync TF32 (the tensor-core path for these small per-CTA GEMMs; fp32
+// accumulate).  A(m, k) = A[m*am + k*ak], B(k, n) = Bm[n*bn + k*bk]; the
+// fragment layouts are the PTX m16n8k8 .row.col ones: lane = 4g + t,
+// a = {(g,t), (g+8,t), (g,t+4), (g+8,t+4)}, b = {(t,g), (t+4,g)},
+// c = {(g,2t), (g,2t+1), (g+8,2t), (g+8,2t+1)}.
+template <int NG>
+__device__ __forceinline__ void warp_mma(float (&c)[NG][4], const float* A, int am, int ak,
+                                         const float* Bm, int bn, int bk, int m0, int n0,
+                                         int nvalid, int ksteps, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const float* pa = A + (m0 + g) * am + t * ak;
+  const float* pb = Bm + (n0 + g) * bn + t * bk;
+  for (int ks = 0; ks < ksteps; ++ks) {
+    const int k = ks * 8;
+    const uint32_t a0 = tf32(pa[k * ak]), a1 = tf32(pa[8 * am + k * ak]);
+    const uint32_t a2 = tf32(pa[(k + 4) * ak]), a3 = tf32(pa[8 * am + (k + 4) * ak]);
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      if (j < nvalid) {
+        const uint32_t b0 = tf32(pb[j * 8 * bn + k * bk]);
+        const uint32_t b1 = tf32(pb[j * 8 * bn + (k + 4) * bk]);
+        asm volatile(
+            "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+            "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(c[j][0]), "+f"(c[j][1]), "+f"(c[j][2]), "+f"(c[j][3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      }
+    }
+  }
+}
+
+// stage rows [0, nrows) x columns [k0, k0+nc) of a row-major [*][ld] matrix
+// into smem [Rp][s] (zero padded to Rp rows and Kp columns)
+__device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, int ld, int nrows,
+                                           int Rp, int k0, int nc, int Kp, bool vec, int tid,
+                                           int nt) {
+  if (vec) {  // float4: Kp, k0, ld multiples of 4, src 16B aligned
+    const int q = Kp >> 2, n = Rp * q;
+    constexpr int kU = 4;
+    for (int base = 0; base < n; base += kU * nt) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = base + u * nt + tid, r = i / q, k = 4 * (i - r * q);
+        v[u] = (r < nrows && k < nc)
+                   ? __ldg(reinterpret_cast<const float4*>(src + (size_t)r * ld + k0 + k))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = base + u * nt + tid, r = i / q, k = 4 * (i - r * q);
+        if (i < n) *reinterpret_cast<float4*>(dst + r * s + k) = v[u];
+      }
+    }
+  } else {
+    const int n = Rp * Kp;
+    for (int i = tid; i < n; i += nt) {
+      const int r = i / Kp, k = i - r * Kp;
+      dst[r * s + k] = (r < nrows && k < nc) ? __ldg(src + (size_t)r * ld + k0 + k) : 0.f;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
+  HPHASE(0);
+  // every CTA of the cluster has started before anyone writes into its smem
+  cluster_arrive_relaxed();
   PDL_ENTRY();
+  HPHASE(1);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const Dims d = dims_of(a.B, a.in, a.h, a.out);
   const int B = a.B, in = a.in, h = a.h, out = a.out;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = nt >> 5;
   extern __shared__ __align__(16) float sm[];
-  float* xT = sm + d.oxT;
-  float* wT = sm + d.owT;
   float* xr = sm + d.oxr;
   float* wr = sm + d.owr;
-  float* P = sm + d.oP;
-  float* gT = sm + d.ogT;
+  float* Ps = sm + d.oPs;
+  float* G = sm + d.oG;
   float* W5 = sm + d.oW5;
   float* hs = sm + d.ohs;
   float* g5 = sm + d.og5;
   float* gl = sm + d.ogl;
   float* p5 = sm + d.op5;
-  __shared__ float red[32];
-  __shared__ float loss_part;
-  const int sW = d.Hp + 4, lh = h + 1;
+  float* sbH = sm + d.obH;
+  float* sbO = sm + d.obO;
+  float* y5 = sm + d.oy5;
+  float* tg = sm + d.otg;
+  __shared__ float lossp[kC];
+  __shared__ float rowloss[kThreadsM / 32];
+  const int lh = h + 1, sK = d.sK, sH = d.sH;
 
-  // ---- stage: my input columns of x and W_H (zero padded), all of W_O ----
+  // ---- stage my input columns of x and W_H (zero padded), all of W_O ----
   const int k0 = rank * d.Kc < in ? rank * d.Kc : in;
   const int nc = k0 + d.Kc <= in ? d.Kc : in - k0;
-  for (int i = tid; i < d.Bp * d.Kp; i += nt) {
-    const int b = i / d.Kp, k = i - b * d.Kp;
-    const float v = (b < B && k < nc) ? __ldg(a.x + (size_t)b * in + k0 + k) : 0.f;
-    xr[b * d.sK + k] = v;
-    xT[k * d.sB + b] = v;
-  }
-  for (int i = tid; i < d.Hp * d.Kp; i += nt) {
-    const int o = i / d.Kp, k = i - o * d.Kp;
-    const float v = (o < h && k < nc) ? __ldg(a.WH + (size_t)o * in + k0 + k) : 0.f;
-    wr[o * d.sK + k] = v;
-    wT[k * sW + o] = v;
-  }
-  for (int i = tid; i < out * h; i += nt) {
-    const int o = i / h, k = i - o * h;
-    W5[o * lh + k] = __ldg(a.WO + i);
-  }
-  __syncthreads();
-
-  // ---- 1: partial P = x[:, mine] W_H[:, mine]^T  ([Bp][Hp], 4x4 tiles) ----
-  {
-    const int th = d.Hp >> 2, nt1 = (d.Bp >> 2) * th;
-    for (int t = tid; t < nt1; t += nt) {
-      const int tb = t / th, to = t - tb * th;
-      float acc[4][4] = {};
-      for (int k = 0; k < d.Kp; ++k) {
-        const float4 xv = *reinterpret_cast<const float4*>(xT + k * d.sB + 4 * tb);
-        const float4 wv = *reinterpret_cast<const float4*>(wT + k * sW + 4 * to);
-        const float xa[4] = {xv.x, xv.y, xv.z, xv.w}, wa[4] = {wv.x, wv.y, wv.z, wv.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(xa[i], wa[j], acc[i][j]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        *reinterpret_cast<float4*>(P + (4 * tb + i) * d.Hp + 4 * to) =
-            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-    }
-  }
-  cluster.sync();
-
-  // ---- 2: my rows: h = act(sum_c P_c + b), then the last layer + loss ----
+  // the small operands phase 2 reads (W_O, b_H, b_O, my rows' targets) are
+  // loaded into registers first so their latency overlaps the x / W_H staging
   const int r0 = rank * d.R < B ? rank * d.R : B;
   const int nr = r0 + d.R <= B ? d.R : B - r0;
+  const bool ce = a.loss_kind == VCNN_LOSS_SOFTMAX_CE;
+  const int nw5 = out * h, ntg = ce ? nr : nr * out;
+  const int nsmall = nw5 + h + out + ntg;
+  auto small_src = [&](int i) -> float {
+    if (i < nw5) return __ldg(a.WO + i);
+    i -= nw5;
+    if (i < h) return __ldg(a.bH + i);
+    i -= h;
+    if (i < out) return __ldg(a.bO + i);
+    i -= out;
+    return ce ? __int_as_float(__ldg(a.cls + r0 + i)) : __ldg(a.values + (size_t)r0 * out + i);
+  };
+  auto small_dst = [&](int i) -> float* {
+    if (i < nw5) return W5 + (i / h) * lh + (i - (i / h) * h);
+    i -= nw5;
+    if (i < h) return sbH + i;
+    i -= h;
+    if (i < out) return sbO + i;
+    return tg + (i - out);
+  };
+  constexpr int kS = 4;
+  float sv[kS];
+#pragma unroll
+  for (int u = 0; u < kS; ++u) {
+    const int i = tid + u * nt;
+    sv[u] = i < nsmall ? small_src(i) : 0.f;
+  }
+  stage_cols(xr, sK, a.x, in, B, d.Bp, k0, nc, d.Kp, a.vec, tid, nt);
+  stage_cols(wr, sK, a.WH, in, h, d.Hp, k0, nc, d.Kp, a.vec, tid, nt);
+#pragma unroll
+  for (int u = 0; u < kS; ++u) {
+    const int i = tid + u * nt;
+    if (i < nsmall) *small_dst(i) = sv[u];
+  }
+  for (int i = tid + kS * nt; i < nsmall; i += nt) *small_dst(i) = small_src(i);
+  for (int i = tid; i < (d.Bp - B) * sH; i += nt) G[B * sH + i] = 0.f;  // pad rows
+  if (tid < kThreadsM / 32) rowloss[tid] = 0.f;
+  __syncthreads();
+  HPHASE(2);
+
+  // ---- 1: partial x[:, mine] W_H[:, mine]^T on the tensor cores (m16 = 16
+  //         batch rows, n = 4 x n8 hidden units per warp tile), pushed to the
+  //         row owner's slot [rank] ----
+  cluster_wait();
+  {
+    const int mt = d.Bp >> 4, nN = d.Hp >> 3, ngr = (nN + 3) >> 2;
+    for (int tile = warp; tile < mt * ngr; tile += nwarps) {
+      const int im = tile / ngr, ig = tile - im * ngr;
+      const int m0 = im * 16, n0 = ig * 32;
+      const int nv = nN - ig * 4 < 4 ? nN - ig * 4 : 4;
+      float c[4][4] = {};
+      warp_mma<4>(c, xr, sK, 1, wr, sK, 1, m0, n0, nv, d.Kp >> 3, lane);
+      const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int b = m0 + g + 8 * hf;
+        if (b >= B) continue;
+        const int owner = b / d.R;
+        float* dst = cluster.map_shared_rank(Ps, owner) + (rank * d.R + (b - owner * d.R)) * sH;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int o = n0 + j * 8 + 2 * t;
+          if (j < nv && o < h)  // o even, h may be odd: o + 1 < Hp always
+            *reinterpret_cast<float2*>(dst + o) = make_float2(c[j][2 * hf], c[j][2 * hf + 1]);
+        }
+      }
+    }
+  }
+  HPHASE(3);
+  cluster_arrive();
+  cluster_wait();
+  HPHASE(4);
+
+  // ---- 2: my rows: h = act(sum over ranks, in order + b); the last layer,
+  //         the loss, dW_O partials, gH rows ----
   for (int e = tid; e < nr * h; e += nt) {
     const int b = e / h, o = e - b * h;
-    const float* src = P + (r0 + b) * d.Hp + o;
     float acc = 0.f;
-    for (int c = 0; c < kC; ++c) acc += *cluster.map_shared_rank(src, c);
-    const float v = act_fwd(a.actH, acc + __ldg(a.bH + o));
-    hs[b * lh + o] = v;
-    a.yH[(size_t)(r0 + b) * h + o] = v;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) acc += Ps[(c * d.R + b) * sH + o];
+    hs[b * lh + o] = act_fwd(a.actH, acc + sbH[o]);
   }
   __syncthreads();
+  HPHASE(10);
   for (int e = tid; e < nr * out; e += nt) {
     const int b = e / out, o = e - b * out;
     const float* hr = hs + b * lh;
@@ -169,26 +314,34 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
       a3 += hr[k + 3] * wo[k + 3];
     }
     for (; k < h; ++k) a0 += hr[k] * wo[k];
-    const float v = act_fwd(a.actO, ((a0 + a1) + (a2 + a3)) + __ldg(a.bO + o));
+    const float v = act_fwd(a.actO, ((a0 + a1) + (a2 + a3)) + sbO[o]);
     g5[e] = v;
-    a.yO[(size_t)r0 * out + e] = v;
+    y5[e] = v;
   }
   __syncthreads();
-  float mine = 0.f;
-  if (a.loss_kind == VCNN_LOSS_SOFTMAX_CE) {
+  HPHASE(11);
+  // loss + dL/dy * act'(y).  softmax-CE: one warp per sample, lanes over
+  // the classes (shuffle-tree max / sum); MSE: one thread per element.  The
+  // partial loss: per-warp values summed by thread 0 in warp order.
+  if (ce) {
     const float inv_b = 1.0f / (float)B;
-    for (int b = tid; b < nr; b += nt) {
+    for (int b = warp; b < nr; b += nwarps) {
       float* l = g5 + b * out;
-      const int c = a.cls[r0 + b];
+      const int c = __float_as_int(tg[b]);
       const bool bad = c < 0 || c >= out;
-      if (bad && a.err) atomicExch(a.err, 1);
-      float m = l[0];
-      for (int u = 1; u < out; ++u) m = fmaxf(m, l[u]);
+      if (bad && a.err && lane == 0) atomicExch(a.err, 1);
+      float m = -INFINITY;
+      for (int u = lane; u < out; u += 32) m = fmaxf(m, l[u]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
       float sum = 0.f;
-      for (int u = 0; u < out; ++u) sum += expf(l[u] - m);
-      if (!bad) mine += m + logf(sum) - l[c];
+      for (int u = lane; u < out; u += 32) sum += expf(l[u] - m);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0 && !bad) rowloss[warp] += m + logf(sum) - l[c];
+      __syncwarp();
       const float inv = inv_b / sum;
-      for (int u = 0; u < out; ++u) {
+      for (int u = lane; u < out; u += 32) {
         const float yv = l[u];
         float gv = expf(yv - m) * inv;
         if (u == c) gv -= inv_b;
@@ -198,27 +351,26 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     }
   } else {
     const float scale = 2.0f / (float)(B * out);
-    const float* vg = a.values + (size_t)r0 * out;
+    float mine = 0.f;
     for (int t = tid; t < nr * out; t += nt) {
-      const float yv = g5[t], dd = yv - vg[t];
+      const float yv = g5[t], dd = yv - tg[t];
       mine += dd * dd;
       float gv = scale * dd;
       if (a.actO != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(a.actO, yv);
       g5[t] = gv;
     }
-  }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if ((tid & 31) == 0) red[tid >> 5] = mine;
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if (lane == 0) rowloss[warp] += mine;
+  }
   __syncthreads();
-  if (tid < 32) {
-    float v = tid < (nt >> 5) ? red[tid] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (tid == 0) loss_part = v;
+  if (tid == 0) {
+    float v = 0.f;
+    for (int w = 0; w < nwarps; ++w) v += rowloss[w];
+    *cluster.map_shared_rank(lossp + rank, 0) = v;
   }
-  for (int t = tid; t < nr * out; t += nt) a.gO[(size_t)r0 * out + t] = g5[t];
-  // partial dW_O | db_O over my rows
+  HPHASE(12);
+  // dW_O | db_O partials over my rows, pushed to the slice owner's slot [rank]
   for (int t = tid; t < out * lh; t += nt) {
     const int o = t / lh, i = t - o * lh;
     float acc = 0.f;
@@ -226,7 +378,8 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
       for (int b = 0; b < nr; ++b) acc += g5[b * out + o] * hs[b * lh + i];
     else
       for (int b = 0; b < nr; ++b) acc += g5[b * out + o];
-    p5[t] = acc;
+    const int c = t / d.per5;
+    *cluster.map_shared_rank(p5 + rank * d.per5 + (t - c * d.per5), c) = acc;
   }
   // gH rows = (gO W_O) * act_H'(h), zero padded to Hp
   for (int t = tid; t < d.R * d.Hp; t += nt) {
@@ -235,31 +388,44 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     if (b < nr && i < h) {
       for (int o = 0; o < out; ++o) acc += g5[b * out + o] * W5[o * lh + i];
       if (a.actH != VCNN_ACT_IDENTITY) acc *= act_grad_from_out(a.actH, hs[b * lh + i]);
-      a.gH[(size_t)(r0 + b) * h + i] = acc;
     }
-    gl[t] = acc;
+    gl[b * sH + i] = acc;
   }
-  cluster.sync();
-
-  // ---- 3: all-gather gH ([Bp][Hp] into P's space and transposed), reduce
-  //         my slice of dW_O | db_O and (rank 0) the loss, in rank order ----
-  float* G = P;
-  for (int e = tid; e < d.Bp * d.Hp; e += nt) {
-    const int b = e / d.Hp, o = e - b * d.Hp;
-    float v = 0.f;
-    if (b < B) {
-      const int c = b / d.R;
-      v = *cluster.map_shared_rank(gl + (b - c * d.R) * d.Hp + o, c);
-    }
-    G[e] = v;
-    gT[o * d.sB + b] = v;
-  }
+  __syncthreads();
+  HPHASE(13);
+  // push my gH rows into every CTA's G (float4)
   {
-    const int np = out * lh, per = (np + kC - 1) / kC;
-    const int e0 = rank * per, e1 = e0 + per < np ? e0 + per : np;
+    const int q = d.Hp >> 2, n = nr * q * kC;
+    for (int t = tid; t < n; t += nt) {
+      const int c = t / (nr * q), u = t - c * (nr * q), b = u / q, k = 4 * (u - b * q);
+      *reinterpret_cast<float4*>(cluster.map_shared_rank(G, c) + (r0 + b) * sH + k) =
+          *reinterpret_cast<const float4*>(gl + b * sH + k);
+    }
+  }
+  HPHASE(5);
+  cluster_arrive();
+  cluster_wait();
+  HPHASE(6);
+  // my rows' layer outputs and gradients (stored after the exchange: the
+  // cluster barrier's release would otherwise wait for them)
+  for (int e = tid; e < nr * h; e += nt) {
+    const int b = e / h, o = e - b * h;
+    a.yH[(size_t)r0 * h + e] = hs[b * lh + o];
+    a.gH[(size_t)r0 * h + e] = gl[b * sH + o];
+  }
+  for (int e = tid; e < nr * out; e += nt) {
+    a.yO[(size_t)r0 * out + e] = y5[e];
+    a.gO[(size_t)r0 * out + e] = g5[e];
+  }
+
+  // ---- 3: my slice of dW_O | db_O and (rank 0) the loss, summed in rank order ----
+  {
+    const int np = out * lh, e0 = rank * d.per5;
+    const int e1 = e0 + d.per5 < np ? e0 + d.per5 : np;
     for (int e = e0 + tid; e < e1; e += nt) {
       float acc = 0.f;
-      for (int c = 0; c < kC; ++c) acc += *cluster.map_shared_rank(p5 + e, c);
+#pragma unroll
+      for (int c = 0; c < kC; ++c) acc += p5[c * d.per5 + (e - e0)];
       const int o = e / lh, i = e - o * lh;
       if (i < h) a.dWO[(size_t)o * h + i] = acc;
       else a.dbO[o] = acc;
@@ -267,77 +433,85 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   }
   if (rank == 0 && tid == 0 && a.loss) {
     float v = 0.f;
-    for (int c = 0; c < kC; ++c) v += *cluster.map_shared_rank(&loss_part, c);
+    for (int c = 0; c < kC; ++c) v += lossp[c];
     *a.loss = a.loss_kind == VCNN_LOSS_SOFTMAX_CE ? v / (float)B : v / (float)(B * out);
   }
-  __syncthreads();
-
-  // ---- 4a: dW_H[:, mine] = gH^T x[:, mine]  ([Hp][Kp]); db_H on rank 0 ----
-  {
-    const int tk = d.Kp >> 2, nt4 = (d.Hp >> 2) * tk;
-    for (int t = tid; t < nt4; t += nt) {
-      const int to = t / tk, tc = t - to * tk;
-      float acc[4][4] = {};
-      for (int b = 0; b < d.Bp; ++b) {
-        const float4 gv = *reinterpret_cast<const float4*>(G + b * d.Hp + 4 * to);
-        const float4 xv = *reinterpret_cast<const float4*>(xr + b * d.sK + 4 * tc);
-        const float ga[4] = {gv.x, gv.y, gv.z, gv.w}, xa[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ga[i], xa[j], acc[i][j]);
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int o = 4 * to + i;
-        if (o >= h) break;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (4 * tc + j < nc) a.dWH[(size_t)o * in + k0 + 4 * tc + j] = acc[i][j];
-      }
+  if (rank == 0)
+    for (int o = tid; o < h; o += nt) {
+      float acc = 0.f;
+      for (int b = 0; b < B; ++b) acc += G[b * sH + o];
+      a.dbH[o] = acc;
     }
-    if (rank == 0)
-      for (int o = tid; o < h; o += nt) {
-        float acc = 0.f;
-        for (int b = 0; b < B; ++b) acc += G[b * d.Hp + o];
-        a.dbH[o] = acc;
-      }
-  }
-  // ---- 4b: dx[:, mine] = (gH W_H[:, mine]) * act_prev'(x)  ([Bp][Kp]) ----
-  if (a.dx) {
-    const int tk = d.Kp >> 2, nt4 = (d.Bp >> 2) * tk;
-    for (int t = tid; t < nt4; t += nt) {
-      const int tb = t / tk, tc = t - tb * tk;
-      float acc[4][4] = {};
-      for (int o = 0; o < d.Hp; ++o) {
-        const float4 gv = *reinterpret_cast<const float4*>(gT + o * d.sB + 4 * tb);
-        const float4 wv = *reinterpret_cast<const float4*>(wr + o * d.sK + 4 * tc);
-        const float ga[4] = {gv.x, gv.y, gv.z, gv.w}, wa[4] = {wv.x, wv.y, wv.z, wv.w};
+  HPHASE(7);
+
+  // ---- 4: on the tensor cores, one tile pool:
+  //         dW_H[:, mine] = gH^T x[:, mine]   (m16 hidden units x 2 n8 columns, K = batch)
+  //         dx[:, mine] = gH W_H[:, mine]      (m16 batch rows x 4 n8 columns, K = hidden)
+  //         dx *= act_prev'(x) ----
+  {
+    const int nN = d.Kp >> 3;
+    const int ga = (nN + 1) >> 1, na = (d.Hp >> 4) * ga;
+    const int gb = (nN + 3) >> 2, nb = a.dx ? (d.Bp >> 4) * gb : 0;
+    const int g = lane >> 2, t = lane & 3;
+    for (int tile = warp; tile < na + nb; tile += nwarps) {
+      if (tile < na) {
+        const int im = tile / ga, ig = tile - im * ga;
+        const int m0 = im * 16, n0 = ig * 16;
+        const int nv = nN - ig * 2 < 2 ? nN - ig * 2 : 2;
+        float c[2][4] = {};
+        warp_mma<2>(c, G, 1, sH, xr, 1, sK, m0, n0, nv, d.Bp >> 3, lane);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int hf = 0; hf < 2; ++hf) {
+          const int o = m0 + g + 8 * hf;
+          if (o >= h) continue;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ga[i], wa[j], acc[i][j]);
-      }
+          for (int j = 0; j < 2; ++j)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int b = 4 * tb + i;
-        if (b >= B) break;
+            for (int e = 0; e < 2; ++e) {
+              const int col = n0 + j * 8 + 2 * t + e;
+              if (j < nv && col < nc) a.dWH[(size_t)o * in + k0 + col] = c[j][2 * hf + e];
+            }
+        }
+      } else {
+        const int u = tile - na, im = u / gb, ig = u - im * gb;
+        const int m0 = im * 16, n0 = ig * 32;
+        const int nv = nN - ig * 4 < 4 ? nN - ig * 4 : 4;
+        float c[4][4] = {};
+        warp_mma<4>(c, G, sH, 1, wr, 1, sK, m0, n0, nv, d.Hp >> 3, lane);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int c = 4 * tc + j;
-          if (c >= nc) continue;
-          float v = acc[i][j];
-          if (a.act_prev != VCNN_ACT_IDENTITY)
-            v *= act_grad_from_out(a.act_prev, xr[b * d.sK + c]);
-          a.dx[(size_t)b * in + k0 + c] = v;
+        for (int hf = 0; hf < 2; ++hf) {
+          const int b = m0 + g + 8 * hf;
+          if (b >= B) continue;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = n0 + j * 8 + 2 * t + e;
+              if (j < nv && col < nc) {
+                float v = c[j][2 * hf + e];
+                if (a.act_prev != VCNN_ACT_IDENTITY)
+                  v *= act_grad_from_out(a.act_prev, xr[b * sK + col]);
+                a.dx[(size_t)b * in + k0 + col] = v;
+              }
+            }
         }
       }
     }
   }
-  cluster.sync();  // no CTA leaves while its shared memory is being read
+  HPHASE(8);
+  HPHASE(9);
 }
 
 }  // namespace
+
+#ifdef VCNN_PHASE_TIMING
+extern "C" int vcnn_debug_hphases(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_hphase, sizeof(unsigned long long) * kC * 16) ==
+                 cudaSuccess
+             ? 0
+             : 4;
+}
+#endif
 
 size_t mlp_head_smem(int B, int in, int h, int out) {
   return sizeof(float) * (size_t)dims_of(B, in, h, out).total;
@@ -375,7 +549,7 @@ static bool cluster_ok(size_t smem) {
 }
 
 bool mlp_head_fusable(int B, int in, int h, int out) {
-  if (B < 1 || B > 128 || h < 1 || h > 64 || out < 1 || out > 64 || in < kC || in > 64 * kC)
+  if (B < 1 || B > 128 || h < 1 || h > 64 || out < 1 || out > 64 || in < kC || in > 128 * kC)
     return false;
   const size_t smem = mlp_head_smem(B, in, h, out);
   return smem <= 200 * 1024 && cluster_ok(smem);
@@ -388,8 +562,10 @@ int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* 
                     float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st) {
   const size_t smem = mlp_head_smem(B, in, h, out);
   if (!cluster_ok(smem)) return fail(VCNN_ECUDA, "mlp head: cluster not schedulable");
+  const bool vec = in % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) |
+                                    reinterpret_cast<uintptr_t>(WH)) & 15) == 0;
   MlpArgs a{B, in, h, out, x, WH, bH, actH, WO, bO, actO, yH, yO, loss_kind, cls, values,
-            loss, err, gH, gO, dWH, dbH, dWO, dbO, dx, act_prev};
+            loss, err, gH, gO, dWH, dbH, dWO, dbO, dx, act_prev, vec ? 1 : 0};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kC);
   cfg.blockDim = dim3(kThreadsM);

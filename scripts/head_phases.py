@@ -1,0 +1,37 @@
+"""Phase timing of the fused two-layer tail kernel (debug build, `make phase`):
+clock64 stamps per CTA of one CIFAR-3 training step.  Diagnostic only."""
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.environ.setdefault("VCNN_LIB_PATH", os.path.join(ROOT, "build", "libvcnn_cuda_phase.so"))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1501_07338_b200 import spec as S  # noqa: E402
+from paper_1501_07338_b200._lib import lib  # noqa: E402
+from paper_1501_07338_b200.engine import Network  # noqa: E402
+from paper_1501_07338_b200.spec import Precision  # noqa: E402
+
+L = lib()
+L.vcnn_debug_hphases.argtypes = [C.c_void_p]
+B = 128
+spec = S.cifar3()
+net = Network(spec, B, Precision.tf32)
+rng = np.random.default_rng(0)
+x = torch.as_tensor(rng.standard_normal((B, 32 * 32 * 3), dtype=np.float32), device="cuda")
+net.load_batch(x, cls=torch.as_tensor(rng.integers(0, 10, B).astype(np.int32), device="cuda"))
+for _ in range(5):
+    net.forward_backward(B)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * 256)()
+L.vcnn_debug_hphases(buf)
+names = ["pdl-wait", "stage", "gemm1", "sync1", "reduce+head", "sync2", "gather", "gemm4", "sync3"]
+for r in range(16):
+    t = [buf[r * 16 + i] for i in range(16)]
+    print(f"cta {r:2d} " + " ".join(f"{n}={t[i + 1] - t[i]}" for i, n in enumerate(names)),
+          "total", t[9] - t[0])
+    print("        head: reduce=%d y=%d loss=%d dWO+gH=%d push=%d" % (
+        t[10] - t[4], t[11] - t[10], t[12] - t[11], t[13] - t[12], t[5] - t[13]))
