@@ -110,6 +110,10 @@ __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// out-of-line activation helpers (one copy of the switch, not one per use)
+__device__ __noinline__ float actf(int act, float x) { return act_fwd(act, x); }
+__device__ __noinline__ float actg(int act, float y) { return act_grad_from_out(act, y); }
+
 __device__ __forceinline__ uint32_t tf32(float f) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
@@ -173,6 +177,7 @@ __device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, 
     }
   } else {
     const int n = Rp * Kp;
+#pragma unroll 1
     for (int i = tid; i < n; i += nt) {
       const int r = i / Kp, k = i - r * Kp;
       dst[r * s + k] = (r < nrows && k < nc) ? __ldg(src + (size_t)r * ld + k0 + k) : 0.f;
@@ -237,21 +242,16 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     if (i < out) return sbO + i;
     return tg + (i - out);
   };
-  constexpr int kS = 4;
-  float sv[kS];
-#pragma unroll
-  for (int u = 0; u < kS; ++u) {
-    const int i = tid + u * nt;
-    sv[u] = i < nsmall ? small_src(i) : 0.f;
-  }
+  // (one straight-line copy each: this kernel runs once per step, so its
+  // instruction footprint is fetched cold -- code size is latency here)
+  const float sv0 = tid < nsmall ? small_src(tid) : 0.f;
+  const float sv1 = tid + nt < nsmall ? small_src(tid + nt) : 0.f;
   stage_cols(xr, sK, a.x, in, B, d.Bp, k0, nc, d.Kp, a.vec, tid, nt);
   stage_cols(wr, sK, a.WH, in, h, d.Hp, k0, nc, d.Kp, a.vec, tid, nt);
-#pragma unroll
-  for (int u = 0; u < kS; ++u) {
-    const int i = tid + u * nt;
-    if (i < nsmall) *small_dst(i) = sv[u];
-  }
-  for (int i = tid + kS * nt; i < nsmall; i += nt) *small_dst(i) = small_src(i);
+  if (tid < nsmall) *small_dst(tid) = sv0;
+  if (tid + nt < nsmall) *small_dst(tid + nt) = sv1;
+#pragma unroll 1
+  for (int i = tid + 2 * nt; i < nsmall; i += nt) *small_dst(i) = small_src(i);
   for (int i = tid; i < (d.Bp - B) * sH; i += nt) G[B * sH + i] = 0.f;  // pad rows
   if (tid < kThreadsM / 32) rowloss[tid] = 0.f;
   __syncthreads();
@@ -292,29 +292,33 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
 
   // ---- 2: my rows: h = act(sum over ranks, in order + b); the last layer,
   //         the loss, dW_O partials, gH rows ----
+#pragma unroll 1
   for (int e = tid; e < nr * h; e += nt) {
     const int b = e / h, o = e - b * h;
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < kC; ++c) acc += Ps[(c * d.R + b) * sH + o];
-    hs[b * lh + o] = act_fwd(a.actH, acc + sbH[o]);
+    hs[b * lh + o] = actf(a.actH, acc + sbH[o]);
   }
   __syncthreads();
   HPHASE(10);
+#pragma unroll 1
   for (int e = tid; e < nr * out; e += nt) {
     const int b = e / out, o = e - b * out;
     const float* hr = hs + b * lh;
     const float* wo = W5 + o * lh;
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     int k = 0;
+#pragma unroll 1
     for (; k + 3 < h; k += 4) {
       a0 += hr[k] * wo[k];
       a1 += hr[k + 1] * wo[k + 1];
       a2 += hr[k + 2] * wo[k + 2];
       a3 += hr[k + 3] * wo[k + 3];
     }
+#pragma unroll 1
     for (; k < h; ++k) a0 += hr[k] * wo[k];
-    const float v = act_fwd(a.actO, ((a0 + a1) + (a2 + a3)) + sbO[o]);
+    const float v = actf(a.actO, ((a0 + a1) + (a2 + a3)) + sbO[o]);
     g5[e] = v;
     y5[e] = v;
   }
@@ -325,38 +329,43 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   // partial loss: per-warp values summed by thread 0 in warp order.
   if (ce) {
     const float inv_b = 1.0f / (float)B;
+#pragma unroll 1
     for (int b = warp; b < nr; b += nwarps) {
       float* l = g5 + b * out;
       const int c = __float_as_int(tg[b]);
       const bool bad = c < 0 || c >= out;
       if (bad && a.err && lane == 0) atomicExch(a.err, 1);
       float m = -INFINITY;
+#pragma unroll 1
       for (int u = lane; u < out; u += 32) m = fmaxf(m, l[u]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
       float sum = 0.f;
+#pragma unroll 1
       for (int u = lane; u < out; u += 32) sum += expf(l[u] - m);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       if (lane == 0 && !bad) rowloss[warp] += m + logf(sum) - l[c];
       __syncwarp();
       const float inv = inv_b / sum;
+#pragma unroll 1
       for (int u = lane; u < out; u += 32) {
         const float yv = l[u];
         float gv = expf(yv - m) * inv;
         if (u == c) gv -= inv_b;
-        if (a.actO != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(a.actO, yv);
+        if (a.actO != VCNN_ACT_IDENTITY) gv *= actg(a.actO, yv);
         l[u] = gv;
       }
     }
   } else {
     const float scale = 2.0f / (float)(B * out);
     float mine = 0.f;
+#pragma unroll 1
     for (int t = tid; t < nr * out; t += nt) {
       const float yv = g5[t], dd = yv - tg[t];
       mine += dd * dd;
       float gv = scale * dd;
-      if (a.actO != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(a.actO, yv);
+      if (a.actO != VCNN_ACT_IDENTITY) gv *= actg(a.actO, yv);
       g5[t] = gv;
     }
 #pragma unroll
@@ -366,28 +375,34 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   __syncthreads();
   if (tid == 0) {
     float v = 0.f;
+#pragma unroll 1
     for (int w = 0; w < nwarps; ++w) v += rowloss[w];
     *cluster.map_shared_rank(lossp + rank, 0) = v;
   }
   HPHASE(12);
   // dW_O | db_O partials over my rows, pushed to the slice owner's slot [rank]
+#pragma unroll 1
   for (int t = tid; t < out * lh; t += nt) {
     const int o = t / lh, i = t - o * lh;
     float acc = 0.f;
     if (i < h)
+#pragma unroll 1
       for (int b = 0; b < nr; ++b) acc += g5[b * out + o] * hs[b * lh + i];
     else
+#pragma unroll 1
       for (int b = 0; b < nr; ++b) acc += g5[b * out + o];
     const int c = t / d.per5;
     *cluster.map_shared_rank(p5 + rank * d.per5 + (t - c * d.per5), c) = acc;
   }
   // gH rows = (gO W_O) * act_H'(h), zero padded to Hp
+#pragma unroll 1
   for (int t = tid; t < d.R * d.Hp; t += nt) {
     const int b = t / d.Hp, i = t - b * d.Hp;
     float acc = 0.f;
     if (b < nr && i < h) {
+#pragma unroll 1
       for (int o = 0; o < out; ++o) acc += g5[b * out + o] * W5[o * lh + i];
-      if (a.actH != VCNN_ACT_IDENTITY) acc *= act_grad_from_out(a.actH, hs[b * lh + i]);
+      if (a.actH != VCNN_ACT_IDENTITY) acc *= actg(a.actH, hs[b * lh + i]);
     }
     gl[b * sH + i] = acc;
   }
@@ -396,6 +411,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   // push my gH rows into every CTA's G (float4)
   {
     const int q = d.Hp >> 2, n = nr * q * kC;
+#pragma unroll 1
     for (int t = tid; t < n; t += nt) {
       const int c = t / (nr * q), u = t - c * (nr * q), b = u / q, k = 4 * (u - b * q);
       *reinterpret_cast<float4*>(cluster.map_shared_rank(G, c) + (r0 + b) * sH + k) =
@@ -408,11 +424,13 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   HPHASE(6);
   // my rows' layer outputs and gradients (stored after the exchange: the
   // cluster barrier's release would otherwise wait for them)
+#pragma unroll 1
   for (int e = tid; e < nr * h; e += nt) {
     const int b = e / h, o = e - b * h;
     a.yH[(size_t)r0 * h + e] = hs[b * lh + o];
     a.gH[(size_t)r0 * h + e] = gl[b * sH + o];
   }
+#pragma unroll 1
   for (int e = tid; e < nr * out; e += nt) {
     a.yO[(size_t)r0 * out + e] = y5[e];
     a.gO[(size_t)r0 * out + e] = g5[e];
@@ -422,6 +440,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   {
     const int np = out * lh, e0 = rank * d.per5;
     const int e1 = e0 + d.per5 < np ? e0 + d.per5 : np;
+#pragma unroll 1
     for (int e = e0 + tid; e < e1; e += nt) {
       float acc = 0.f;
 #pragma unroll
@@ -433,12 +452,15 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   }
   if (rank == 0 && tid == 0 && a.loss) {
     float v = 0.f;
+#pragma unroll 1
     for (int c = 0; c < kC; ++c) v += lossp[c];
     *a.loss = a.loss_kind == VCNN_LOSS_SOFTMAX_CE ? v / (float)B : v / (float)(B * out);
   }
   if (rank == 0)
+#pragma unroll 1
     for (int o = tid; o < h; o += nt) {
       float acc = 0.f;
+#pragma unroll 1
       for (int b = 0; b < B; ++b) acc += G[b * sH + o];
       a.dbH[o] = acc;
     }
@@ -490,7 +512,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
               if (j < nv && col < nc) {
                 float v = c[j][2 * hf + e];
                 if (a.act_prev != VCNN_ACT_IDENTITY)
-                  v *= act_grad_from_out(a.act_prev, xr[b * sK + col]);
+                  v *= actg(a.act_prev, xr[b * sK + col]);
                 a.dx[(size_t)b * in + k0 + col] = v;
               }
             }
