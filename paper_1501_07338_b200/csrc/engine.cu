@@ -393,6 +393,9 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
         if (dense)
           TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
                                 wsw, sw));
+        else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_ok(d, gs) &&
+                 wsw.bytes >= direct::wgrad_workspace(d))
+          TRY(direct::conv_wgrad(d, in, gs, gW, gB, wsw, sw));
         else if (fpool)
           TRY(tc::slab_conv_wgrad(d, in, gs, gW, gB, wsw, sw));
         else
@@ -735,8 +738,11 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
     // net may run -- the split plan depends on the batch
     for (int B = 1; B <= max_batch; ++B) {
       size_t need = 0;
-      if (l.spec.kind == VCNN_LAYER_CONV)
+      if (l.spec.kind == VCNN_LAYER_CONV) {
         need = conv_workspace(conv_of(l, B), VCNN_PREC_TF32);
+        const size_t dw = direct::wgrad_workspace(conv_of(l, B));
+        if (dw > need) need = dw;
+      }
       else if (l.spec.kind == VCNN_LAYER_FULL)
         need = full_workspace(B, (int)l.in_per, l.spec.units, VCNN_PREC_TF32);
       if (need > wsb) wsb = need;

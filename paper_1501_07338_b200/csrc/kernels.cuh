@@ -179,6 +179,13 @@ struct PackSpec {
 };
 int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st);
+// weight gradient as shifted-view GEMMs (wgrad.cu): dW [K][C][kh][kw] and db
+// [K] (nullable) from x and the (possibly pool-routed) gradient; per-image
+// partials in ws, fixed-order reduce
+bool wgrad_ok(const ConvDesc& d, const GradSrc& gs);
+size_t wgrad_workspace(const ConvDesc& d);
+int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
+               const Workspace& ws, cudaStream_t st);
 }  // namespace direct
 
 // ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----

@@ -1,0 +1,365 @@
+// wgrad.cu -- stride-1 convolution weight gradient as shifted-view GEMMs on
+// the sm_100a tensor cores (tcgen05, TF32): conv_backward_core dW / db
+// (layers.hpp:164-178: dW = G^T * im2col(x), db = column sums of G).
+//
+// For a kernel offset (ky,kx) the weight gradient is a GEMM over output
+// positions q of one image's super-grid (row width Wg = W):
+//     dW[n][c][ky][kx] = sum_q G[n][q] * x[c][q + d],   d = ky*W + kx.
+// The reduction runs along positions, so the shift lands on the GEMM K axis,
+// where a K-major operand moves in 16-byte (4-position) granules only.  The
+// CTA therefore stages S = 128/Cp copies of the image, copy j shifted by j
+// positions, stacked as the M = 128 rows (j, c) of the A operand:
+//     A[(j,c)][q] = x[c][q + 4a + j]
+// so ONE MMA at granule offset a yields dW for the S consecutive shifts
+// d = 4a .. 4a+S-1 of all channels.  Per kernel row ky the kw shifts
+// ky*W .. ky*W+kw-1 need ceil(.../S) such MMA groups; each group has its own
+// TMEM accumulator (M=128 x N=K maps).  B = G staged [granule][n][4].
+// Layouts are K-major, no swizzle: element (row, k) at
+// (k/4)*rows*16 + row*16 + (k%4)*4 (SBO = 128 B, LBO = rows*16 B), so the
+// shift is +a*LBO on the descriptor start and a K step of 8 positions is
+// +2*LBO.  One CTA per image; its dW|db partial (the reference layout) goes
+// to the workspace and a fixed-order reduce over images writes dW / db
+// (deterministic).  The routed pool backward (GradSrc.pool) scatters dP to
+// the argmax positions while G is staged.
+#include "kernels.cuh"
+#include "tc_ptx.cuh"
+
+namespace vcnn_b200 {
+namespace direct {
+
+namespace {
+
+constexpr int WT = 256;                 // threads
+constexpr size_t kSmemMax = 227 * 1024;
+constexpr int kMaxGroups = 32;
+
+struct WGeo {
+  int B, C, H, W, K, kh, kw, OH, OW;
+  int Cp, S;          // channels per copy (8/16/32), copies (128 / Cp)
+  int Kn;             // N = maps padded to 16
+  int Q, ksteps;      // positions per image (multiple of 8), K steps of 8
+  int amax, NG;       // max granule offset, staged A granules
+  int ngroups;        // MMA groups (shift sets)
+  int gky[kMaxGroups], ga[kMaxGroups];
+  int tmem_cols;      // power of 2 >= ngroups * Kn
+  int off_a, off_g, off_raw, off_win, smem;   // bytes
+  int raw_n, wsz;     // floats: image, routed windows (K*POH*POW)
+  int64_t part;       // floats per image partial: K*C*kh*kw + K
+  int64_t pstride;    // partial stride (multiple of 4: float4 stores)
+};
+
+bool wplan(const ConvDesc& d, const GradSrc& gs, WGeo& g) {
+  g = WGeo{};
+  if (d.s != 1 || d.C < 1 || d.C > 32 || d.K < 1 || d.K > 256) return false;
+  g.B = d.B, g.C = d.C, g.H = d.H, g.W = d.W, g.K = d.K, g.kh = d.kh, g.kw = d.kw;
+  g.OH = d.OH, g.OW = d.OW;
+  g.Cp = d.C <= 8 ? 8 : d.C <= 16 ? 16 : 32;
+  g.S = 128 / g.Cp;
+  g.Kn = (d.K + 15) / 16 * 16;
+  g.Q = (d.OH * d.W + 7) / 8 * 8;
+  g.ksteps = g.Q / 8;
+  const int dmax = (d.kh - 1) * d.W + d.kw - 1;
+  g.amax = dmax / 4;
+  g.NG = g.Q / 4 + g.amax;
+  int ng = 0;
+  for (int ky = 0; ky < d.kh; ++ky) {
+    const int lo = ky * d.W, hi = ky * d.W + d.kw - 1;
+    for (int a = lo / 4; 4 * a <= hi; a += g.S / 4) {
+      if (ng == kMaxGroups) return false;
+      g.gky[ng] = ky;
+      g.ga[ng] = a;
+      ++ng;
+    }
+  }
+  g.ngroups = ng;
+  int cols = 32;
+  while (cols < ng * g.Kn) cols *= 2;
+  if (cols > 512) return false;
+  g.tmem_cols = cols;
+  g.raw_n = d.C * d.H * d.W;
+  if (g.raw_n % 4) return false;
+  g.wsz = gs.pool ? d.K * gs.POH * gs.POW : 0;
+  if (gs.pool && g.wsz % 4) return false;
+  if (!gs.pool && (d.K * d.OH * d.OW) % 4) return false;
+  g.part = (int64_t)d.K * d.C * d.kh * d.kw + d.K;
+  g.pstride = (g.part + 3) / 4 * 4;
+  // A: NG granules x 128 rows x 16 B (reused for the dW tile in the
+  // epilogue); G: Q/4 granules x Kn rows x 16 B; the image; routed windows
+  // (or the plain gradient image)
+  const int a_bytes = g.NG * 128 * 16;
+  const int dw_bytes = (int)(4 * (g.part - d.K));
+  g.off_a = 0;
+  g.off_g = ((a_bytes > dw_bytes ? a_bytes : dw_bytes) + 127) & ~127;
+  g.off_raw = g.off_g + g.Q / 4 * g.Kn * 16;
+  const int gin = gs.pool ? 2 * g.wsz : d.K * d.OH * d.OW;
+  g.off_win = g.off_raw + 4 * g.raw_n;
+  g.smem = g.off_win + 4 * gin + 1024;
+  return (size_t)g.smem + 512 <= kSmemMax;
+}
+
+struct WArgs {
+  WGeo g;
+  const float* x;       // [B][C][H][W]
+  GradSrc gs;           // routed (pool) or plain g [B][K][OH][OW]
+  float* part;          // [B][part]
+};
+
+__global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
+  pdl_launch_dependents();
+  const WGeo& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  __shared__ uint64_t load_bar, done_bar;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.x;
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t s_a = sbase + g.off_a, s_g = sbase + g.off_g, s_raw = sbase + g.off_raw,
+                 s_win = sbase + g.off_win;
+  const bool routed = a.gs.pool != 0;
+  const int ohw = g.OH * g.OW;
+
+  if (warp == 0) {
+    ptx::tmem_alloc(&tmem_base_sh, g.tmem_cols);
+    ptx::tmem_relinquish();
+  }
+  pdl_wait();
+  if (tid == 0) {
+    ptx::mbar_init(&load_bar, 1);
+    ptx::mbar_init(&done_bar, 1);
+    ptx::fence_mbar_init();
+    const uint32_t rb = 4u * (uint32_t)g.raw_n;
+    uint32_t gb;
+    ptx::mbar_expect_tx(&load_bar, rb);
+    ptx::bulk_g2s(s_raw, a.x + (int64_t)b * g.raw_n, rb, &load_bar);
+    if (routed) {
+      gb = 4u * (uint32_t)g.wsz;
+      ptx::mbar_expect_tx(&load_bar, 2 * gb);
+      ptx::bulk_g2s(s_win, a.gs.dP + (int64_t)b * g.wsz, gb, &load_bar);
+      ptx::bulk_g2s(s_win + gb, a.gs.parg + (int64_t)b * g.wsz, gb, &load_bar);
+    } else {
+      gb = 4u * (uint32_t)(g.K * ohw);
+      ptx::mbar_expect_tx(&load_bar, gb);
+      ptx::bulk_g2s(s_win, a.gs.g + (int64_t)b * g.K * ohw, gb, &load_bar);
+    }
+    ptx::mbar_arrive(&load_bar);
+  }
+  // zero the G operand while the loads land
+  const int g_floats = g.Q * g.Kn;
+  for (int i = tid; i < g_floats / 4; i += WT)
+    ptx::sts_f32x4(s_g + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  ptx::mbar_wait(&load_bar, 0);
+
+  // ---- G[n][q] (q = oy*W + ox) in [granule][n][4], tf32 ----
+  auto g_at = [&](int n, int q) -> uint32_t {
+    return s_g + 4u * (uint32_t)(((q >> 2) * g.Kn + n) * 4 + (q & 3));
+  };
+  if (routed) {
+    const int base = (int)((int64_t)b * g.K * ohw);
+    for (int i = tid; i < g.wsz; i += WT) {
+      const int at = ptx::lds_s32(s_win + 4u * (uint32_t)(g.wsz + i)) - base;
+      const int n = at / ohw, r = at - n * ohw, oy = r / g.OW, ox = r - oy * g.OW;
+      ptx::sts_f32(g_at(n, oy * g.W + ox), ptx::to_tf32(ptx::lds_f32(s_win + 4u * i)));
+    }
+  } else {
+    for (int i = tid; i < g.K * ohw; i += WT) {
+      const int n = i / ohw, r = i - n * ohw, oy = r / g.OW, ox = r - oy * g.OW;
+      ptx::sts_f32(g_at(n, oy * g.W + ox), ptx::to_tf32(ptx::lds_f32(s_win + 4u * i)));
+    }
+  }
+  // ---- A: S shifted copies of the image, rows (j, c), [granule][row][4] ----
+  if ((g.H * g.W) % 4 == 0) {
+    // thread -> (granule, channel): the S+3 positions from 4*gr are read as
+    // aligned float4s once and written as the S copies' granule entries
+    const int hw = g.H * g.W, nq = (g.S + 3 + 3) / 4;  // float4s per item
+    for (int i = tid; i < g.NG * g.Cp; i += WT) {
+      const int gr = i / g.Cp, c = i - gr * g.Cp;
+      float v[20];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        if (u < nq) {
+          const int p = 4 * gr + 4 * u;
+          float4 f = (c < g.C && p < hw) ? ptx::lds_f32x4(s_raw + 4u * (uint32_t)(c * hw + p))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[4 * u] = ptx::to_tf32(f.x);
+          v[4 * u + 1] = ptx::to_tf32(f.y);
+          v[4 * u + 2] = ptx::to_tf32(f.z);
+          v[4 * u + 3] = ptx::to_tf32(f.w);
+        }
+      }
+      const uint32_t dst = s_a + 16u * (uint32_t)(gr * 128 + c);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < g.S)
+          ptx::sts_f32x4(dst + 16u * (uint32_t)(j * g.Cp),
+                         make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+    }
+  } else {
+    const int hw = g.H * g.W;
+    for (int i = tid; i < g.NG * 128; i += WT) {
+      const int gr = i >> 7, row = i & 127;
+      const int j = row / g.Cp, c = row - j * g.Cp;
+      const int p0 = 4 * gr + j;
+      float v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int p = p0 + t;
+        v[t] = (c < g.C && p < hw) ? ptx::to_tf32(ptx::lds_f32(s_raw + 4u * (c * hw + p))) : 0.f;
+      }
+      ptx::sts_f32x4(s_a + 16u * i, make_float4(v[0], v[1], v[2], v[3]));
+    }
+  }
+  ptx::fence_proxy_async_smem();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+
+  // ---- one elected lane of warp 0 issues ksteps x ngroups MMAs ----
+  if (warp == 0) {
+    if (ptx::elect_one()) {
+      const uint32_t idesc = ptx::idesc_tf32(128, g.Kn);
+      const uint32_t lbo_a = 128u * 16u, lbo_g = (uint32_t)g.Kn * 16u;
+      const uint64_t a0 = ptx::interleave_desc(s_a, lbo_a, 128u);
+      const uint64_t g0 = ptx::interleave_desc(s_g, lbo_g, 128u);
+      for (int k = 0; k < g.ksteps; ++k) {
+        const uint64_t bd = g0 + (uint64_t)(2u * k * lbo_g >> 4);
+        for (int m = 0; m < g.ngroups; ++m) {
+          const uint64_t ad = a0 + (uint64_t)((2u * k + (uint32_t)g.ga[m]) * lbo_a >> 4);
+          ptx::mma_tf32(tmem + (uint32_t)(m * g.Kn), ad, bd, idesc, k > 0 ? 1u : 0u);
+        }
+      }
+      ptx::mma_commit(&done_bar);
+    }
+    __syncwarp();
+  }
+  // db partial (sum of G over positions, fixed order) while the MMAs run
+  float* part = a.part + (int64_t)b * g.pstride;
+  const int64_t nw = g.part - g.K;
+  for (int n = tid; n < g.K; n += WT) {
+    float acc = 0.f;
+    for (int q = 0; q < g.Q; ++q) acc += ptx::lds_f32(g_at(n, q));
+    part[nw + n] = acc;
+  }
+  ptx::mbar_wait(&done_bar, 0);
+  ptx::tc_fence_after();
+
+  // ---- epilogue: TMEM rows (j, c) x cols n -> dW tile [n][c][ky][kx] in
+  //      shared memory (over A, dead now), then coalesced stores ----
+  const uint32_t s_dw = s_a;
+  const int khw = g.kh * g.kw, ckk = g.C * khw;
+  {  // warps w and w+4 share TMEM lanes 32*(w%4)..; they split the groups
+    const int row = (warp & 3) * 32 + lane, j = row / g.Cp, c = row - j * g.Cp;
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    for (int m = warp >> 2; m < g.ngroups; m += 2) {
+      const int ky = g.gky[m], kx = 4 * g.ga[m] + j - ky * g.W;
+      const bool ok = c < g.C && kx >= 0 && kx < g.kw;
+      for (int n0 = 0; n0 < g.Kn; n0 += 16) {
+        uint32_t r[16];
+        ptx::tmem_ld16(trow + (uint32_t)(m * g.Kn + n0), r);
+        ptx::tmem_wait_ld();
+        if (ok) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int n = n0 + u;
+            if (n < g.K)
+              ptx::sts_f32(s_dw + 4u * (uint32_t)(n * ckk + c * khw + ky * g.kw + kx),
+                           __uint_as_float(r[u]));
+          }
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  for (int64_t i = tid; i < nw / 4; i += WT)
+    reinterpret_cast<float4*>(part)[i] = ptx::lds_f32x4(s_dw + 16u * (uint32_t)i);
+  for (int64_t i = nw / 4 * 4 + tid; i < nw; i += WT) part[i] = ptx::lds_f32(s_dw + 4u * (uint32_t)i);
+  __syncthreads();
+  if (warp == 0) ptx::tmem_dealloc(tmem, g.tmem_cols);
+}
+
+// out[i] = sum over images of part[b][i] (dW then db) in a fixed order:
+// slice s of the block sums images [s*per_s, (s+1)*per_s) for 32 consecutive
+// outputs (loads coalesced, all in flight), then lane-wise over slices in
+// order.  Deterministic; latency is one round of loads, not nimg.
+constexpr int kRedSlices = 8;
+__global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
+    int nimg, int64_t per, int64_t stride, int64_t nw, const float* __restrict__ part,
+    float* __restrict__ dw, float* __restrict__ db) {
+  PDL_ENTRY();
+  __shared__ float red[kRedSlices][33];
+  const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int64_t i = blockIdx.x * 32ll + lane;
+  const int per_s = (nimg + kRedSlices - 1) / kRedSlices;
+  const int b0 = sl * per_s, b1 = b0 + per_s < nimg ? b0 + per_s : nimg;
+  float acc = 0.f;
+  if (i < per) {
+    const float* p = part + i;
+    int bb = b0;
+    for (; bb + 8 <= b1; bb += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (int64_t)(bb + u) * stride);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    for (; bb < b1; ++bb) acc += __ldg(p + (int64_t)bb * stride);
+  }
+  red[sl][lane] = acc;
+  __syncthreads();
+  if (sl == 0 && i < per) {
+    float t = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < kRedSlices; ++s2) t += red[s2][lane];
+    if (i < nw) dw[i] = t;
+    else if (db) db[i - nw] = t;
+  }
+}
+
+}  // namespace
+
+bool wgrad_ok(const ConvDesc& d, const GradSrc& gs) {
+  WGeo g;
+  return wplan(d, gs, g);
+}
+
+size_t wgrad_workspace(const ConvDesc& d) {
+  WGeo g;
+  GradSrc gs;
+  if (!wplan(d, gs, g)) return 0;
+  return sizeof(float) * (size_t)(g.pstride * d.B);
+}
+
+int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
+               const Workspace& ws, cudaStream_t st) {
+  WArgs a{};
+  if (!wplan(d, gs, a.g)) return fail(VCNN_ESHAPE, "direct wgrad: geometry not supported");
+  const size_t need = sizeof(float) * (size_t)(a.g.pstride * d.B);
+  if (ws.bytes < need) return fail(VCNN_ECONFIG, "direct wgrad: workspace too small");
+  a.x = x;
+  a.gs = gs;
+  a.part = ws.ptr;
+  const size_t smem = (size_t)a.g.smem;
+  static size_t configured = 0;
+  if (smem > configured) {
+    VCNN_CUDA_TRY(cudaFuncSetAttribute(wgrad_shift_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  VCNN_CUDA_TRY(launch_pdl(wgrad_shift_kernel, dim3((unsigned)d.B), dim3(WT), smem, st, a));
+  VCNN_LAUNCHED();
+  const int64_t per = a.g.part, nw = per - d.K;
+  const int64_t blocks = cdiv(per, 32);
+  VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)blocks), dim3(32 * kRedSlices), 0, st, d.B, per,
+                           a.g.pstride, nw, (const float*)ws.ptr, dw, db));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+}  // namespace direct
+}  // namespace vcnn_b200
