@@ -97,6 +97,18 @@ bool wplan(const ConvDesc& d, const GradSrc& gs, WGeo& g) {
   return (size_t)g.smem + 512 <= kSmemMax;
 }
 
+#ifdef VCNN_PHASE_TIMING
+__device__ unsigned long long g_wphase[4][8];
+#define WPHASE(i)                                                             \
+  do {                                                                        \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x < 4) g_wphase[blockIdx.x][i] = clock64(); \
+  } while (0)
+#else
+#define WPHASE(i) \
+  do {            \
+  } while (0)
+#endif
+
 struct WArgs {
   WGeo g;
   const float* x;       // [B][C][H][W]
@@ -119,6 +131,7 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
                  s_win = sbase + g.off_win;
   const bool routed = a.gs.pool != 0;
   const int ohw = g.OH * g.OW;
+  if (tid == 0) WPHASE(0);
 
   if (warp == 0) {
     ptx::tmem_alloc(&tmem_base_sh, g.tmem_cols);
@@ -154,6 +167,7 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   ptx::mbar_wait(&load_bar, 0);
+  if (tid == 0) WPHASE(1);
 
   // ---- G[n][q] (q = oy*W + ox) in [granule][n][4], tf32 ----
   auto g_at = [&](int n, int q) -> uint32_t {
@@ -218,6 +232,7 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  if (tid == 0) WPHASE(2);
 
   // ---- one elected lane of warp 0 issues ksteps x ngroups MMAs ----
   if (warp == 0) {
@@ -226,14 +241,21 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
       const uint32_t lbo_a = 128u * 16u, lbo_g = (uint32_t)g.Kn * 16u;
       const uint64_t a0 = ptx::interleave_desc(s_a, lbo_a, 128u);
       const uint64_t g0 = ptx::interleave_desc(s_g, lbo_g, 128u);
-      for (int k = 0; k < g.ksteps; ++k) {
-        const uint64_t bd = g0 + (uint64_t)(2u * k * lbo_g >> 4);
-        for (int m = 0; m < g.ngroups; ++m) {
-          const uint64_t ad = a0 + (uint64_t)((2u * k + (uint32_t)g.ga[m]) * lbo_a >> 4);
-          ptx::mma_tf32(tmem + (uint32_t)(m * g.Kn), ad, bd, idesc, k > 0 ? 1u : 0u);
+      // group-major: each accumulator's K sequence is a run of additions on
+      // the descriptors (the issue loop is the MMA rate limiter)
+      const uint64_t sa = (uint64_t)(2u * lbo_a >> 4), sg = (uint64_t)(2u * lbo_g >> 4);
+      for (int m = 0; m < g.ngroups; ++m) {
+        uint64_t ad = a0 + (uint64_t)((uint32_t)g.ga[m] * lbo_a >> 4), bd = g0;
+        const uint32_t dt = tmem + (uint32_t)(m * g.Kn);
+        ptx::mma_tf32(dt, ad, bd, idesc, 0u);
+        for (int k = 1; k < g.ksteps; ++k) {
+          ad += sa;
+          bd += sg;
+          ptx::mma_tf32(dt, ad, bd, idesc, 1u);
         }
       }
       ptx::mma_commit(&done_bar);
+      WPHASE(3);
     }
     __syncwarp();
   }
@@ -247,6 +269,7 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
   }
   ptx::mbar_wait(&done_bar, 0);
   ptx::tc_fence_after();
+  if (tid == 0) WPHASE(4);
 
   // ---- epilogue: TMEM rows (j, c) x cols n -> dW tile [n][c][ky][kx] in
   //      shared memory (over A, dead now), then coalesced stores ----
@@ -276,10 +299,12 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (tid == 0) WPHASE(5);
   for (int64_t i = tid; i < nw / 4; i += WT)
     reinterpret_cast<float4*>(part)[i] = ptx::lds_f32x4(s_dw + 16u * (uint32_t)i);
   for (int64_t i = nw / 4 * 4 + tid; i < nw; i += WT) part[i] = ptx::lds_f32(s_dw + 4u * (uint32_t)i);
   __syncthreads();
+  if (tid == 0) WPHASE(6);
   if (warp == 0) ptx::tmem_dealloc(tmem, g.tmem_cols);
 }
 
@@ -363,3 +388,12 @@ int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, 
 
 }  // namespace direct
 }  // namespace vcnn_b200
+
+#ifdef VCNN_PHASE_TIMING
+extern "C" int vcnn_debug_wphases(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_wphase, sizeof(unsigned long long) * 32) ==
+                 cudaSuccess
+             ? 0
+             : 4;
+}
+#endif

@@ -35,3 +35,16 @@ for r in range(16):
           "total", t[9] - t[0])
     print("        head: reduce=%d y=%d loss=%d dWO+gH=%d push=%d" % (
         t[10] - t[4], t[11] - t[10], t[12] - t[11], t[13] - t[12], t[5] - t[13]))
+
+# the shifted-view weight gradient of conv2 (wgrad.cu) in the same step
+try:
+    L.vcnn_debug_wphases.argtypes = [C.c_void_p]
+    wb = (C.c_ulonglong * 32)()
+    L.vcnn_debug_wphases(wb)
+    wn = ["load", "build", "mma-issue", "mma-drain", "tmem->smem", "store"]
+    for r in range(2):
+        t = [wb[r * 8 + i] for i in range(8)]
+        print(f"wgrad cta {r} " + " ".join(f"{n}={t[i + 1] - t[i]}" for i, n in enumerate(wn)),
+              "total", t[6] - t[0])
+except AttributeError:
+    pass

@@ -5,7 +5,8 @@
 #include "../../paper_1501_07338_b200/csrc/tc_ptx.cuh"
 using namespace vcnn_b200;
 
-template <int N, int UNROLL, int STEP, int BSTEP = 0, int TC = 256, int LBOA = 4096>
+template <int N, int UNROLL, int STEP, int BSTEP = 0, int TC = 256, int LBOA = 4096,
+          int LBOB = 128, int SBOB = 256, int NACC = 1>
 __global__ void rate(unsigned long long* out, int batches) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar;
@@ -22,14 +23,14 @@ __global__ void rate(unsigned long long* out, int batches) {
   if (threadIdx.x < 32) {
     const uint32_t a = ptx::smem_u32(s);
     const uint64_t ad0 = ptx::interleave_desc(a, LBOA, 128);
-    const uint64_t bd0 = ptx::interleave_desc(a + 32768, 128, 256);
+    const uint64_t bd0 = ptx::interleave_desc(a + 32768, LBOB, SBOB);
     const uint32_t id = ptx::idesc_tf32(128, N);
     unsigned long long t0 = clock64();
     if (ptx::elect_one()) {
       for (int bt = 0; bt < batches; ++bt) {
 #pragma unroll
         for (int i = 0; i < UNROLL; ++i)
-          ptx::mma_tf32(tm, ad0 + (uint64_t)((i * STEP) & 63), bd0 + (uint64_t)(BSTEP ? (i * BSTEP) & 1023 : (i >> 3) * 2), id, (bt | i) != 0);
+          ptx::mma_tf32(tm + (uint32_t)((i % NACC) * N), ad0 + (uint64_t)((i * STEP) & 63), bd0 + (uint64_t)(BSTEP ? (i * BSTEP) & 1023 : (i >> 3) * 2), id, (bt | i) != 0);
       }
       ptx::mma_commit(&bar);
     }
@@ -56,6 +57,11 @@ int main() {
            batches * per, h[0], h[1], (double)h[1] / (batches * per), cudaGetErrorString(e));
     fflush(stdout);
   };
+  // the wgrad kernel's operands: A lbo 2048 / sbo 128, B lbo 512 / sbo 128,
+  // 10 accumulators, A advancing by granules
+  run(rate<32, 16, 1, 64, 512, 2048, 512, 128, 10>, "wgrad-like g1", 32, 16, 1);
+  run(rate<32, 16, 1, 64, 512, 2048, 512, 128, 10>, "wgrad-like g128", 32, 16, 128);
+  run(rate<32, 16, 1, 64, 512, 2048, 512, 128, 1>, "wgrad-like 1acc", 32, 16, 1);
   run(rate<32, 16, 1, 64, 32, 3072>, "N=32 tc32 l3072 g148", 32, 16, 148);
   run(rate<32, 16, 1, 64, 32, 3072>, "N=32 tc32 l3072 g1", 32, 16, 1);
   run(rate<32, 16, 1, 64, 256, 3072>, "N=32 tc256 l3072", 32, 16, 1);
