@@ -37,11 +37,13 @@ struct WGeo {
   int B, C, H, W, K, kh, kw, OH, OW;
   int Cp, S;          // channels per copy (8/16/32), copies (128 / Cp)
   int Kn;             // N = maps padded to 16
-  int Q, ksteps;      // positions per image (multiple of 8), K steps of 8
-  int amax, NG;       // max granule offset, staged A granules
+  int Rc, nchunk;     // output rows per position chunk, chunks per image
+  int Q, ksteps;      // positions per chunk (Rc*W padded to 8), K steps of 8
+  int amax, NG;       // max granule offset, staged A granules per chunk
   int ngroups;        // MMA groups (shift sets)
   int gky[kMaxGroups], ga[kMaxGroups];
   int tmem_cols;      // power of 2 >= ngroups * Kn
+  int pool, POH, POW; // routed gradient (pool > 0)
   int off_a, off_g, off_raw, off_win, smem;   // bytes
   int raw_n, wsz;     // floats: image, routed windows (K*POH*POW)
   int64_t part;       // floats per image partial: K*C*kh*kw + K
@@ -56,11 +58,8 @@ bool wplan(const ConvDesc& d, const GradSrc& gs, WGeo& g) {
   g.Cp = d.C <= 8 ? 8 : d.C <= 16 ? 16 : 32;
   g.S = 128 / g.Cp;
   g.Kn = (d.K + 15) / 16 * 16;
-  g.Q = (d.OH * d.W + 7) / 8 * 8;
-  g.ksteps = g.Q / 8;
   const int dmax = (d.kh - 1) * d.W + d.kw - 1;
   g.amax = dmax / 4;
-  g.NG = g.Q / 4 + g.amax;
   int ng = 0;
   for (int ky = 0; ky < d.kh; ++ky) {
     const int lo = ky * d.W, hi = ky * d.W + d.kw - 1;
@@ -78,23 +77,40 @@ bool wplan(const ConvDesc& d, const GradSrc& gs, WGeo& g) {
   g.tmem_cols = cols;
   g.raw_n = d.C * d.H * d.W;
   if (g.raw_n % 4) return false;
+  g.pool = gs.pool, g.POH = gs.POH, g.POW = gs.POW;
   g.wsz = gs.pool ? d.K * gs.POH * gs.POW : 0;
   if (gs.pool && g.wsz % 4) return false;
-  if (!gs.pool && (d.K * d.OH * d.OW) % 4) return false;
+  // window scratch is reserved for any >= 2x2 pool whether or not this call
+  // is routed, so a routed layer and its unrouted trace twin get the same
+  // plan (bit-identical results)
+  const int win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
+  if (g.wsz > win_n) return false;
   g.part = (int64_t)d.K * d.C * d.kh * d.kw + d.K;
   g.pstride = (g.part + 3) / 4 * 4;
-  // A: NG granules x 128 rows x 16 B (reused for the dW tile in the
-  // epilogue); G: Q/4 granules x Kn rows x 16 B; the image; routed windows
-  // (or the plain gradient image)
-  const int a_bytes = g.NG * 128 * 16;
-  const int dw_bytes = (int)(4 * (g.part - d.K));
-  g.off_a = 0;
-  g.off_g = ((a_bytes > dw_bytes ? a_bytes : dw_bytes) + 127) & ~127;
-  g.off_raw = g.off_g + g.Q / 4 * g.Kn * 16;
-  const int gin = gs.pool ? 2 * g.wsz : d.K * d.OH * d.OW;
-  g.off_win = g.off_raw + 4 * g.raw_n;
-  g.smem = g.off_win + 4 * gin + 1024;
-  return (size_t)g.smem + 512 <= kSmemMax;
+  // per chunk: A = NG granules x 128 rows x 16 B (the dW tile reuses it at
+  // the end), G = Q/4 granules x Kn rows x 16 B; per image: the input image
+  // and the routed windows.  The largest chunk that fits; chunk starts must
+  // be granule aligned (Rc*W % 4 == 0) and whole pool rows.
+  const int dw_bytes = (int)(4 * g.part);
+  // (one chunk only for now: with a single A buffer, chunked images
+  // serialise build and MMA and lose to the slab kernel -- conv1 of CIFAR-3
+  // measured 47 us vs 34 us)
+  for (int Rc = d.OH; Rc >= d.OH; --Rc) {
+    const int nch = (d.OH + Rc - 1) / Rc;
+    if (nch > 1 && ((Rc * d.W) % 4 || (gs.pool && Rc % gs.pool))) continue;
+    const int Q = (Rc * d.W + 7) / 8 * 8;
+    const int NG = Q / 4 + g.amax;
+    const int a_bytes = NG * 128 * 16;
+    const int off_g = ((a_bytes > dw_bytes ? a_bytes : dw_bytes) + 127) & ~127;
+    const int off_raw = off_g + Q / 4 * g.Kn * 16;
+    const int off_win = off_raw + 4 * g.raw_n;
+    const int smem = off_win + 4 * 2 * win_n + 1024;
+    if ((size_t)smem + 512 > kSmemMax) continue;
+    g.Rc = Rc, g.nchunk = nch, g.Q = Q, g.ksteps = Q / 8, g.NG = NG;
+    g.off_a = 0, g.off_g = off_g, g.off_raw = off_raw, g.off_win = off_win, g.smem = smem;
+    return true;
+  }
+  return false;
 }
 
 #ifdef VCNN_PHASE_TIMING
@@ -142,26 +158,19 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
     ptx::mbar_init(&load_bar, 1);
     ptx::mbar_init(&done_bar, 1);
     ptx::fence_mbar_init();
+    // the image and (routed) the pooled windows; a plain gradient is read
+    // chunk by chunk from global memory
     const uint32_t rb = 4u * (uint32_t)g.raw_n;
-    uint32_t gb;
     ptx::mbar_expect_tx(&load_bar, rb);
     ptx::bulk_g2s(s_raw, a.x + (int64_t)b * g.raw_n, rb, &load_bar);
     if (routed) {
-      gb = 4u * (uint32_t)g.wsz;
+      const uint32_t gb = 4u * (uint32_t)g.wsz;
       ptx::mbar_expect_tx(&load_bar, 2 * gb);
       ptx::bulk_g2s(s_win, a.gs.dP + (int64_t)b * g.wsz, gb, &load_bar);
       ptx::bulk_g2s(s_win + gb, a.gs.parg + (int64_t)b * g.wsz, gb, &load_bar);
-    } else {
-      gb = 4u * (uint32_t)(g.K * ohw);
-      ptx::mbar_expect_tx(&load_bar, gb);
-      ptx::bulk_g2s(s_win, a.gs.g + (int64_t)b * g.K * ohw, gb, &load_bar);
     }
     ptx::mbar_arrive(&load_bar);
   }
-  // zero the G operand while the loads land
-  const int g_floats = g.Q * g.Kn;
-  for (int i = tid; i < g_floats / 4; i += WT)
-    ptx::sts_f32x4(s_g + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -169,105 +178,124 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
   ptx::mbar_wait(&load_bar, 0);
   if (tid == 0) WPHASE(1);
 
-  // ---- G[n][q] (q = oy*W + ox) in [granule][n][4], tf32 ----
-  auto g_at = [&](int n, int q) -> uint32_t {
+  auto g_at = [&](int n, int q) -> uint32_t {  // G[n][q] in [granule][n][4]
     return s_g + 4u * (uint32_t)(((q >> 2) * g.Kn + n) * 4 + (q & 3));
   };
-  if (routed) {
-    const int base = (int)((int64_t)b * g.K * ohw);
-    for (int i = tid; i < g.wsz; i += WT) {
-      const int at = ptx::lds_s32(s_win + 4u * (uint32_t)(g.wsz + i)) - base;
-      const int n = at / ohw, r = at - n * ohw, oy = r / g.OW, ox = r - oy * g.OW;
-      ptx::sts_f32(g_at(n, oy * g.W + ox), ptx::to_tf32(ptx::lds_f32(s_win + 4u * i)));
+  const int hw = g.H * g.W;
+  float db_acc = 0.f;  // thread n < K: this image's bias gradient, chunk by chunk
+  for (int ch = 0; ch < g.nchunk; ++ch) {
+    const int r0 = ch * g.Rc, nrows = r0 + g.Rc <= g.OH ? g.Rc : g.OH - r0;
+    if (ch > 0) {  // the previous chunk's MMAs have read A and G
+      ptx::mbar_wait(&done_bar, (uint32_t)((ch - 1) & 1));
+      ptx::tc_fence_after();
+      __syncthreads();
     }
-  } else {
-    for (int i = tid; i < g.K * ohw; i += WT) {
-      const int n = i / ohw, r = i - n * ohw, oy = r / g.OW, ox = r - oy * g.OW;
-      ptx::sts_f32(g_at(n, oy * g.W + ox), ptx::to_tf32(ptx::lds_f32(s_win + 4u * i)));
+    // ---- G[n][q] (q = (oy - r0)*W + ox) for this chunk, tf32 ----
+    for (int i = tid; i < g.Q * g.Kn / 4; i += WT)
+      ptx::sts_f32x4(s_g + 16u * i, make_float4(0.f, 0.f, 0.f, 0.f));
+    __syncthreads();
+    if (routed) {  // the windows of this chunk's pooled rows, dP at the argmax
+      const int base = (int)((int64_t)b * g.K * ohw);
+      const int prs = r0 / g.pool;
+      int npr = (nrows + g.pool - 1) / g.pool;
+      if (prs + npr > g.POH) npr = g.POH - prs;
+      const int per_n = npr * g.POW;
+      for (int i = tid; i < g.K * per_n; i += WT) {
+        const int n = i / per_n, r = i - n * per_n;
+        const int w = n * g.POH * g.POW + prs * g.POW + r;
+        const int at = ptx::lds_s32(s_win + 4u * (uint32_t)(g.wsz + w)) - base;
+        const int rr = at - n * ohw, oy = rr / g.OW, ox = rr - oy * g.OW;
+        ptx::sts_f32(g_at(n, (oy - r0) * g.W + ox), ptx::to_tf32(ptx::lds_f32(s_win + 4u * w)));
+      }
+    } else {
+      const int per_n = nrows * g.OW;
+      const float* gsrc = a.gs.g + (int64_t)b * g.K * ohw + (int64_t)r0 * g.OW;
+      for (int i = tid; i < g.K * per_n; i += WT) {
+        const int n = i / per_n, r = i - n * per_n, oy = r / g.OW, ox = r - oy * g.OW;
+        ptx::sts_f32(g_at(n, oy * g.W + ox), ptx::to_tf32(__ldg(gsrc + (int64_t)n * ohw + r)));
+      }
     }
-  }
-  // ---- A: S shifted copies of the image, rows (j, c), [granule][row][4] ----
-  if ((g.H * g.W) % 4 == 0) {
-    // thread -> (granule, channel): the S+3 positions from 4*gr are read as
-    // aligned float4s once and written as the S copies' granule entries
-    const int hw = g.H * g.W, nq = (g.S + 3 + 3) / 4;  // float4s per item
-    for (int i = tid; i < g.NG * g.Cp; i += WT) {
-      const int gr = i / g.Cp, c = i - gr * g.Cp;
-      float v[20];
+    // ---- A: S shifted copies of the image from position r0*W, rows (j, c) ----
+    const int pbase = r0 * g.W;
+    if (hw % 4 == 0) {
+      // thread -> (granule, channel): the S+3 positions from 4*gr are read as
+      // aligned float4s once and written as the S copies' granule entries
+      const int nq = (g.S + 6) / 4;  // float4s per item
+      for (int i = tid; i < g.NG * g.Cp; i += WT) {
+        const int gr = i / g.Cp, c = i - gr * g.Cp;
+        float v[20];
 #pragma unroll
-      for (int u = 0; u < 5; ++u) {
-        if (u < nq) {
-          const int p = 4 * gr + 4 * u;
-          float4 f = (c < g.C && p < hw) ? ptx::lds_f32x4(s_raw + 4u * (uint32_t)(c * hw + p))
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
-          v[4 * u] = ptx::to_tf32(f.x);
-          v[4 * u + 1] = ptx::to_tf32(f.y);
-          v[4 * u + 2] = ptx::to_tf32(f.z);
-          v[4 * u + 3] = ptx::to_tf32(f.w);
+        for (int u = 0; u < 5; ++u) {
+          if (u < nq) {
+            const int p = pbase + 4 * gr + 4 * u;
+            float4 f = (c < g.C && p < hw) ? ptx::lds_f32x4(s_raw + 4u * (uint32_t)(c * hw + p))
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[4 * u] = ptx::to_tf32(f.x);
+            v[4 * u + 1] = ptx::to_tf32(f.y);
+            v[4 * u + 2] = ptx::to_tf32(f.z);
+            v[4 * u + 3] = ptx::to_tf32(f.w);
+          }
         }
-      }
-      const uint32_t dst = s_a + 16u * (uint32_t)(gr * 128 + c);
+        const uint32_t dst = s_a + 16u * (uint32_t)(gr * 128 + c);
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < g.S)
-          ptx::sts_f32x4(dst + 16u * (uint32_t)(j * g.Cp),
-                         make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
-    }
-  } else {
-    const int hw = g.H * g.W;
-    for (int i = tid; i < g.NG * 128; i += WT) {
-      const int gr = i >> 7, row = i & 127;
-      const int j = row / g.Cp, c = row - j * g.Cp;
-      const int p0 = 4 * gr + j;
-      float v[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int p = p0 + t;
-        v[t] = (c < g.C && p < hw) ? ptx::to_tf32(ptx::lds_f32(s_raw + 4u * (c * hw + p))) : 0.f;
+        for (int j = 0; j < 16; ++j)
+          if (j < g.S)
+            ptx::sts_f32x4(dst + 16u * (uint32_t)(j * g.Cp),
+                           make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
       }
-      ptx::sts_f32x4(s_a + 16u * i, make_float4(v[0], v[1], v[2], v[3]));
+    } else {
+      for (int i = tid; i < g.NG * 128; i += WT) {
+        const int gr = i >> 7, row = i & 127;
+        const int j = row / g.Cp, c = row - j * g.Cp;
+        const int p0 = pbase + 4 * gr + j;
+        float v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int p = p0 + t;
+          v[t] = (c < g.C && p < hw) ? ptx::to_tf32(ptx::lds_f32(s_raw + 4u * (c * hw + p))) : 0.f;
+        }
+        ptx::sts_f32x4(s_a + 16u * i, make_float4(v[0], v[1], v[2], v[3]));
+      }
     }
-  }
-  ptx::fence_proxy_async_smem();
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  if (tid == 0) WPHASE(2);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (tid == 0 && ch == 0) WPHASE(2);
 
-  // ---- one elected lane of warp 0 issues ksteps x ngroups MMAs ----
-  if (warp == 0) {
-    if (ptx::elect_one()) {
-      const uint32_t idesc = ptx::idesc_tf32(128, g.Kn);
-      const uint32_t lbo_a = 128u * 16u, lbo_g = (uint32_t)g.Kn * 16u;
-      const uint64_t a0 = ptx::interleave_desc(s_a, lbo_a, 128u);
-      const uint64_t g0 = ptx::interleave_desc(s_g, lbo_g, 128u);
-      // group-major: each accumulator's K sequence is a run of additions on
-      // the descriptors (the issue loop is the MMA rate limiter)
-      const uint64_t sa = (uint64_t)(2u * lbo_a >> 4), sg = (uint64_t)(2u * lbo_g >> 4);
-      for (int m = 0; m < g.ngroups; ++m) {
-        uint64_t ad = a0 + (uint64_t)((uint32_t)g.ga[m] * lbo_a >> 4), bd = g0;
-        const uint32_t dt = tmem + (uint32_t)(m * g.Kn);
-        ptx::mma_tf32(dt, ad, bd, idesc, 0u);
-        for (int k = 1; k < g.ksteps; ++k) {
-          ad += sa;
-          bd += sg;
-          ptx::mma_tf32(dt, ad, bd, idesc, 1u);
+    // ---- one elected lane of warp 0 issues ngroups x ksteps MMAs ----
+    if (warp == 0) {
+      if (ptx::elect_one()) {
+        const uint32_t idesc = ptx::idesc_tf32(128, g.Kn);
+        const uint32_t lbo_a = 128u * 16u, lbo_g = (uint32_t)g.Kn * 16u;
+        const uint64_t a0 = ptx::interleave_desc(s_a, lbo_a, 128u);
+        const uint64_t g0 = ptx::interleave_desc(s_g, lbo_g, 128u);
+        // group-major: each accumulator's K sequence is a run of additions
+        // on the descriptors (the issue loop is the MMA rate limiter)
+        const uint64_t sa = (uint64_t)(2u * lbo_a >> 4), sg = (uint64_t)(2u * lbo_g >> 4);
+        for (int m = 0; m < g.ngroups; ++m) {
+          uint64_t ad = a0 + (uint64_t)((uint32_t)g.ga[m] * lbo_a >> 4), bd = g0;
+          const uint32_t dt = tmem + (uint32_t)(m * g.Kn);
+          ptx::mma_tf32(dt, ad, bd, idesc, ch > 0 ? 1u : 0u);
+          for (int k = 1; k < g.ksteps; ++k) {
+            ad += sa;
+            bd += sg;
+            ptx::mma_tf32(dt, ad, bd, idesc, 1u);
+          }
         }
+        ptx::mma_commit(&done_bar);
+        if (ch == 0) WPHASE(3);
       }
-      ptx::mma_commit(&done_bar);
-      WPHASE(3);
+      __syncwarp();
     }
-    __syncwarp();
+    // this chunk's share of db (fixed order) while the MMAs run
+    for (int n = tid; n < g.K; n += WT)
+      for (int q = 0; q < g.Q; ++q) db_acc += ptx::lds_f32(g_at(n, q));
   }
-  // db partial (sum of G over positions, fixed order) while the MMAs run
   float* part = a.part + (int64_t)b * g.pstride;
   const int64_t nw = g.part - g.K;
-  for (int n = tid; n < g.K; n += WT) {
-    float acc = 0.f;
-    for (int q = 0; q < g.Q; ++q) acc += ptx::lds_f32(g_at(n, q));
-    part[nw + n] = acc;
-  }
-  ptx::mbar_wait(&done_bar, 0);
+  if (tid < g.K) part[nw + tid] = db_acc;
+  ptx::mbar_wait(&done_bar, (uint32_t)((g.nchunk - 1) & 1));
   ptx::tc_fence_after();
   if (tid == 0) WPHASE(4);
 
