@@ -126,7 +126,7 @@ __device__ __forceinline__ uint32_t tf32(float f) {
 // fragment layouts are the PTX m16n8k8 .row.col ones: lane = 4g + t,
 // a = {(g,t), (g+8,t), (g,t+4), (g+8,t+4)}, b = {(t,g), (t+4,g)},
 // c = {(g,2t), (g,2t+1), (g+8,2t), (g+8,2t+1)}.
-template <int NG>
+template <int NG, bool B_TF32 = false>  // B_TF32: B already rounded in smem
 __device__ __forceinline__ void warp_mma(float (&c)[NG][4], const float* A, int am, int ak,
                                          const float* Bm, int bn, int bk, int m0, int n0,
                                          int nvalid, int ksteps, int lane) {
@@ -140,8 +140,9 @@ __device__ __forceinline__ void warp_mma(float (&c)[NG][4], const float* A, int 
 #pragma unroll
     for (int j = 0; j < NG; ++j) {
       if (j < nvalid) {
-        const uint32_t b0 = tf32(pb[j * 8 * bn + k * bk]);
-        const uint32_t b1 = tf32(pb[j * 8 * bn + (k + 4) * bk]);
+        const float f0 = pb[j * 8 * bn + k * bk], f1 = pb[j * 8 * bn + (k + 4) * bk];
+        const uint32_t b0 = B_TF32 ? __float_as_uint(f0) : tf32(f0);
+        const uint32_t b1 = B_TF32 ? __float_as_uint(f1) : tf32(f1);
         asm volatile(
             "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
             "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
@@ -156,7 +157,7 @@ __device__ __forceinline__ void warp_mma(float (&c)[NG][4], const float* A, int 
 // into smem [Rp][s] (zero padded to Rp rows and Kp columns)
 __device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, int ld, int nrows,
                                            int Rp, int k0, int nc, int Kp, bool vec, int tid,
-                                           int nt) {
+                                           int nt, bool round = false) {
   if (vec) {  // float4: Kp, k0, ld multiples of 4, src 16B aligned
     const int q = Kp >> 2, n = Rp * q;
     constexpr int kU = 4;
@@ -172,7 +173,14 @@ __device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, 
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = base + u * nt + tid, r = i / q, k = 4 * (i - r * q);
-        if (i < n) *reinterpret_cast<float4*>(dst + r * s + k) = v[u];
+        float4 w = v[u];
+        if (round) {
+          w.x = __uint_as_float(tf32(w.x));
+          w.y = __uint_as_float(tf32(w.y));
+          w.z = __uint_as_float(tf32(w.z));
+          w.w = __uint_as_float(tf32(w.w));
+        }
+        if (i < n) *reinterpret_cast<float4*>(dst + r * s + k) = w;
       }
     }
   } else {
@@ -180,7 +188,8 @@ __device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, 
 #pragma unroll 1
     for (int i = tid; i < n; i += nt) {
       const int r = i / Kp, k = i - r * Kp;
-      dst[r * s + k] = (r < nrows && k < nc) ? __ldg(src + (size_t)r * ld + k0 + k) : 0.f;
+      const float v = (r < nrows && k < nc) ? __ldg(src + (size_t)r * ld + k0 + k) : 0.f;
+      dst[r * s + k] = round ? __uint_as_float(tf32(v)) : v;
     }
   }
 }
@@ -247,7 +256,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   const float sv0 = tid < nsmall ? small_src(tid) : 0.f;
   const float sv1 = tid + nt < nsmall ? small_src(tid + nt) : 0.f;
   stage_cols(xr, sK, a.x, in, B, d.Bp, k0, nc, d.Kp, a.vec, tid, nt);
-  stage_cols(wr, sK, a.WH, in, h, d.Hp, k0, nc, d.Kp, a.vec, tid, nt);
+  stage_cols(wr, sK, a.WH, in, h, d.Hp, k0, nc, d.Kp, a.vec, tid, nt, true);  // MMA-only: tf32
   if (tid < nsmall) *small_dst(tid) = sv0;
   if (tid + nt < nsmall) *small_dst(tid + nt) = sv1;
 #pragma unroll 1
@@ -268,7 +277,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
       const int m0 = im * 16, n0 = ig * 32;
       const int nv = nN - ig * 4 < 4 ? nN - ig * 4 : 4;
       float c[4][4] = {};
-      warp_mma<4>(c, xr, sK, 1, wr, sK, 1, m0, n0, nv, d.Kp >> 3, lane);
+      warp_mma<4, true>(c, xr, sK, 1, wr, sK, 1, m0, n0, nv, d.Kp >> 3, lane);
       const int g = lane >> 2, t = lane & 3;
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
@@ -499,7 +508,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
         const int m0 = im * 16, n0 = ig * 32;
         const int nv = nN - ig * 4 < 4 ? nN - ig * 4 : 4;
         float c[4][4] = {};
-        warp_mma<4>(c, G, sH, 1, wr, 1, sK, m0, n0, nv, d.Hp >> 3, lane);
+        warp_mma<4, true>(c, G, sH, 1, wr, 1, sK, m0, n0, nv, d.Hp >> 3, lane);
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const int b = m0 + g + 8 * hf;
