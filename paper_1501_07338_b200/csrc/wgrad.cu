@@ -92,9 +92,12 @@ bool wplan(const ConvDesc& d, const GradSrc& gs, WGeo& g) {
   // and the routed windows.  The largest chunk that fits; chunk starts must
   // be granule aligned (Rc*W % 4 == 0) and whole pool rows.
   const int dw_bytes = (int)(4 * g.part);
-  // (one chunk only for now: with a single A buffer, chunked images
-  // serialise build and MMA and lose to the slab kernel -- conv1 of CIFAR-3
-  // measured 47 us vs 34 us)
+  // (one chunk only: chunked images lose to the slab kernel on CIFAR-3's
+  // conv1 (C=3): with one A buffer build and MMA serialise (47 us vs 34 us);
+  // a per-kernel-row variant without the shift halo, A/G double-buffered,
+  // measured 79 us -- rebuilding 64 KB of shifted copies per 16 MMAs doubles
+  // the shared-memory traffic the MMAs already saturate, and 5/8 of the rows
+  // are channel padding at C=3)
   for (int Rc = d.OH; Rc >= d.OH; --Rc) {
     const int nch = (d.OH + Rc - 1) / Rc;
     if (nch > 1 && ((Rc * d.W) % 4 || (gs.pool && Rc % gs.pool))) continue;
