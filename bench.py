@@ -36,6 +36,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cifar3")
     ap.add_argument("--batch", type=int, default=128, help="per-GPU batch")
+    ap.add_argument("--channels", type=int, default=64, help="single-conv: C_in = C_out")
+    ap.add_argument("--ksize", type=int, default=5, help="single-conv: kernel size")
     ap.add_argument("--precision", default="tf32", choices=["tf32", "tf32x3", "fp32"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--momentum", type=float, default=0.9)
@@ -191,12 +193,25 @@ def cpu_reference(spec, B, steps, warmup, seconds=None):
             "ms_per_step": 1e3 * total / len(times)}
 
 
+def make_spec(args):
+    from paper_1501_07338_b200 import spec as S
+    if args.config == "single-conv":
+        return S.single_conv(channels=args.channels, k=args.ksize)
+    return S.PRESETS[args.config]()
+
+
+def workload_name(args):
+    if args.config == "single-conv":
+        return f"single-conv-c{args.channels}-k{args.ksize}-b{args.batch}-train"
+    return f"{args.config}-b{args.batch}-train"
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from paper_1501_07338_b200 import spec as S
-    spec = S.PRESETS[args.config]()
+    spec = make_spec(args)
     r = cpu_reference(spec, args.batch, args.steps, args.warmup)
     if r is None:
         print(json.dumps({"impl": "reference",
@@ -206,7 +221,7 @@ def run_reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Rng(8) stream, bench.cpp:29-45)",
-            "config": {"workload": f"{args.config}-b{args.batch}-train", "per_gpu_batch": args.batch,
+            "config": {"workload": workload_name(args), "per_gpu_batch": args.batch,
                        "global_batch": args.batch, "parallelism": "cpu (reference runs on host)"},
             "impl": "reference",
             "cpu_baseline": {"value": r["value"], "unit": "img/s", "cores": r["cores"],
@@ -235,7 +250,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    spec = S.PRESETS[args.config]()
+    spec = make_spec(args)
     B = args.batch
     prec = S.Precision[args.precision]
     lr, mom = args.lr, args.momentum
@@ -467,7 +482,7 @@ def main():
             "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (Rng(8) stream, bench.cpp:29-45); random-init Glorot weights",
-            "config": {"workload": f"{args.config}-b{B}-train", "per_gpu_batch": B,
+            "config": {"workload": workload_name(args), "per_gpu_batch": B,
                        "global_batch": B * world, "parallelism": f"dp{world}",
                        "precision": args.precision, "graph": not args.no_graph,
                        "l2": f"inputs > L2: {nbatch} distinct batches cycled from a "

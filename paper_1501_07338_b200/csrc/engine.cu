@@ -349,7 +349,7 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
   } else {
     Mark m(n, OTHER_F, nl - 1, OP_LOSS);
     TRY(launch_loss(n->spec.loss, B, (int)n->out_units, last.out, n->cls, n->values, n->loss,
-                    last.gpre, last.spec.act, n->err, st));
+                    last.gpre, last.spec.act, n->err, st, n->loss + 4));
   }
   // weight gradients on the side stream (not in breakdown mode, whose
   // per-op events live on the main stream)
@@ -393,6 +393,9 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
         if (dense)
           TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
                                 wsw, sw));
+        else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_small_ok(d, gs) &&
+                 wsw.bytes >= direct::wgrad_small_workspace(d))
+          TRY(direct::conv_wgrad_small(d, in, gs, gW, gB, wsw, sw));
         else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_ok(d, gs) &&
                  wsw.bytes >= direct::wgrad_workspace(d))
           TRY(direct::conv_wgrad(d, in, gs, gW, gB, wsw, sw));
@@ -711,7 +714,7 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
   s = s ? s : dalloc((void**)&n->x, sizeof(float) * n->in_per * max_batch);
   s = s ? s : dalloc((void**)&n->cls, sizeof(int) * max_batch);
   s = s ? s : dalloc((void**)&n->values, sizeof(float) * n->out_units * max_batch);
-  s = s ? s : dalloc((void**)&n->loss, sizeof(float) * 4);
+  s = s ? s : dalloc((void**)&n->loss, sizeof(float) * (4 + kLossWsFloats));
   s = s ? s : dalloc((void**)&n->err, sizeof(int) * 4);
   size_t wsb = 0;
   for (LayerRt& l : n->L) {
@@ -742,6 +745,8 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
         need = conv_workspace(conv_of(l, B), VCNN_PREC_TF32);
         const size_t dw = direct::wgrad_workspace(conv_of(l, B));
         if (dw > need) need = dw;
+        const size_t dws = direct::wgrad_small_workspace(conv_of(l, B));
+        if (dws > need) need = dws;
       }
       else if (l.spec.kind == VCNN_LAYER_FULL)
         need = full_workspace(B, (int)l.in_per, l.spec.units, VCNN_PREC_TF32);
@@ -770,7 +775,8 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
         cudaMemset(n->vel, 0, pbytes) != cudaSuccess ||
         cudaMemset(n->values, 0, sizeof(float) * n->out_units * max_batch) != cudaSuccess ||
         cudaMemset(n->cls, 0, sizeof(int) * max_batch) != cudaSuccess ||
-        cudaMemset(n->err, 0, sizeof(int) * 4) != cudaSuccess)
+        cudaMemset(n->err, 0, sizeof(int) * 4) != cudaSuccess ||
+        cudaMemset(n->loss, 0, sizeof(float) * (4 + kLossWsFloats)) != cudaSuccess)
       s = fail(VCNN_ECUDA, "net_create: initial upload failed");
   }
   if (!s) {

@@ -59,10 +59,14 @@ int launch_act_fwd(int64_t n, int act, const float* x, float* y, cudaStream_t st
 int launch_act_bwd(int64_t n, int act, const float* y, const float* dy, float* g,
                    cudaStream_t st);
 // fused loss forward+backward; grad = dL/dpred * act_last'(pred); err set on
-// out-of-range class.  Any of loss/grad may be null.
+// out-of-range class.  Any of loss/grad may be null.  ws (nullable, at least
+// kLossWsFloats floats, zero-initialised once) lets MSE spread over the whole
+// chip: per-CTA partials + a last-CTA fixed-order reduce (deterministic).
+constexpr int kMseMaxCtas = 1024;
+constexpr int kLossWsFloats = kMseMaxCtas + 4;
 int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
                 const float* values, float* loss, float* grad, int act_last, int* err,
-                cudaStream_t st);
+                cudaStream_t st, float* ws = nullptr);
 int launch_sgd(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
                cudaStream_t st);
 // batch row j <- dataset row order[start + j] (+ class / value targets)
@@ -186,6 +190,12 @@ bool wgrad_ok(const ConvDesc& d, const GradSrc& gs);
 size_t wgrad_workspace(const ConvDesc& d);
 int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
                const Workspace& ws, cudaStream_t st);
+// small-Kd variant (C*kh*kw + 1 <= 96, K <= 32: first layers), mma.sync TF32,
+// one CTA per image, same partial layout and fixed-order reduce
+bool wgrad_small_ok(const ConvDesc& d, const GradSrc& gs);
+size_t wgrad_small_workspace(const ConvDesc& d);
+int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
+                     const Workspace& ws, cudaStream_t st);
 }  // namespace direct
 
 // ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----

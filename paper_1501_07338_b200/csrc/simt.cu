@@ -324,6 +324,70 @@ __global__ void __launch_bounds__(kLossThreads) mse_kernel(int64_t n, const floa
   if (threadIdx.x == 0 && loss) *loss = acc / (float)n;
 }
 
+// MSE over many CTAs: CTA i owns the contiguous chunk [i*chunk, (i+1)*chunk)
+// (float4 when the pointers allow), writes its fixed-order partial, and the
+// last CTA to finish sums the partials in CTA order and re-arms the counter.
+// The chunking depends only on n, so the loss is deterministic.
+constexpr int kMseThreads = 512;
+__global__ void __launch_bounds__(kMseThreads) mse_multi_kernel(
+    int64_t n, int64_t chunk, const float* __restrict__ p, const float* __restrict__ t,
+    float* __restrict__ loss, float* __restrict__ grad, int act_last, float* ws, int vec) {
+  PDL_ENTRY();
+  __shared__ float sh[kMseThreads];
+  __shared__ bool last;
+  const float scale = 2.0f / (float)n;
+  const int64_t lo = (int64_t)blockIdx.x * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  float acc = 0.f;
+  auto one = [&](float pv, float tv, float& gv) {
+    const float dd = pv - tv;
+    acc += dd * dd;
+    gv = scale * dd;
+    if (act_last != VCNN_ACT_IDENTITY) gv *= act_grad_from_out(act_last, pv);
+  };
+  if (vec) {  // lo, hi multiples of 4 except possibly hi == n
+    const int64_t h4 = lo + ((hi - lo) & ~int64_t(3));
+    for (int64_t i = lo + 4 * (int64_t)threadIdx.x; i < h4; i += 4 * kMseThreads) {
+      const float4 pv = *reinterpret_cast<const float4*>(p + i);
+      const float4 tv = *reinterpret_cast<const float4*>(t + i);
+      float4 g;
+      one(pv.x, tv.x, g.x);
+      one(pv.y, tv.y, g.y);
+      one(pv.z, tv.z, g.z);
+      one(pv.w, tv.w, g.w);
+      if (grad) *reinterpret_cast<float4*>(grad + i) = g;
+    }
+    for (int64_t i = h4 + threadIdx.x; i < hi; i += kMseThreads) {
+      float g;
+      one(p[i], t[i], g);
+      if (grad) grad[i] = g;
+    }
+  } else {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kMseThreads) {
+      float g;
+      one(p[i], t[i], g);
+      if (grad) grad[i] = g;
+    }
+  }
+  acc = block_sum<kMseThreads>(acc, sh);
+  unsigned* counter = reinterpret_cast<unsigned*>(ws + kMseMaxCtas);
+  if (threadIdx.x == 0) {
+    ws[blockIdx.x] = acc;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  float v = 0.f;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += kMseThreads) v += ((volatile float*)ws)[i];
+  v = block_sum<kMseThreads>(v, sh);
+  if (threadIdx.x == 0) {
+    if (loss) *loss = v / (float)n;
+    *counter = 0u;
+  }
+}
+
 // sgd_step (network.hpp:242-273): v = mom*v + g; w -= lr*v
 __global__ void sgd_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
                            const float* __restrict__ g, float lr, float mom, float scale,
@@ -689,7 +753,21 @@ int launch_act_bwd(int64_t n, int act, const float* y, const float* dy, float* g
 
 int launch_loss(int kind, int B, int units, const float* pred, const int* cls,
                 const float* values, float* loss, float* grad, int act_last, int* err,
-                cudaStream_t st) {
+                cudaStream_t st, float* ws) {
+  const int64_t n = (int64_t)B * units;
+  if (kind == VCNN_LOSS_MSE && ws && n >= 32768) {
+    // ~16K elements per CTA, chunk a multiple of 4 so float4 runs stay aligned
+    int64_t ctas = cdiv(n, 16384);
+    if (ctas > kMseMaxCtas) ctas = kMseMaxCtas;
+    const int64_t chunk = (cdiv(n, ctas) + 3) & ~int64_t(3);
+    ctas = cdiv(n, chunk);
+    const int vec = ((reinterpret_cast<uintptr_t>(pred) | reinterpret_cast<uintptr_t>(values) |
+                      reinterpret_cast<uintptr_t>(grad)) & 15) == 0;
+    VCNN_CUDA_TRY(launch_pdl(mse_multi_kernel, dim3((unsigned)ctas), dim3(kMseThreads), 0, st, n,
+                             chunk, pred, values, loss, grad, act_last, ws, vec));
+    VCNN_LAUNCHED();
+    return VCNN_OK;
+  }
   if (kind == VCNN_LOSS_SOFTMAX_CE) {
     VCNN_CUDA_TRY(launch_pdl(softmax_ce_kernel, dim3(1), dim3(kLossThreads), 0, st, B, units, pred, cls, loss, grad, act_last, err));
   } else {

@@ -377,6 +377,222 @@ __global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small-Kd weight gradient (first layers: C*kh*kw + 1 <= 96, e.g. CIFAR-3
+// conv1 C=3 5x5, LeNet conv1 C=1 5x5) on mma.sync m16n8k8 TF32.
+//   dW|db [n][j] = sum_q G[n][q] * P[j][q],  P[j][q] = x[c][oy+ky][ox+kx]
+// for j = (c,ky,kx) < Kd, and P[Kd][q] = 1 (the bias gradient as a ones
+// column).  One CTA per image; M = maps (G rows, tf32 in shared memory),
+// N = Kd+1 columns gathered straight from the staged image (a column is a
+// fixed offset into [c][H][W]; a position is an offset table), K = the
+// image's output positions split over the 8 warps, whose partial tiles are
+// summed in warp order (deterministic).  At these sizes the per-image GEMM
+// (32 x 76 x 784 for conv1) is far below one tcgen05 tile's fill cost: the
+// tcgen05 slab kernel spends 5/8 of its A rows on channel padding and
+// serialises staging and MMA; here staging is one bulk copy + one scatter
+// and the MMAs run at 512 FMA/clk/SM from registers.
+constexpr int ST = 256;  // threads
+constexpr int kSmallMaxCols = 96;
+
+struct SGeo {
+  int B, C, H, W, K, kh, kw, OH, OW;
+  int Kd, mt, nt;        // columns, M tiles (16 maps), N tiles (8 columns)
+  int ohw, Q8, Qs;       // positions, padded to 8 (K extent), G row stride
+  int ksteps;
+  int pool, POH, POW, wsz;
+  int off_g, off_x, off_q, off_win, smem;  // bytes
+  int xfl;               // floats staged for x: image + zero + ones regions
+  int64_t part, pstride;
+};
+
+bool splan(const ConvDesc& d, const GradSrc& gs, SGeo& g) {
+  g = SGeo{};
+  if (d.s != 1 || d.K < 1 || d.K > 32) return false;
+  g.B = d.B, g.C = d.C, g.H = d.H, g.W = d.W, g.K = d.K, g.kh = d.kh, g.kw = d.kw;
+  g.OH = d.OH, g.OW = d.OW;
+  g.Kd = d.C * d.kh * d.kw;
+  if (g.Kd + 1 > kSmallMaxCols) return false;
+  g.mt = (d.K + 15) / 16;
+  g.nt = (g.Kd + 1 + 7) / 8;
+  g.ohw = d.OH * d.OW;
+  g.Q8 = (g.ohw + 7) / 8 * 8;
+  g.Qs = g.Q8 + 4;  // row stride = 4 (mod 8): the A-fragment loads are conflict-free
+  g.ksteps = g.Q8 / 8;
+  const int hw = d.H * d.W;
+  if ((d.C * hw) % 4) return false;
+  g.xfl = (d.C + 2) * hw;
+  g.pool = gs.pool, g.POH = gs.POH, g.POW = gs.POW;
+  g.wsz = gs.pool ? d.K * gs.POH * gs.POW : 0;
+  if (gs.pool && g.wsz % 4) return false;
+  // windows reserved for any 2x2-or-larger pool, routed or not (same plan on
+  // the fused and the trace path -> bit-identical)
+  const int win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
+  if (g.wsz > win_n) return false;
+  g.off_g = 0;
+  const int gbytes = 4 * g.mt * 16 * g.Qs;
+  const int ntb = g.nt <= 4 ? 4 : g.nt <= 8 ? 8 : 12;  // the kernel's NT bucket
+  const int red_bytes = 4 * (ST / 32) * g.mt * 16 * ntb * 8;  // reuses G
+  g.off_x = ((gbytes > red_bytes ? gbytes : red_bytes) + 127) & ~127;
+  g.off_q = (g.off_x + 4 * g.xfl + 127) & ~127;
+  g.off_win = (g.off_q + 4 * g.Q8 + 127) & ~127;
+  g.smem = g.off_win + 8 * win_n + 128;
+  if ((size_t)g.smem > kSmemMax) return false;
+  g.part = (int64_t)d.K * g.Kd + d.K;
+  g.pstride = (g.part + 3) / 4 * 4;
+  return true;
+}
+
+struct SArgs {
+  SGeo g;
+  const float* x;
+  GradSrc gs;
+  float* part;
+};
+
+__device__ __forceinline__ void mma_tf32_sync(float (&c)[4], uint32_t a0, uint32_t a1,
+                                              uint32_t a2, uint32_t a3, uint32_t b0,
+                                              uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
+  pdl_launch_dependents();
+  const SGeo& g = a.g;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
+                                             ~static_cast<uintptr_t>(127));
+  __shared__ uint64_t load_bar;
+  float* sg = reinterpret_cast<float*>(smem + g.off_g);
+  float* sx = reinterpret_cast<float*>(smem + g.off_x);
+  int* sq = reinterpret_cast<int*>(smem + g.off_q);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.x, hw = g.H * g.W, ohw = g.ohw;
+  const bool routed = a.gs.pool != 0;
+  const uint32_t s_x = ptx::smem_u32(sx), s_win = ptx::smem_u32(smem + g.off_win);
+
+  if (tid == 0) {
+    ptx::mbar_init(&load_bar, 1);
+    ptx::fence_mbar_init();
+  }
+  // independent of the predecessor: zero G, the zero / ones columns, the
+  // position table (q -> oy*W + ox, padding clamped to a real position)
+  const int gfl = MT * 16 * g.Qs;
+  for (int i = tid; i < gfl / 4; i += ST)
+    reinterpret_cast<float4*>(sg)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = tid; i < 2 * hw; i += ST) sx[g.C * hw + i] = i < hw ? 0.f : 1.f;
+  for (int q = tid; q < g.Q8; q += ST) {
+    const int qq = q < ohw ? q : ohw - 1, oy = qq / g.OW;
+    sq[q] = oy * g.W + (qq - oy * g.OW);
+  }
+  __syncthreads();
+  pdl_wait();
+  if (tid == 0) {
+    const uint32_t xb = 4u * (uint32_t)(g.C * hw);
+    uint32_t tx = xb;
+    if (routed) tx += 8u * (uint32_t)g.wsz;
+    ptx::mbar_expect_tx(&load_bar, tx);
+    ptx::bulk_g2s(s_x, a.x + (int64_t)b * g.C * hw, xb, &load_bar);
+    if (routed) {
+      const uint32_t gb = 4u * (uint32_t)g.wsz;
+      ptx::bulk_g2s(s_win, a.gs.dP + (int64_t)b * g.wsz, gb, &load_bar);
+      ptx::bulk_g2s(s_win + gb, a.gs.parg + (int64_t)b * g.wsz, gb, &load_bar);
+    }
+    ptx::mbar_arrive(&load_bar);
+  }
+  if (!routed) {  // plain gradient [K][OH][OW] of this image, tf32
+    const float* src = a.gs.g + (int64_t)b * g.K * ohw;
+    for (int i = tid; i < g.K * ohw; i += ST) {
+      const int n = i / ohw, q = i - n * ohw;
+      sg[n * g.Qs + q] = ptx::to_tf32(__ldg(src + i));
+    }
+  }
+  ptx::mbar_wait(&load_bar, 0);
+  if (routed) {  // dP scattered to the argmax positions (global index - image base)
+    const float* wv = reinterpret_cast<const float*>(smem + g.off_win);
+    const int* wa = reinterpret_cast<const int*>(smem + g.off_win) + g.wsz;
+    const int base = b * g.K * ohw, pw = g.POH * g.POW;
+    for (int i = tid; i < g.wsz; i += ST) {
+      const int n = i / pw;
+      sg[n * g.Qs + (wa[i] - base - n * ohw)] = ptx::to_tf32(wv[i]);
+    }
+  }
+  for (int i = tid; i < g.C * hw; i += ST) sx[i] = ptx::to_tf32(sx[i]);
+  __syncthreads();
+
+  // ---- per lane: N-tile column offsets (c,ky,kx) -> c*hw + ky*W + kx ----
+  const int gq = lane >> 2, t = lane & 3;
+  int coff[NT];
+#pragma unroll
+  for (int jt = 0; jt < NT; ++jt) {
+    const int j = jt * 8 + gq;
+    if (j < g.Kd) {
+      const int c = j / (g.kh * g.kw), r = j - c * g.kh * g.kw, ky = r / g.kw;
+      coff[jt] = c * hw + ky * g.W + (r - ky * g.kw);
+    } else {
+      coff[jt] = (j == g.Kd ? g.C + 1 : g.C) * hw;  // ones (bias) / zero column
+    }
+  }
+  float acc[MT][NT][4];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int jt = 0; jt < NT; ++jt)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[mi][jt][u] = 0.f;
+  const int nt = g.nt;
+  for (int ks = warp; ks < g.ksteps; ks += ST / 32) {
+    const int q0 = ks * 8 + t;
+    uint32_t af[MT][4];
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi) {
+      const float* r0 = sg + (mi * 16 + gq) * g.Qs + q0;
+      af[mi][0] = __float_as_uint(r0[0]);
+      af[mi][1] = __float_as_uint(r0[8 * g.Qs]);
+      af[mi][2] = __float_as_uint(r0[4]);
+      af[mi][3] = __float_as_uint(r0[8 * g.Qs + 4]);
+    }
+    const int p0 = sq[q0], p1 = sq[q0 + 4];
+#pragma unroll
+    for (int jt = 0; jt < NT; ++jt) {
+      if (jt < nt) {
+        const uint32_t b0 = __float_as_uint(sx[coff[jt] + p0]);
+        const uint32_t b1 = __float_as_uint(sx[coff[jt] + p1]);
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+          mma_tf32_sync(acc[mi][jt], af[mi][0], af[mi][1], af[mi][2], af[mi][3], b0, b1);
+      }
+    }
+  }
+  __syncthreads();  // G is dead: the warps' partial tiles go over it
+  const int tw = MT * 16 * NT * 8;  // floats per warp tile [m][n]
+  float* red = sg + warp * tw;
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int jt = 0; jt < NT; ++jt) {
+      const int m = mi * 16 + gq, n = jt * 8 + 2 * t;
+      red[m * NT * 8 + n] = acc[mi][jt][0];
+      red[m * NT * 8 + n + 1] = acc[mi][jt][1];
+      red[(m + 8) * NT * 8 + n] = acc[mi][jt][2];
+      red[(m + 8) * NT * 8 + n + 1] = acc[mi][jt][3];
+    }
+  __syncthreads();
+  float* part = a.part + (int64_t)b * g.pstride;
+  const int cols = g.Kd + 1;
+  for (int i = tid; i < g.K * cols; i += ST) {
+    const int m = i / cols, j = i - m * cols;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < ST / 32; ++w) s += sg[w * tw + m * NT * 8 + j];
+    part[j < g.Kd ? m * g.Kd + j : g.K * g.Kd + m] = s;
+  }
+}
+
 }  // namespace
 
 bool wgrad_ok(const ConvDesc& d, const GradSrc& gs) {
@@ -413,6 +629,55 @@ int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, 
   const int64_t blocks = cdiv(per, 32);
   VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)blocks), dim3(32 * kRedSlices), 0, st, d.B, per,
                            a.g.pstride, nw, (const float*)ws.ptr, dw, db));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+bool wgrad_small_ok(const ConvDesc& d, const GradSrc& gs) {
+  SGeo g;
+  return splan(d, gs, g);
+}
+
+size_t wgrad_small_workspace(const ConvDesc& d) {
+  SGeo g;
+  GradSrc gs;
+  if (!splan(d, gs, g)) return 0;
+  return sizeof(float) * (size_t)(g.pstride * d.B);
+}
+
+int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
+                     const Workspace& ws, cudaStream_t st) {
+  SArgs a{};
+  if (!splan(d, gs, a.g)) return fail(VCNN_ESHAPE, "small wgrad: geometry not supported");
+  const size_t need = sizeof(float) * (size_t)(a.g.pstride * d.B);
+  if (ws.bytes < need) return fail(VCNN_ECONFIG, "small wgrad: workspace too small");
+  a.x = x;
+  a.gs = gs;
+  a.part = ws.ptr;
+  const size_t smem = (size_t)a.g.smem;
+  auto go = [&](auto kern, size_t& configured) -> int {
+    if (smem > configured) {
+      VCNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      configured = smem;
+    }
+    VCNN_CUDA_TRY(launch_pdl(kern, dim3((unsigned)d.B), dim3(ST), smem, st, a));
+    VCNN_LAUNCHED();
+    return VCNN_OK;
+  };
+  static size_t c14 = 0, c18 = 0, c112 = 0, c24 = 0, c28 = 0, c212 = 0;
+  int s;
+  if (a.g.mt == 1)
+    s = a.g.nt <= 4 ? go(wgrad_small_kernel<1, 4>, c14)
+        : a.g.nt <= 8 ? go(wgrad_small_kernel<1, 8>, c18) : go(wgrad_small_kernel<1, 12>, c112);
+  else
+    s = a.g.nt <= 4 ? go(wgrad_small_kernel<2, 4>, c24)
+        : a.g.nt <= 8 ? go(wgrad_small_kernel<2, 8>, c28) : go(wgrad_small_kernel<2, 12>, c212);
+  if (s) return s;
+  const int64_t per = a.g.part, nw = per - d.K;
+  VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)cdiv(per, 32)),
+                           dim3(32 * kRedSlices), 0, st, d.B, per, a.g.pstride, nw,
+                           (const float*)ws.ptr, dw, db));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

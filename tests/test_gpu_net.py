@@ -459,3 +459,25 @@ def test_model_export_reference_predicts_the_same(tmp_path):
     assert np.array_equal(net2.get_params(), net.get_params())
     net.close()
     net2.close()
+
+
+@pytest.mark.parametrize("prec", [Precision.tf32x3, Precision.fp32], ids=lambda p: p.name)
+def test_large_mse_loss_multi_cta(prec):
+    """A conv-output MSE large enough for the multi-CTA loss kernel (per-CTA
+    partials, last-CTA fixed-order reduce): loss and gradients match the
+    oracle, and two runs are bit-identical (deterministic reduction)."""
+    spec = S.single_conv(channels=8, k=3, hw=32)
+    B = 64  # 64 x 8 x 30 x 30 = 460,800 loss elements
+    x, cls, vals = O.synth_bench_data(spec, B, 8)
+    outs = []
+    for _ in range(2):
+        net = Network(spec, B, prec)
+        _load(net, spec, x, cls, vals)
+        net.forward_backward(B)
+        outs.append((net.loss(), net.get_grads(), net.get_params().astype(np.float64)))
+        net.close()
+    (l0, g0, p0), (l1, g1, _) = outs
+    assert l0 == l1 and np.array_equal(g0, g1)
+    r = O.net_run_batch(spec, p0, f32(x), values=vals)
+    assert abs(l0 - r["loss"]) <= TOL[prec] * max(1.0, abs(r["loss"]))
+    assert_close(g0, r["grads"], 5 * TOL[prec], "grads")
