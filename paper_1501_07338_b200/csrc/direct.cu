@@ -82,6 +82,9 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
     g.Wg = d.W + d.kw - 1, g.Hout = d.H, g.Wout = d.W, g.pad_y = d.kh - 1, g.pad_x = d.kw - 1;
   }
   if (g.Wg > BM || g.Hout < 1) return false;
+  // a forward view with < 4 input channels pads the MMA K (8 channels) by 2x
+  // or more; those layers go to the small-Kd kernel or the generic implicit GEMM
+  if (mode == 0 && g.Cin < 4) return false;
   int R = BM / g.Wg;
   if (R > g.Hout) R = g.Hout;
   if (pool) {
@@ -632,6 +635,318 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
   VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, w, v, g, lr, mom, scale, t));
   VCNN_LAUNCHED();
   return VCNN_OK;
+}
+
+namespace {
+// ---------------------------------------------------------------------------
+// Small-Kd forward (first layers: C*kh*kw <= 96, K <= 32; CIFAR-3 conv1 is
+// 3x5x5 -> 32) on mma.sync m16n8k8 TF32, one CTA per image.
+//   y[n][q] = act(sum_j W[n][j] * x[c][oy+ky][ox+kx] + b[n]),  j = (c,ky,kx)
+// M = output positions (16 per tile), N = maps (W fragments live in
+// registers for the whole CTA), K = Kd (a column j is a fixed offset into the
+// staged image, a row a position offset).  When OH and OW are even the 16
+// rows of a tile are four 2x2 windows, element-major (row = 4e + w), so a lane
+// and its lane^16 partner hold all four elements of a window for two maps and
+// the fused max pool + argmax is one shuffle; the trace path (no pool) uses
+// the same row mapping, so fused and unfused runs are bit-identical.  The
+// output of the image is staged in shared memory and written as one
+// contiguous block.  At 2 FLOP/B the layer is HBM/latency-bound; the tcgen05
+// direct kernel pays 5/8 channel padding (C=3 of 8) and a TMEM round trip.
+constexpr int FT = 128;   // 4 warps
+constexpr int kTilesPerWarp = 2;
+constexpr int kTilesPerCta = 4 * kTilesPerWarp;
+struct FGeo {
+  int B, C, H, W, K, kh, kw, OH, OW;
+  int Kd, nks, nnt;   // columns, K steps (8), N tiles (8 maps)
+  int wst;            // W row stride in smem (4 mod 8: conflict-free B fragments)
+  int win;            // 1: rows are 2x2 windows (OH, OW even)
+  int POH, POW, nmt;  // pooled extents, M tiles per image
+  int S;              // CTAs per image (kTilesPerCta M tiles each)
+  int off_w, off_o, smem;  // bytes
+  int pool;
+  int jo[96];         // column j = (c,ky,kx) -> c*H*W + ky*W + kx (no device divisions)
+};
+
+bool fplan_small(const ConvDesc& d, int pool, FGeo& g) {
+  g = FGeo{};
+  if (d.s != 1 || d.K < 1 || d.K > 32) return false;
+  g.B = d.B, g.C = d.C, g.H = d.H, g.W = d.W, g.K = d.K, g.kh = d.kh, g.kw = d.kw;
+  g.OH = d.OH, g.OW = d.OW;
+  g.Kd = d.C * d.kh * d.kw;
+  if (g.Kd > 96) return false;
+  g.nks = (g.Kd + 7) / 8;
+  g.nnt = (d.K + 7) / 8;
+  const int hw = d.H * d.W, ohw = d.OH * d.OW;
+  g.wst = (g.nks <= 4 ? 32 : 96) + 4;  // the kernel's KS*8 staged columns + 4
+  for (int j = 0; j < 96; ++j) {
+    if (j < g.Kd) {
+      const int c = j / (d.kh * d.kw), r = j - c * d.kh * d.kw, ky = r / d.kw;
+      g.jo[j] = c * hw + ky * d.W + (r - ky * d.kw);
+    } else {
+      g.jo[j] = d.C * hw;  // the zero column
+    }
+  }
+  if ((d.C * hw) % 4) return false;
+  g.win = (d.OH % 2 == 0 && d.OW % 2 == 0) ? 1 : 0;
+  if (pool && (pool != 2 || !g.win)) return false;
+  g.pool = pool;
+  g.POH = d.OH / 2, g.POW = d.OW / 2;
+  g.nmt = g.win ? (g.POH * g.POW + 3) / 4 : (ohw + 15) / 16;
+  g.S = (g.nmt + kTilesPerCta - 1) / kTilesPerCta;
+  g.off_w = (4 * (d.C + 1) * hw + 127) & ~127;
+  g.off_o = (g.off_w + 4 * g.nnt * 8 * g.wst + 127) & ~127;
+  const int ob = 8 * d.K * kTilesPerCta * 4;  // pooled values + args of the CTA's windows
+  g.smem = g.off_o + ob + 128;
+  if (g.smem > 227 * 1024) return false;
+  return true;
+}
+
+struct FSArgs {
+  FGeo g;
+  const float* x;
+  const float* w;  // [K][Kd] (params, rounded to tf32 when staged)
+  const float* bias;
+  float* y;        // [B][K][OH][OW] (unpooled)
+  float* py;       // [B][K][POH][POW] (pooled)
+  int32_t* parg;
+};
+
+__device__ __forceinline__ void mma_tf32_m16n8k8(float (&c)[4], uint32_t a0, uint32_t a1,
+                                                 uint32_t a2, uint32_t a3, uint32_t b0,
+                                                 uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+      "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// CTA (b, s) computes M tiles [s*kTilesPerCta, ...) of image b; warp w the
+// pair 2w, 2w+1 of them (two independent accumulator sets per K step)
+template <int KS, int ACT>
+__global__ void __launch_bounds__(FT) conv_small_fwd_kernel(const FSArgs a) {
+  pdl_launch_dependents();
+  const FGeo& g = a.g;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
+  __shared__ uint64_t load_bar;
+  float* sx = reinterpret_cast<float*>(smem);
+  float* sw = reinterpret_cast<float*>(smem + g.off_w);
+  float* so = reinterpret_cast<float*>(smem + g.off_o);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, t = lane & 3;
+  const int b = blockIdx.x / g.S, sidx = blockIdx.x - b * g.S;
+  const int hw = g.H * g.W, ohw = g.OH * g.OW, PP = g.POH * g.POW;
+  if (tid == 0) {
+    ptx::mbar_init(&load_bar, 1);
+    ptx::fence_mbar_init();
+  }
+  for (int i = tid; i < hw; i += FT) sx[g.C * hw + i] = 0.f;  // zero column
+  int coff[KS][2];  // A column offsets of this lane's two K slots per step
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) coff[ks][h] = g.jo[ks * 8 + t + 4 * h];
+  __syncthreads();
+  pdl_wait();
+  if (tid == 0) {
+    const uint32_t xb = 4u * (uint32_t)(g.C * hw);
+    ptx::mbar_expect_tx(&load_bar, xb);
+    ptx::bulk_g2s(ptx::smem_u32(sx), a.x + (int64_t)b * g.C * hw, xb, &load_bar);
+    ptx::mbar_arrive(&load_bar);
+  }
+  // W -> smem [n][wst], tf32, zero padded (rows to nnt*8, columns to KS*8)
+  constexpr int wcols = KS * 8;
+  const int wrows = g.nnt * 8;
+  // (cp.async: every element's load in flight at once; rounded after the wait)
+  for (int i = tid; i < wrows * wcols; i += FT) {
+    const int n = i / wcols, j = i - n * wcols;
+    if (n < g.K && j < g.Kd)
+      ptx::cp_async4(ptx::smem_u32(sw + n * g.wst + j), a.w + n * g.Kd + j);
+    else
+      sw[n * g.wst + j] = 0.f;
+  }
+  ptx::cp_async_wait_all();
+  ptx::mbar_wait(&load_bar, 0);
+  for (int i = tid; i < g.C * hw; i += FT) sx[i] = ptx::to_tf32(sx[i]);
+  for (int i = tid; i < wrows * wcols; i += FT) {
+    const int n = i / wcols, j = i - n * wcols;
+    sw[n * g.wst + j] = ptx::to_tf32(sw[n * g.wst + j]);
+  }
+  __syncthreads();
+
+  const int mbase = sidx * kTilesPerCta;
+  float acc[kTilesPerWarp][4][4];
+  int qi[kTilesPerWarp][2], po[kTilesPerWarp][2];
+  bool ok[kTilesPerWarp][2];
+#pragma unroll
+  for (int p = 0; p < kTilesPerWarp; ++p) {
+    const int mt = mbase + warp * kTilesPerWarp + p;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = gq + 8 * h;
+      int oy, ox;
+      if (g.win) {
+        int wi = mt * 4 + (r & 3);
+        ok[p][h] = wi < PP;
+        wi = ok[p][h] ? wi : PP - 1;
+        const int e = r >> 2, py = wi / g.POW, px = wi - py * g.POW;
+        oy = 2 * py + (e >> 1);
+        ox = 2 * px + (e & 1);
+      } else {
+        int m = mt * 16 + r;
+        ok[p][h] = m < ohw;
+        m = ok[p][h] ? m : ohw - 1;
+        oy = m / g.OW;
+        ox = m - oy * g.OW;
+      }
+      qi[p][h] = oy * g.OW + ox;
+      po[p][h] = oy * g.W + ox;
+    }
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[p][nt][u] = 0.f;
+  }
+  const float* wrow = sw + gq * g.wst + t;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    if (ks < g.nks) {
+      uint32_t bf[4][2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        if (nt < g.nnt) {
+          bf[nt][0] = __float_as_uint(wrow[nt * 8 * g.wst + ks * 8]);
+          bf[nt][1] = __float_as_uint(wrow[nt * 8 * g.wst + ks * 8 + 4]);
+        }
+#pragma unroll
+      for (int p = 0; p < kTilesPerWarp; ++p) {
+        const uint32_t a0 = __float_as_uint(sx[coff[ks][0] + po[p][0]]);
+        const uint32_t a1 = __float_as_uint(sx[coff[ks][0] + po[p][1]]);
+        const uint32_t a2 = __float_as_uint(sx[coff[ks][1] + po[p][0]]);
+        const uint32_t a3 = __float_as_uint(sx[coff[ks][1] + po[p][1]]);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          if (nt < g.nnt) mma_tf32_m16n8k8(acc[p][nt], a0, a1, a2, a3, bf[nt][0], bf[nt][1]);
+      }
+    }
+  }
+  // epilogue: c = {(gq, 2t), (gq, 2t+1), (gq+8, 2t), (gq+8, 2t+1)}
+  float bb[4][2];
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int nc = nt * 8 + 2 * t + h;
+      bb[nt][h] = nc < g.K ? __ldg(a.bias + nc) : 0.f;
+    }
+  const int wloc0 = warp * kTilesPerWarp * 4;  // first window of this warp in the CTA
+#pragma unroll
+  for (int p = 0; p < kTilesPerWarp; ++p) {
+    const int mt = mbase + warp * kTilesPerWarp + p;
+    const int wi = mt * 4 + (gq & 3);
+    const int wpy = wi / g.POW, wpx = wi - wpy * g.POW;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = actf<ACT>(acc[p][nt][u] + bb[nt][u & 1]);
+      if (!g.pool) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int n = nt * 8 + 2 * t + (u & 1), h = u >> 1;
+          if (ok[p][h] && n < g.K && mt < g.nmt)
+            a.y[((int64_t)b * g.K + n) * ohw + qi[p][h]] = v[u];
+        }
+      } else {
+        // lane gq<4 holds elements e=0 (row gq), e=2 (row gq+8) of window
+        // w=gq; its partner lane^16 holds e=1, e=3.  The low lane pools map
+        // 2t, the high lane map 2t+1; window order e = 0,1,2,3, strict >.
+        float pv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) pv[u] = __shfl_xor_sync(0xffffffffu, v[u], 16);
+        const bool lo = gq < 4;
+        float e[4];
+        e[0] = lo ? v[0] : pv[1];
+        e[1] = lo ? pv[0] : v[1];
+        e[2] = lo ? v[2] : pv[3];
+        e[3] = lo ? pv[2] : v[3];
+        float best = e[0];
+        int bi = 0;
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+          if (e[k] > best) {
+            best = e[k];
+            bi = k;
+          }
+        const int n = nt * 8 + 2 * t + (lo ? 0 : 1);
+        if (wi < PP && n < g.K) {
+          const int q = (2 * wpy + (bi >> 1)) * g.OW + 2 * wpx + (bi & 1);
+          const int wl = wloc0 + p * 4 + (gq & 3);
+          so[n * kTilesPerCta * 4 + wl] = best;
+          reinterpret_cast<int32_t*>(so)[(g.K + n) * kTilesPerCta * 4 + wl] =
+              (b * g.K + n) * ohw + q;
+        }
+      }
+    }
+  }
+  if (g.pool) {  // the CTA's windows [w0, w0+nw) of every map: row segments
+    __syncthreads();
+    constexpr int CW = kTilesPerCta * 4;
+    const int w0 = mbase * 4;
+    const int nw = PP - w0 < CW ? PP - w0 : CW;
+    for (int i = tid; i < g.K * CW; i += FT) {
+      const int n = i / CW, r = i - n * CW;
+      if (r >= nw) continue;
+      const int64_t o = ((int64_t)b * g.K + n) * PP + w0 + r;
+      a.py[o] = so[n * CW + r];
+      a.parg[o] = reinterpret_cast<const int32_t*>(so)[(g.K + n) * CW + r];
+    }
+  }
+}
+
+template <int ACT>
+int launch_small_fwd(const FSArgs& a, cudaStream_t st) {
+  const size_t smem = (size_t)a.g.smem;
+  auto go = [&](auto kern, size_t& configured) -> int {
+    if (smem > configured) {
+      VCNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+      configured = smem;
+    }
+    VCNN_CUDA_TRY(launch_pdl(kern, dim3((unsigned)(a.g.B * a.g.S)), dim3(FT), smem, st, a));
+    VCNN_LAUNCHED();
+    return VCNN_OK;
+  };
+  static size_t c4 = 0, c12 = 0;
+  if (a.g.nks <= 4) return go(conv_small_fwd_kernel<4, ACT>, c4);
+  return go(conv_small_fwd_kernel<12, ACT>, c12);
+}
+
+}  // namespace
+
+bool small_fwd_ok(const ConvDesc& d, int pool) {
+  FGeo g;
+  return fplan_small(d, pool, g);
+}
+
+int conv_fwd_small(const ConvDesc& d, const float* x, const float* w, const float* bias, int act,
+                   float* y, const PoolFuse& pf, cudaStream_t st) {
+  FSArgs a{};
+  if (!fplan_small(d, pf.pool, a.g))
+    return fail(VCNN_ESHAPE, "small conv forward: geometry not supported");
+  a.x = x;
+  a.w = w;
+  a.bias = bias;
+  a.y = y;
+  a.py = pf.y;
+  a.parg = pf.arg;
+  switch (act) {
+    case VCNN_ACT_RELU: return launch_small_fwd<VCNN_ACT_RELU>(a, st);
+    case VCNN_ACT_SIGMOID: return launch_small_fwd<VCNN_ACT_SIGMOID>(a, st);
+    case VCNN_ACT_TANH: return launch_small_fwd<VCNN_ACT_TANH>(a, st);
+    default: return launch_small_fwd<VCNN_ACT_IDENTITY>(a, st);
+  }
 }
 
 int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bias, int act,

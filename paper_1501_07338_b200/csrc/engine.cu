@@ -241,7 +241,11 @@ int fused_pool_of(const vcnn_net* n, size_t i, int B) {
   if (i + 2 >= n->L.size()) return 0;  // the layer above applies the conv act' for the pool
   const ConvDesc d = conv_of(l, B);
   const int pz = p.spec.kh;
-  const bool fwd = (l.pf && direct::fwd_ok(d, pz)) || tc::slab_fwd_ok(d, pz);
+  // the small-Kd kernel serves a layer's trace path and its fused path alike
+  // (same accumulation -> bit-identical), or neither
+  if (direct::small_fwd_ok(d, 0) != direct::small_fwd_ok(d, pz)) return 0;
+  const bool fwd = direct::small_fwd_ok(d, pz) || (l.pf && direct::fwd_ok(d, pz)) ||
+                   tc::slab_fwd_ok(d, pz);
   const bool dg = i == 0 || (l.pd && direct::dgrad_ok(d, pz, p.out_h, p.out_w)) ||
                   tc::slab_dgrad_ok(d, pz, p.out_w);
   if (!fwd || !dg || !tc::slab_wgrad_ok(d, pz, p.out_h, p.out_w)) return 0;
@@ -265,10 +269,14 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
     pf.POW = p.out_w;
     pf.y = p.out;
     pf.arg = p.arg;
+    if (direct::small_fwd_ok(d, fpool))
+      return direct::conv_fwd_small(d, in, W, b, l.spec.act, nullptr, pf, st);
     if (l.pf && direct::fwd_ok(d, fpool))
       return direct::conv_fwd(d, in, l.pf, b, l.spec.act, nullptr, pf, st);
     return tc::slab_conv_fwd(d, in, l.wf, b, l.spec.act, nullptr, pf, st);
   }
+  if (n->precision == VCNN_PREC_TF32 && direct::small_fwd_ok(d, 0))
+    return direct::conv_fwd_small(d, in, W, b, l.spec.act, l.out, PoolFuse{}, st);
   if (n->precision == VCNN_PREC_TF32 && l.pf && direct::fwd_ok(d, 0))
     return direct::conv_fwd(d, in, l.pf, b, l.spec.act, l.out, PoolFuse{}, st);
   return launch_conv_fwd(d, in, W, b, l.spec.act, l.out, n->precision, n->ws, st, l.wf);
@@ -732,7 +740,9 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
       const size_t nd = first ? 0 : direct::pack_floats(d1, 1);
       if (nf) s = s ? s : dalloc((void**)&l.pf, sizeof(float) * nf);
       if (nd) s = s ? s : dalloc((void**)&l.pd, sizeof(float) * nd);
-      if (!nf || (!first && !nd)) {
+      // (the small-Kd kernels read the fp32 params directly)
+      const bool small = direct::small_fwd_ok(d1, 0);
+      if ((!nf && !small) || (!first && !nd)) {
         s = s ? s : dalloc((void**)&l.wf, sizeof(float) * tc::prep_floats_f(d1));
         s = s ? s : dalloc((void**)&l.wt, sizeof(float) * tc::prep_floats_t(d1));
       }

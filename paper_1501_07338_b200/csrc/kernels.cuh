@@ -165,6 +165,11 @@ struct PoolFuse {
 // ---- direct (shifted-view) stride-1 conv forward / dgrad (direct.cu, TF32) ----
 namespace direct {
 bool fwd_ok(const ConvDesc& d, int pool);
+// small-Kd forward (C*kh*kw <= 96, K <= 32: first layers), mma.sync TF32,
+// optional fused 2x2 max pool; reads the fp32 weights [K][Kd] directly
+bool small_fwd_ok(const ConvDesc& d, int pool);
+int conv_fwd_small(const ConvDesc& d, const float* x, const float* w, const float* bias, int act,
+                   float* y, const PoolFuse& pf, cudaStream_t st);
 bool dgrad_ok(const ConvDesc& d, int pool = 0, int POH = 0, int POW = 0);
 // prepacked tf32 weights: mode 0 forward, 1 dgrad (0 floats: not supported)
 size_t pack_floats(const ConvDesc& d, int mode);

@@ -463,9 +463,10 @@ template <int MT, int NT>
 __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
   pdl_launch_dependents();
   const SGeo& g = a.g;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) &
-                                             ~static_cast<uintptr_t>(127));
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  // pointer arithmetic on the shared array (not an integer round trip) keeps
+  // the accesses below LDS/STS instead of generic LD/ST
+  uint8_t* smem = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
   __shared__ uint64_t load_bar;
   float* sg = reinterpret_cast<float*>(smem + g.off_g);
   float* sx = reinterpret_cast<float*>(smem + g.off_x);

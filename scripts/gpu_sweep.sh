@@ -25,4 +25,4 @@ all() {
     run sc-c$1-k$2 --config single-conv --channels $1 --ksize $2 --batch 128
   done
 }
-${SWEEP:-all}
+eval "${SWEEP:-all}"
