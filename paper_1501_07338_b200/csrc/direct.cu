@@ -652,9 +652,9 @@ namespace {
 // output of the image is staged in shared memory and written as one
 // contiguous block.  At 2 FLOP/B the layer is HBM/latency-bound; the tcgen05
 // direct kernel pays 5/8 channel padding (C=3 of 8) and a TMEM round trip.
-constexpr int FT = 128;   // 4 warps
+constexpr int FT = 256;   // 8 warps
 constexpr int kTilesPerWarp = 2;
-constexpr int kTilesPerCta = 4 * kTilesPerWarp;
+constexpr int kTilesPerCta = (FT / 32) * kTilesPerWarp;
 struct FGeo {
   int B, C, H, W, K, kh, kw, OH, OW;
   int Kd, nks, nnt;   // columns, K steps (8), N tiles (8 maps)
