@@ -277,6 +277,16 @@ int vcnn_net_train_step(vcnn_net* net, int batch, float lr, float mom);
  * H2D copy, train step, D2H loss; synchronous */
 int vcnn_net_train_step_host(vcnn_net* net, int batch, const float* x, const int* cls,
                              const float* values, float lr, float mom, float* loss_out);
+/* end-to-end training over a stream of HOST batches: step i reads
+ * x + i*x_stride (batch rows) and cls/values + i*t_stride; its loss lands in
+ * losses[i] (host).  The H2D copy of batch i+1 runs on a copy stream while
+ * step i computes (two device staging slots), so the copies overlap the
+ * steps; results equal nsteps calls of vcnn_net_train_step_host.  Host
+ * buffers should be pinned (pageable memory serialises the copies).
+ * Synchronous: returns after the last loss is on the host. */
+int vcnn_net_train_host_stream(vcnn_net* net, int nsteps, int batch, const float* x,
+                               int64_t x_stride, const int* cls, const float* values,
+                               int64_t t_stride, float lr, float mom, float* losses);
 /* Trainer<T>::fit's inner loop for ONE epoch, device-resident
  * (training.hpp:60-88, gather_batch network.hpp:165-176): the dataset
  * (images [count][in], cls [count] or values [count][out]) lives in device

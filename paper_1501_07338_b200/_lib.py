@@ -113,6 +113,8 @@ _SIGS = {
     "vcnn_net_sgd_step": [c_vp, c_float, c_float, c_float],
     "vcnn_net_train_step": [c_vp, c_int, c_float, c_float],
     "vcnn_net_train_step_host": [c_vp, c_int, c_vp, c_vp, c_vp, c_float, c_float, P_float],
+    "vcnn_net_train_host_stream": [c_vp, c_int, c_int, c_vp, C.c_int64, c_vp, c_vp, C.c_int64,
+                                   c_float, c_float, c_vp],
     "vcnn_net_forward_host": [c_vp, c_int, c_vp, c_vp],
     "vcnn_net_enable_graph": [c_vp, c_int],
     "vcnn_net_get_loss": [c_vp, P_float],

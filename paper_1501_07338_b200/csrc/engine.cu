@@ -125,6 +125,17 @@ struct vcnn_net {
   std::vector<GraphEntry> graphs;
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;  // capture needs a non-legacy stream
+  // host-stream training (vcnn_net_train_host_stream): two device staging
+  // slots filled by a copy stream while the previous step computes
+  struct Pipe {
+    cudaStream_t cp = nullptr;
+    cudaEvent_t start = nullptr, copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    float* xs[2] = {nullptr, nullptr};
+    int* cs[2] = {nullptr, nullptr};
+    float* vs[2] = {nullptr, nullptr};
+    float* hl = nullptr;  // pinned per-step losses (a pageable D2H would block the host)
+    int hl_cap = 0;
+  } pipe;
   int g_batch = -1;
   float g_lr = 0, g_mom = 0;
   int kernels_per_step = 0;
@@ -831,6 +842,16 @@ int vcnn_net_destroy(vcnn_net* n) {
   if (n->join_ev) cudaEventDestroy(n->join_ev);
   if (n->side) cudaStreamDestroy(n->side);
   if (n->cap_stream) cudaStreamDestroy(n->cap_stream);
+  for (int k = 0; k < 2; ++k) {
+    cudaFree(n->pipe.xs[k]);
+    cudaFree(n->pipe.cs[k]);
+    cudaFree(n->pipe.vs[k]);
+    if (n->pipe.copied[k]) cudaEventDestroy(n->pipe.copied[k]);
+    if (n->pipe.consumed[k]) cudaEventDestroy(n->pipe.consumed[k]);
+  }
+  if (n->pipe.start) cudaEventDestroy(n->pipe.start);
+  if (n->pipe.hl) cudaFreeHost(n->pipe.hl);
+  if (n->pipe.cp) cudaStreamDestroy(n->pipe.cp);
   for (cudaEvent_t e : n->event_pool) cudaEventDestroy(e);
   delete n;
   return VCNN_OK;
@@ -996,6 +1017,77 @@ int vcnn_net_train_step_host(vcnn_net* n, int batch, const float* x, const int* 
   float l = 0;
   TRY(copy_out(n, &l, n->loss, sizeof(float)));
   if (loss_out) *loss_out = l;
+  return VCNN_OK;
+}
+
+int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* x,
+                               int64_t x_stride, const int* cls, const float* values,
+                               int64_t t_stride, float lr, float mom, float* losses) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (nsteps < 1) return VCNN_OK;
+  TRY(check_batch(n, batch));
+  TRY(check_cfg(lr, mom));
+  const bool ce = n->spec.loss == VCNN_LOSS_SOFTMAX_CE;
+  if (!x || (ce ? !cls : !values)) return fail(VCNN_ESHAPE, "loss: targets required");
+  if (ce)  // the host step's validation (Targets bounds), every batch
+    for (int i = 0; i < nsteps; ++i)
+      for (int b = 0; b < batch; ++b) {
+        const int c = cls[(int64_t)i * t_stride + b];
+        if (c < 0 || c >= n->out_units)
+          return fail(VCNN_EBOUNDS, "loss: class index " + std::to_string(c) +
+                                        " out of range [0," + std::to_string(n->out_units) + ")");
+      }
+  auto& P = n->pipe;
+  if (!P.cp) {
+    VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.cp, cudaStreamNonBlocking));
+    VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) {
+      VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.copied[k], cudaEventDisableTiming));
+      VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.consumed[k], cudaEventDisableTiming));
+      VCNN_CUDA_TRY(cudaMalloc(&P.xs[k], sizeof(float) * n->in_per * n->max_batch));
+      VCNN_CUDA_TRY(cudaMalloc(&P.cs[k], sizeof(int) * n->max_batch));
+      VCNN_CUDA_TRY(cudaMalloc(&P.vs[k], sizeof(float) * n->out_units * n->max_batch));
+    }
+  }
+  if (P.hl_cap < nsteps) {
+    if (P.hl) cudaFreeHost(P.hl);
+    P.hl = nullptr;
+    P.hl_cap = 0;
+    VCNN_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P.hl), sizeof(float) * nsteps,
+                                cudaHostAllocDefault));
+    P.hl_cap = nsteps;
+  }
+  const size_t xb = sizeof(float) * n->in_per * batch;
+  const size_t tb = ce ? sizeof(int) * batch : sizeof(float) * n->out_units * batch;
+  // every copy is ordered after the work already queued on the net's stream
+  VCNN_CUDA_TRY(cudaEventRecord(P.start, n->stream));
+  VCNN_CUDA_TRY(cudaStreamWaitEvent(P.cp, P.start, 0));
+  for (int i = 0; i < nsteps; ++i) {
+    const int k = i & 1;
+    // copy stream: batch i into slot k once step i-2 has taken it over
+    if (i >= 2) VCNN_CUDA_TRY(cudaStreamWaitEvent(P.cp, P.consumed[k], 0));
+    VCNN_CUDA_TRY(cudaMemcpyAsync(P.xs[k], x + (int64_t)i * x_stride, xb,
+                                  cudaMemcpyHostToDevice, P.cp));
+    if (ce)
+      VCNN_CUDA_TRY(cudaMemcpyAsync(P.cs[k], cls + (int64_t)i * t_stride, tb,
+                                    cudaMemcpyHostToDevice, P.cp));
+    else
+      VCNN_CUDA_TRY(cudaMemcpyAsync(P.vs[k], values + (int64_t)i * t_stride, tb,
+                                    cudaMemcpyHostToDevice, P.cp));
+    VCNN_CUDA_TRY(cudaEventRecord(P.copied[k], P.cp));
+    // compute stream: slot k -> the input slots, the step, the loss to host
+    VCNN_CUDA_TRY(cudaStreamWaitEvent(n->stream, P.copied[k], 0));
+    VCNN_CUDA_TRY(cudaMemcpyAsync(n->x, P.xs[k], xb, cudaMemcpyDeviceToDevice, n->stream));
+    VCNN_CUDA_TRY(cudaMemcpyAsync(ce ? (void*)n->cls : (void*)n->values,
+                                  ce ? (void*)P.cs[k] : (void*)P.vs[k], tb,
+                                  cudaMemcpyDeviceToDevice, n->stream));
+    VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
+    TRY(train_step(n, batch, lr, mom));
+    VCNN_CUDA_TRY(cudaMemcpyAsync(P.hl + i, n->loss, sizeof(float), cudaMemcpyDeviceToHost,
+                                  n->stream));
+  }
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  if (losses) std::memcpy(losses, P.hl, sizeof(float) * nsteps);
   return VCNN_OK;
 }
 

@@ -217,6 +217,40 @@ class Network:
                                              C.byref(loss)))
         return loss.value
 
+    def train_host_stream(self, x, cls=None, values=None, lr=0.01, momentum=0.0, steps=None):
+        """End to end over a stream of host batches (vcnn_net_train_host_stream):
+        x is [steps][B][...] (or one batch [B][...] reused for `steps` steps);
+        the H2D copy of each batch overlaps the previous step.  Returns the
+        per-step losses.  Pass pinned torch tensors for overlapped copies."""
+        keep = []
+
+        def prep(a, dt, tdt):
+            if a is None:
+                return None, None
+            if isinstance(a, torch.Tensor):
+                a = a.contiguous() if a.dtype == tdt else a.to(tdt).contiguous()
+                keep.append(a)
+                return a, C.c_void_p(a.data_ptr())
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a, a.ctypes.data_as(C.c_void_p)
+
+        xa, xp = prep(x, np.float32, torch.float32)
+        ca, cp = prep(cls, np.int32, torch.int32)
+        va, vp = prep(values, np.float32, torch.float32)
+        ta = ca if ca is not None else va
+        per_x = self.in_per
+        if steps is None:  # [steps][B][...]
+            steps, B = xa.shape[0], xa.shape[1]
+            xs, ts = B * per_x, ta[0].numel() if isinstance(ta, torch.Tensor) else ta[0].size
+        else:  # one batch, reused
+            B, xs, ts = xa.shape[0], 0, 0
+        losses = np.empty(steps, dtype=np.float32)
+        check(lib().vcnn_net_train_host_stream(self._h, int(steps), int(B), xp, int(xs), cp, vp,
+                                               int(ts), float(lr), float(momentum),
+                                               losses.ctypes.data_as(C.c_void_p)))
+        return losses
+
     def forward_host(self, x):
         x = np.ascontiguousarray(x, dtype=np.float32)
         B = x.shape[0]

@@ -481,3 +481,26 @@ def test_large_mse_loss_multi_cta(prec):
     r = O.net_run_batch(spec, p0, f32(x), values=vals)
     assert abs(l0 - r["loss"]) <= TOL[prec] * max(1.0, abs(r["loss"]))
     assert_close(g0, r["grads"], 5 * TOL[prec], "grads")
+
+
+def test_host_stream_equals_host_steps():
+    """vcnn_net_train_host_stream (H2D of batch i+1 on a copy stream while
+    step i computes) gives bit-identical losses and weights to the same
+    batches fed one synchronous vcnn_net_train_step_host at a time; class
+    bounds are validated like the host step."""
+    spec, B, steps = S.cifar3(), 32, 5
+    x, cls, _ = O.synth_bench_data(spec, B * steps, 8)
+    xs = torch.from_numpy(x.reshape(steps, B, -1)).pin_memory()
+    cs = torch.from_numpy(cls.reshape(steps, B).astype(np.int32)).pin_memory()
+    a, b = Network(spec, B), Network(spec, B)
+    la = a.train_host_stream(xs, cls=cs, lr=0.01, momentum=0.9)
+    lb = np.array([b.train_step_host(x.reshape(steps, B, -1)[i], cls=cls.reshape(steps, B)[i],
+                                     lr=0.01, momentum=0.9) for i in range(steps)], np.float32)
+    assert np.array_equal(la, lb)
+    assert np.array_equal(a.get_params(), b.get_params())
+    bad = cs.clone()
+    bad[3, 7] = 10
+    with pytest.raises(BoundsError):
+        a.train_host_stream(xs, cls=bad, lr=0.01, momentum=0.9)
+    a.close()
+    b.close()
