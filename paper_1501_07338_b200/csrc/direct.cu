@@ -87,10 +87,10 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   if (mode == 0 && g.Cin < 4) return false;
   int R = BM / g.Wg;
   if (R > g.Hout) R = g.Hout;
-  if (pool) {
+  if (pool && mode == 0) {  // the forward epilogue pools whole windows of its tile
     R = (R / pool) * pool;
     if (R < 1) return false;
-  } else {
+  } else {  // (a routed dgrad stages the whole gradient image: any row tiling)
     R = (int)cdiv(g.Hout, cdiv(g.Hout, R));  // balanced row blocks
   }
   g.R = R;
