@@ -90,6 +90,9 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   if (pool && mode == 0) {  // the forward epilogue pools whole windows of its tile
     R = (R / pool) * pool;
     if (R < 1) return false;
+    // balanced: as few tiles as before, window rows spread evenly over them
+    const int nt = (int)cdiv(g.Hout, R);
+    R = pool * (int)cdiv(cdiv(g.Hout, pool), nt);
   } else {  // (a routed dgrad stages the whole gradient image: any row tiling)
     R = (int)cdiv(g.Hout, cdiv(g.Hout, R));  // balanced row blocks
   }
