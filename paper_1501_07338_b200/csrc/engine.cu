@@ -272,6 +272,8 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
   if (conv_is_dense(l))
     return launch_full_fwd(B, (int)l.in_per, l.spec.units, in, W, b, l.spec.act, l.out,
                            n->precision, n->ws, st);
+  if (!fpool && k1::fwd_ok(d))  // K = 1: exact fp32 direct conv (N = 1 GEMM)
+    return k1::conv_fwd(d, in, W, b, l.spec.act, l.out, st);
   if (fpool) {
     LayerRt& p = n->L[i + 1];
     PoolFuse pf;
@@ -412,6 +414,8 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
         if (dense)
           TRY(launch_full_wgrad(B, (int)l.in_per, l.spec.units, in, l.gpre, gW, gB, n->precision,
                                 wsw, sw));
+        else if (!fpool && k1::wgrad_ok(d) && wsw.bytes >= k1::wgrad_workspace(d))
+          TRY(k1::conv_wgrad(d, in, l.gpre, gW, gB, wsw, sw));
         else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_small_ok(d, gs) &&
                  wsw.bytes >= direct::wgrad_small_workspace(d))
           TRY(direct::conv_wgrad_small(d, in, gs, gW, gB, wsw, sw));
@@ -768,6 +772,8 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
         if (dw > need) need = dw;
         const size_t dws = direct::wgrad_small_workspace(conv_of(l, B));
         if (dws > need) need = dws;
+        const size_t dk1 = k1::wgrad_workspace(conv_of(l, B));
+        if (dk1 > need) need = dk1;
       }
       else if (l.spec.kind == VCNN_LAYER_FULL)
         need = full_workspace(B, (int)l.in_per, l.spec.units, VCNN_PREC_TF32);

@@ -203,6 +203,17 @@ int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float
                      const Workspace& ws, cudaStream_t st);
 }  // namespace direct
 
+// ---- single-output-map convolutions (k1.cu, K = 1, exact fp32, any precision) ----
+namespace k1 {
+bool fwd_ok(const ConvDesc& d);
+int conv_fwd(const ConvDesc& d, const float* x, const float* w, const float* bias, int act,
+             float* y, cudaStream_t st);
+bool wgrad_ok(const ConvDesc& d);
+size_t wgrad_workspace(const ConvDesc& d);
+int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
+               const Workspace& ws, cudaStream_t st);
+}  // namespace k1
+
 // ---- tcgen05 implementations (tc.cu) for VCNN_PREC_TF32 / 3XTF32 ----
 namespace tc {
 // Slab kernels (TF32, stride 1): the CTA stages its input window in shared
