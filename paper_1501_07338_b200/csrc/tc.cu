@@ -1416,8 +1416,10 @@ DenseProb dense_prob(int M, int N, int K, const float* a, int64_t as_m, int64_t 
 }
 
 bool explicit_dgrad(const ConvDesc& d) {
-  // implicit dgrad multiplies H*W/(OH*OW) times the algorithmic work
-  return (int64_t)d.H * d.W > 2 * (int64_t)d.OH * d.OW;
+  // implicit dgrad multiplies H*W/(OH*OW) times the algorithmic work; the
+  // explicit one writes and re-reads the kd x pixels dP matrix (1.2 GB for
+  // deconv-121's 1x121 layer: 2.0 ms GEMM + 1.4 ms col2im)
+  return (int64_t)d.H * d.W > 4 * (int64_t)d.OH * d.OW;
 }
 
 Plan plan_conv_fwd(const ConvDesc& d) { return make_plan(d.pixels(), d.K, d.kd(), 1); }
