@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
 // slice s of the block sums images [s*per_s, (s+1)*per_s) for 32 consecutive
 // outputs (loads coalesced, all in flight), then lane-wise over slices in
 // order.  Deterministic; latency is one round of loads, not nimg.
-constexpr int kRedSlices = 8;
+constexpr int kRedSlices = 16;
 __global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
     int nimg, int64_t per, int64_t stride, int64_t nw, const float* __restrict__ part,
     float* __restrict__ dw, float* __restrict__ db) {
