@@ -491,17 +491,24 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
         const int nv = nN - ig * 2 < 2 ? nN - ig * 2 : 2;
         float c[2][4] = {};
         warp_mma<2>(c, G, 1, sH, xr, 1, sK, m0, n0, nv, d.Bp >> 3, lane);
+        // column pairs (2t, 2t+1) are adjacent: one 8-byte store when both
+        // are in range and the address is 8-byte aligned
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const int o = m0 + g + 8 * hf;
           if (o >= h) continue;
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = n0 + j * 8 + 2 * t + e;
-              if (j < nv && col < nc) a.dWH[(size_t)o * in + k0 + col] = c[j][2 * hf + e];
+          for (int j = 0; j < 2; ++j) {
+            const int col = n0 + j * 8 + 2 * t;
+            if (j >= nv || col >= nc) continue;
+            float* p = a.dWH + (size_t)o * in + k0 + col;
+            if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+              *reinterpret_cast<float2*>(p) = make_float2(c[j][2 * hf], c[j][2 * hf + 1]);
+            } else {
+              p[0] = c[j][2 * hf];
+              if (col + 1 < nc) p[1] = c[j][2 * hf + 1];
             }
+          }
         }
       } else {
         const int u = tile - na, im = u / gb, ig = u - im * gb;
@@ -514,17 +521,25 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
           const int b = m0 + g + 8 * hf;
           if (b >= B) continue;
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = n0 + j * 8 + 2 * t + e;
-              if (j < nv && col < nc) {
-                float v = c[j][2 * hf + e];
-                if (a.act_prev != VCNN_ACT_IDENTITY)
-                  v *= actg(a.act_prev, xr[b * sK + col]);
-                a.dx[(size_t)b * in + k0 + col] = v;
-              }
+          for (int j = 0; j < 4; ++j) {
+            const int col = n0 + j * 8 + 2 * t;
+            if (j >= nv || col >= nc) continue;
+            float v0 = c[j][2 * hf], v1 = c[j][2 * hf + 1];
+            if (a.act_prev == VCNN_ACT_RELU) {  // the common case inline
+              v0 *= xr[b * sK + col] > 0.f ? 1.f : 0.f;
+              v1 *= xr[b * sK + col + 1] > 0.f ? 1.f : 0.f;
+            } else if (a.act_prev != VCNN_ACT_IDENTITY) {
+              v0 *= actg(a.act_prev, xr[b * sK + col]);
+              if (col + 1 < nc) v1 *= actg(a.act_prev, xr[b * sK + col + 1]);
             }
+            float* p = a.dx + (size_t)b * in + k0 + col;
+            if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+              *reinterpret_cast<float2*>(p) = make_float2(v0, v1);
+            } else {
+              p[0] = v0;
+              if (col + 1 < nc) p[1] = v1;
+            }
+          }
         }
       }
     }
