@@ -111,8 +111,13 @@ inline bool tiny(int64_t m, int64_t n, int64_t k) { return m * n * k < kTinyGemm
 
 int launch_full_fwd(int B, int in, int out, const float* x, const float* w, const float* b,
                     int act, float* y, int prec, const Workspace& ws, cudaStream_t st) {
-  if (prec == VCNN_PREC_FP32 || tiny(B, out, in))
+  if (prec == VCNN_PREC_FP32 || tiny(B, out, in)) {
+    if (simt::full_fwd_warp_ok(B, in, out, x, w))
+      return simt::full_fwd_mid(B, in, out, x, w, b, act, y, st);
     return simt::full_fwd(B, in, out, x, w, b, act, y, st);
+  }
+  if (simt::full_fwd_warp_ok(B, in, out, x, w))  // exact fp32, no split-K reduce
+    return simt::full_fwd_mid(B, in, out, x, w, b, act, y, st);
   return tc::full_fwd(B, in, out, x, w, b, act, y, prec == VCNN_PREC_3XTF32, ws, st);
 }
 

@@ -130,6 +130,9 @@ int conv_wgrad(const ConvDesc& d, const float* x, const float* gpre, float* dw, 
                cudaStream_t st);
 int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
                const float* yprev, int act_prev, cudaStream_t st);
+bool full_fwd_warp_ok(int B, int in, int out, const float* x, const float* w);
+int full_fwd_mid(int B, int in, int out, const float* x, const float* w, const float* b, int act,
+                 float* y, cudaStream_t st);
 int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
              float* y, cudaStream_t st);
 int full_wgrad(int B, int in, int out, const float* x, const float* gpre, float* dw, float* db,

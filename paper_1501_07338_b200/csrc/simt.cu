@@ -1089,6 +1089,49 @@ int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
   return VCNN_OK;
 }
 
+// mid-size FC forward (in the forward-only chain: CIFAR-3's dense conv3,
+// 128 x 800 -> 64): one warp per output, float4 loads of the x row and the W
+// row strided over the lanes, fixed shuffle-tree reduction (deterministic,
+// exact fp32).  ~3 us where a split-K tensor-core GEMM + reduce takes 16 us.
+__global__ void full_fwd_warp(int B, int in, int out, const float* __restrict__ x,
+                              const float* __restrict__ w, const float* __restrict__ b, int act,
+                              float* __restrict__ y) {
+  PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (wid >= (int64_t)B * out) return;
+  const int o = (int)(wid % out);
+  const int64_t bb = wid / out;
+  const float4* xr = reinterpret_cast<const float4*>(x + bb * in);
+  const float4* wr = reinterpret_cast<const float4*>(w + (int64_t)o * in);
+  float acc = 0.f;
+  for (int k = lane; k < (in >> 2); k += 32) {
+    const float4 a = __ldg(xr + k), c = __ldg(wr + k);
+    acc = fmaf(a.x, c.x, acc);
+    acc = fmaf(a.y, c.y, acc);
+    acc = fmaf(a.z, c.z, acc);
+    acc = fmaf(a.w, c.w, acc);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) y[wid] = act_fwd(act, acc + b[o]);
+}
+
+bool full_fwd_warp_ok(int B, int in, int out, const float* x, const float* w) {
+  const int64_t macs = (int64_t)B * in * out;
+  return in % 4 == 0 && in >= 64 && macs < (int64_t(1) << 24) &&
+         ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(w)) & 15) == 0;
+}
+
+int full_fwd_mid(int B, int in, int out, const float* x, const float* w, const float* b, int act,
+                 float* y, cudaStream_t st) {
+  const int64_t threads = (int64_t)B * out * 32;
+  VCNN_CUDA_TRY(launch_pdl(full_fwd_warp, dim3((unsigned)cdiv(threads, 256)), dim3(256), 0, st, B,
+                           in, out, x, w, b, act, y));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
 int full_fwd(int B, int in, int out, const float* x, const float* w, const float* b, int act,
              float* y, cudaStream_t st) {
   VCNN_CUDA_TRY(launch_pdl(full_fwd_simt, dim3(grid_for((int64_t)B * out)), dim3(kThreads), 0, st, B, in, out, x, w, b, act, y));
