@@ -607,7 +607,8 @@ __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restr
       const int64_t k = i - L.w_off;
       if (k < 0 || k >= L.w_len) continue;
       const int khw = L.kh * L.kw, kd = L.C * khw;
-      const int nn = (int)(k / kd), rem = (int)(k - (int64_t)nn * kd);
+      const int k32 = (int)k;  // w_len < 2^31 (checked on the host): 32-bit divisions
+      const int nn = k32 / kd, rem = k32 - nn * kd;
       const int c = rem / khw, s = rem - c * khw;
       const float q = ptx::to_tf32(wi);
       if (L.pf) L.pf[pack_index(L.gf, nn, c, s)] = q;
@@ -626,6 +627,7 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
     PackLayer& L = t.L[t.n++];
     L.w_off = p.w_off;
     L.w_len = p.d.kd() * p.d.K;
+    if (L.w_len >= (int64_t(1) << 31)) return fail(VCNN_ESHAPE, "sgd_pack: layer too large");
     L.pf = p.pf;
     L.pd = p.pd;
     L.K = p.d.K, L.C = p.d.C, L.kh = p.d.kh, L.kw = p.d.kw;
