@@ -575,6 +575,8 @@ struct PackLayer {
   Geo gf, gd;            // fwd / dgrad pack geometry (BN, CG, nblk, ...)
   float* pf;
   float* pd;
+  float* ps;  // small-Kd forward image [n][wst]
+  int wst;
   int K, C, kh, kw;
 };
 struct PackTable {
@@ -611,6 +613,7 @@ __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restr
       const int nn = k32 / kd, rem = k32 - nn * kd;
       const int c = rem / khw, s = rem - c * khw;
       const float q = ptx::to_tf32(wi);
+      if (L.ps) L.ps[nn * L.wst + rem] = q;
       if (L.pf) L.pf[pack_index(L.gf, nn, c, s)] = q;
       if (L.pd) L.pd[pack_index(L.gd, c, nn, khw - 1 - s)] = q;
     }
@@ -622,7 +625,7 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
              const std::vector<PackSpec>& layers, cudaStream_t st) {
   PackTable t{};
   for (const PackSpec& p : layers) {
-    if (!p.pf && !p.pd) continue;
+    if (!p.pf && !p.pd && !p.ps) continue;
     if (t.n == kMaxPackLayers) return fail(VCNN_ECONFIG, "sgd_pack: too many conv layers");
     PackLayer& L = t.L[t.n++];
     L.w_off = p.w_off;
@@ -630,6 +633,11 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
     if (L.w_len >= (int64_t(1) << 31)) return fail(VCNN_ESHAPE, "sgd_pack: layer too large");
     L.pf = p.pf;
     L.pd = p.pd;
+    L.ps = p.ps;
+    if (p.ps) {
+      L.wst = small_fwd_wst(p.d);
+      if (!L.wst) return fail(VCNN_ESHAPE, "sgd_pack: small plan");
+    }
     L.K = p.d.K, L.C = p.d.C, L.kh = p.d.kh, L.kw = p.d.kw;
     if (p.pf && !plan(p.d, 0, 0, 0, 0, L.gf)) return fail(VCNN_ESHAPE, "sgd_pack: fwd plan");
     if (p.pd && !plan(p.d, 1, 0, 0, 0, L.gd)) return fail(VCNN_ESHAPE, "sgd_pack: dgrad plan");
@@ -709,6 +717,7 @@ bool fplan_small(const ConvDesc& d, int pool, FGeo& g) {
 struct FSArgs {
   FGeo g;
   const float* x;
+  const float* ps;  // prepacked tf32 weight image [nnt*8][wst] (or null: stage from w)
   const float* w;  // [K][Kd] (params, rounded to tf32 when staged)
   const float* bias;
   float* y;        // [B][K][OH][OW] (unpooled)
@@ -754,30 +763,34 @@ __global__ void __launch_bounds__(FT) conv_small_fwd_kernel(const FSArgs a) {
     for (int h = 0; h < 2; ++h) coff[ks][h] = g.jo[ks * 8 + t + 4 * h];
   __syncthreads();
   pdl_wait();
-  if (tid == 0) {
-    const uint32_t xb = 4u * (uint32_t)(g.C * hw);
-    ptx::mbar_expect_tx(&load_bar, xb);
-    ptx::bulk_g2s(ptx::smem_u32(sx), a.x + (int64_t)b * g.C * hw, xb, &load_bar);
-    ptx::mbar_arrive(&load_bar);
-  }
-  // W -> smem [n][wst], tf32, zero padded (rows to nnt*8, columns to KS*8)
   constexpr int wcols = KS * 8;
   const int wrows = g.nnt * 8;
-  // (cp.async: every element's load in flight at once; rounded after the wait)
-  for (int i = tid; i < wrows * wcols; i += FT) {
-    const int n = i / wcols, j = i - n * wcols;
-    if (n < g.K && j < g.Kd)
-      ptx::cp_async4(ptx::smem_u32(sw + n * g.wst + j), a.w + n * g.Kd + j);
-    else
-      sw[n * g.wst + j] = 0.f;
+  if (tid == 0) {
+    const uint32_t xb = 4u * (uint32_t)(g.C * hw);
+    const uint32_t wb = a.ps ? 4u * (uint32_t)(wrows * g.wst) : 0u;
+    ptx::mbar_expect_tx(&load_bar, xb + wb);
+    ptx::bulk_g2s(ptx::smem_u32(sx), a.x + (int64_t)b * g.C * hw, xb, &load_bar);
+    if (a.ps) ptx::bulk_g2s(ptx::smem_u32(sw), a.ps, wb, &load_bar);  // prepacked tf32 image
+    ptx::mbar_arrive(&load_bar);
   }
-  ptx::cp_async_wait_all();
+  if (!a.ps) {
+    // W -> smem [n][wst], tf32, zero padded (rows to nnt*8, columns to KS*8)
+    // (cp.async: every element's load in flight at once; rounded after the wait)
+    for (int i = tid; i < wrows * wcols; i += FT) {
+      const int n = i / wcols, j = i - n * wcols;
+      if (n < g.K && j < g.Kd)
+        ptx::cp_async4(ptx::smem_u32(sw + n * g.wst + j), a.w + n * g.Kd + j);
+      else
+        sw[n * g.wst + j] = 0.f;
+    }
+    ptx::cp_async_wait_all();
+    for (int i = tid; i < wrows * wcols; i += FT) {
+      const int n = i / wcols, j = i - n * wcols;
+      sw[n * g.wst + j] = ptx::to_tf32(sw[n * g.wst + j]);
+    }
+  }
   ptx::mbar_wait(&load_bar, 0);
   for (int i = tid; i < g.C * hw; i += FT) sx[i] = ptx::to_tf32(sx[i]);
-  for (int i = tid; i < wrows * wcols; i += FT) {
-    const int n = i / wcols, j = i - n * wcols;
-    sw[n * g.wst + j] = ptx::to_tf32(sw[n * g.wst + j]);
-  }
   __syncthreads();
 
   const int mbase = sidx * kTilesPerCta;
@@ -935,11 +948,44 @@ bool small_fwd_ok(const ConvDesc& d, int pool) {
   return fplan_small(d, pool, g);
 }
 
+int small_fwd_wst(const ConvDesc& d) {
+  FGeo g;
+  return fplan_small(d, 0, g) ? g.wst : 0;
+}
+
+size_t small_fwd_pack_floats(const ConvDesc& d) {
+  FGeo g;
+  if (!fplan_small(d, 0, g)) return 0;
+  return (size_t)g.nnt * 8 * g.wst;
+}
+
+namespace {
+__global__ void small_pack_kernel(int K, int Kd, int rows, int wst, const float* __restrict__ w,
+                                  float* __restrict__ ps) {
+  PDL_ENTRY();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows * wst; i += gridDim.x * blockDim.x) {
+    const int n = i / wst, j = i - n * wst;
+    ps[i] = (n < K && j < Kd) ? ptx::to_tf32(w[n * Kd + j]) : 0.f;
+  }
+}
+}  // namespace
+
+int small_fwd_pack(const ConvDesc& d, const float* w, float* ps, cudaStream_t st) {
+  FGeo g;
+  if (!fplan_small(d, 0, g)) return fail(VCNN_ESHAPE, "small pack: geometry not supported");
+  const int rows = g.nnt * 8;
+  VCNN_CUDA_TRY(launch_pdl(small_pack_kernel, dim3((unsigned)cdiv(rows * g.wst, 256)), dim3(256), 0,
+                           st, d.K, g.Kd, rows, g.wst, w, ps));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
 int conv_fwd_small(const ConvDesc& d, const float* x, const float* w, const float* bias, int act,
-                   float* y, const PoolFuse& pf, cudaStream_t st) {
+                   float* y, const PoolFuse& pf, cudaStream_t st, const float* ps) {
   FSArgs a{};
   if (!fplan_small(d, pf.pool, a.g))
     return fail(VCNN_ESHAPE, "small conv forward: geometry not supported");
+  a.ps = ps;
   a.x = x;
   a.w = w;
   a.bias = bias;

@@ -43,6 +43,7 @@ struct LayerRt {
   // direct (shifted-view) kernels: prepacked tf32 weights, fwd and dgrad
   float* pf = nullptr;
   float* pd = nullptr;
+  float* ps = nullptr;  // small-Kd forward weight image (tf32, padded)
 };
 
 // host Rng identical to the reference (common.hpp:51-66): mt19937_64 with
@@ -283,13 +284,13 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
     pf.y = p.out;
     pf.arg = p.arg;
     if (direct::small_fwd_ok(d, fpool))
-      return direct::conv_fwd_small(d, in, W, b, l.spec.act, nullptr, pf, st);
+      return direct::conv_fwd_small(d, in, W, b, l.spec.act, nullptr, pf, st, l.ps);
     if (l.pf && direct::fwd_ok(d, fpool))
       return direct::conv_fwd(d, in, l.pf, b, l.spec.act, nullptr, pf, st);
     return tc::slab_conv_fwd(d, in, l.wf, b, l.spec.act, nullptr, pf, st);
   }
   if (n->precision == VCNN_PREC_TF32 && direct::small_fwd_ok(d, 0))
-    return direct::conv_fwd_small(d, in, W, b, l.spec.act, l.out, PoolFuse{}, st);
+    return direct::conv_fwd_small(d, in, W, b, l.spec.act, l.out, PoolFuse{}, st, l.ps);
   if (n->precision == VCNN_PREC_TF32 && l.pf && direct::fwd_ok(d, 0))
     return direct::conv_fwd(d, in, l.pf, b, l.spec.act, l.out, PoolFuse{}, st);
   return launch_conv_fwd(d, in, W, b, l.spec.act, l.out, n->precision, n->ws, st, l.wf);
@@ -483,6 +484,7 @@ int prep_weights(vcnn_net* n) {
     if (l.wf) TRY(tc::prep_weights(d, w, l.wf, l.wt, n->stream));
     if (l.pf) TRY(direct::pack_weights(d, 0, w, l.pf, n->stream));
     if (l.pd) TRY(direct::pack_weights(d, 1, w, l.pd, n->stream));
+    if (l.ps) TRY(direct::small_fwd_pack(d, w, l.ps, n->stream));
   }
   return VCNN_OK;
 }
@@ -494,7 +496,7 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   std::vector<direct::PackSpec> packs;
   bool slab_copies = false;
   for (LayerRt& l : n->L) {
-    if (l.pf || l.pd) packs.push_back({conv_of(l, 1), l.w_off, l.pf, l.pd});
+    if (l.pf || l.pd || l.ps) packs.push_back({conv_of(l, 1), l.w_off, l.pf, l.pd, l.ps});
     slab_copies = slab_copies || l.wf;
   }
   TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
@@ -757,6 +759,8 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
       if (nd) s = s ? s : dalloc((void**)&l.pd, sizeof(float) * nd);
       // (the small-Kd kernels read the fp32 params directly)
       const bool small = direct::small_fwd_ok(d1, 0);
+      const size_t ns = small ? direct::small_fwd_pack_floats(d1) : 0;
+      if (ns) s = s ? s : dalloc((void**)&l.ps, sizeof(float) * ns);
       if ((!nf && !small) || (!first && !nd)) {
         s = s ? s : dalloc((void**)&l.wf, sizeof(float) * tc::prep_floats_f(d1));
         s = s ? s : dalloc((void**)&l.wt, sizeof(float) * tc::prep_floats_t(d1));
@@ -832,6 +836,7 @@ int vcnn_net_destroy(vcnn_net* n) {
     cudaFree(l.wt);
     cudaFree(l.pf);
     cudaFree(l.pd);
+    cudaFree(l.ps);
   }
   cudaFree(n->params);
   cudaFree(n->grads);

@@ -172,7 +172,12 @@ bool fwd_ok(const ConvDesc& d, int pool);
 // optional fused 2x2 max pool; reads the fp32 weights [K][Kd] directly
 bool small_fwd_ok(const ConvDesc& d, int pool);
 int conv_fwd_small(const ConvDesc& d, const float* x, const float* w, const float* bias, int act,
-                   float* y, const PoolFuse& pf, cudaStream_t st);
+                   float* y, const PoolFuse& pf, cudaStream_t st, const float* ps = nullptr);
+// the small forward's weight image: tf32, [nnt*8][wst], zero padded; one TMA
+// bulk copy per CTA when passed as `ps` (kept current by sgd_pack)
+size_t small_fwd_pack_floats(const ConvDesc& d);
+int small_fwd_wst(const ConvDesc& d);  // row stride of that image (0: not supported)
+int small_fwd_pack(const ConvDesc& d, const float* w, float* ps, cudaStream_t st);
 bool dgrad_ok(const ConvDesc& d, int pool = 0, int POH = 0, int POW = 0);
 // prepacked tf32 weights: mode 0 forward, 1 dgrad (0 floats: not supported)
 size_t pack_floats(const ConvDesc& d, int mode);
@@ -188,6 +193,7 @@ struct PackSpec {
   int64_t w_off;
   float* pf;
   float* pd;
+  float* ps = nullptr;  // small-Kd forward image (small_fwd_pack_floats)
 };
 int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st);
