@@ -190,7 +190,7 @@ def cpu_reference(spec, B, steps, warmup, seconds=None):
     return {"value": B * len(times) / total, "unit": "img/s", "cores": cores, "kind": kind,
             "sample": f"{len(times)} steps of batch {B} ({os.path.basename(O.ref_path())}, "
                       f"Executor<float>(imp6).run_batch + sgd_step, OpenMP {cores} threads)",
-            "ms_per_step": 1e3 * total / len(times)}
+            "ms_per_step": 1e3 * total / len(times), "cpu_model": cpu_model()}
 
 
 def make_spec(args):
@@ -198,6 +198,27 @@ def make_spec(args):
     if args.config == "single-conv":
         return S.single_conv(channels=args.channels, k=args.ksize)
     return S.PRESETS[args.config]()
+
+
+def cpu_model():
+    """`lscpu` model name of this host."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def bench_config(args, world):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": workload_name(args), "per_gpu_batch": args.batch,
+            "global_batch": args.batch * world, "parallelism": f"dp{world}",
+            "l2": "inputs > L2: distinct batches cycled from a 256 MiB device pool, D2D "
+                  "staging copy inside each timed step (GPU arm)",
+            "update": f"sgd momentum {args.momentum} lr {args.lr}"}
 
 
 def workload_name(args):
@@ -221,11 +242,11 @@ def run_reference_arm(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (Rng(8) stream, bench.cpp:29-45)",
-            "config": {"workload": workload_name(args), "per_gpu_batch": args.batch,
-                       "global_batch": args.batch, "parallelism": "cpu (reference runs on host)"},
-            "impl": "reference",
+            "config": bench_config(args, world),
+            "impl": "reference", "where": "host CPU, rank 0 only",
             "cpu_baseline": {"value": r["value"], "unit": "img/s", "cores": r["cores"],
-                             "kind": "reference", "sample": r["sample"]},
+                             "kind": "reference", "sample": r["sample"],
+                             "cpu_model": r["cpu_model"]},
             "e2e": {"value": r["value"], "unit": "img/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -240,7 +261,6 @@ def main():
     import torch
     import torch.distributed as dist
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from paper_1501_07338_b200 import _lib, spec as S
     from paper_1501_07338_b200.engine import Network
 
@@ -256,8 +276,7 @@ def main():
     lr, mom = args.lr, args.momentum
 
     # synthetic data: the global batch from one Rng(8) stream, sharded contiguously
-    import oracle_py as O  # data generator only (bench.cpp:29-45 stream)
-    xg, clsg, valsg = O.synth_bench_data(spec, B * world, 8)
+    xg, clsg, valsg = S.synth_bench_data(spec, B * world, 8)
     sl = slice(rank * B, (rank + 1) * B)
     x_host = torch.from_numpy(np.ascontiguousarray(xg[sl]).reshape(B, -1)).pin_memory()
     is_ce = spec.loss == S.LossKind.softmax_ce
@@ -271,7 +290,7 @@ def main():
     # device input pool larger than L2, cycled one batch per step (the D2D
     # staging copy into the net's input slot is inside the timed step)
     nbatch = max(2, -(-POOL_BYTES // (x_host.numel() * 4)))
-    xp, cp, vp = O.synth_bench_data(spec, B * nbatch, 9 + rank)
+    xp, cp, vp = S.synth_bench_data(spec, B * nbatch, 9 + rank)
     pool_x = torch.from_numpy(xp.reshape(nbatch, B, -1)).to(dev)
     pool_t = torch.from_numpy((cp.reshape(nbatch, B) if is_ce else vp.reshape(nbatch, B, -1))).to(dev)
     del xp, cp, vp
@@ -504,7 +523,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(spec, B, 3, 1, seconds=args.cpu_seconds)
         if cpu:
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
 
     if rank == 0:
         kps = net.kernels_per_step()
@@ -514,13 +533,9 @@ def main():
             "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision,
             "data": "synthetic (Rng(8) stream, bench.cpp:29-45); random-init Glorot weights",
-            "config": {"workload": workload_name(args), "per_gpu_batch": B,
-                       "global_batch": B * world, "parallelism": f"dp{world}",
-                       "precision": args.precision, "graph": not args.no_graph,
-                       "l2": f"inputs > L2: {nbatch} distinct batches cycled from a "
-                             f"{nbatch * x_host.numel() * 4 >> 20} MiB device pool, D2D staging "
-                             "copy inside each timed step",
-                       "update": f"sgd momentum {mom} lr {lr}"},
+            "config": bench_config(args, world),
+            "precision": args.precision, "graph": not args.no_graph,
+            "input_pool": f"{nbatch} batches, {nbatch * x_host.numel() * 4 >> 20} MiB",
             "e2e": e2e, "roofline": roof, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "kernels_per_step": kps,
             "clocks": clk.result(),

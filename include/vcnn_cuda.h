@@ -123,6 +123,12 @@ int vcnn_pool_geometry_init(vcnn_pool_geometry* g, int in_h, int in_w, int chann
 /* NetworkSpec::chain (network.hpp:45-67): per-layer (h,w,c), 3 ints each */
 int vcnn_net_spec_chain(const vcnn_net_spec* spec, int* shapes);
 
+/* the reference bench's synthetic batch (bench.cpp:29-45): Rng(seed), X ~
+ * U[0,1) NCHW [batch][C][H][W], then cls[batch] = uniform_int(units) for
+ * softmax-CE or values[batch][units] ~ U[0,1) for MSE (host buffers) */
+int vcnn_synth_bench_data(const vcnn_net_spec* spec, int batch, uint64_t seed, float* x, int* cls,
+                          float* values);
+
 /* ------------------------------------------------------------------------ */
 /* L1 tensor primitives (tensor.hpp)                                         */
 /* ------------------------------------------------------------------------ */
@@ -255,8 +261,13 @@ int vcnn_net_set_params(vcnn_net* net, const float* host);
 int vcnn_net_get_grads(vcnn_net* net, float* host);
 int vcnn_net_get_velocity(vcnn_net* net, float* host);
 int vcnn_net_set_velocity(vcnn_net* net, const float* host);
-/* device pointers of the flat buffers (for collectives: all-reduce grads) */
+/* device pointers of the flat buffers (for collectives: all-reduce grads).
+ * `params` is READ-ONLY for callers unless they call vcnn_net_params_updated
+ * afterwards: the conv kernels read tf32 weight images derived from it. */
 int vcnn_net_device_buffers(vcnn_net* net, float** params, float** grads, float** velocity);
+/* re-derive the conv kernels' weight images after params were written
+ * through the device pointer (stream-ordered) */
+int vcnn_net_params_updated(vcnn_net* net);
 /* device pointers of the input slots (x [max_batch][C][H][W], cls, values) */
 int vcnn_net_input_buffers(vcnn_net* net, float** x, int** cls, float** values);
 /* stage a batch already in device memory (copied, stream-ordered) */

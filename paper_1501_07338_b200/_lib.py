@@ -62,6 +62,7 @@ _SIGS = {
     "vcnn_conv_geometry_init": [C.POINTER(ConvGeometryC)] + [c_int] * 7,
     "vcnn_pool_geometry_init": [C.POINTER(PoolGeometryC)] + [c_int] * 8,
     "vcnn_net_spec_chain": [C.POINTER(NetSpecC), P_int],
+    "vcnn_synth_bench_data": [C.POINTER(NetSpecC), c_int, C.c_uint64, c_vp, c_vp, c_vp],
     "vcnn_matmul": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "vcnn_matmul_transB": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "vcnn_accumulate_by_index": [c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_int, c_vp, c_vp],
@@ -106,6 +107,7 @@ _SIGS = {
     "vcnn_net_get_velocity": [c_vp, c_vp],
     "vcnn_net_set_velocity": [c_vp, c_vp],
     "vcnn_net_device_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
+    "vcnn_net_params_updated": [c_vp],
     "vcnn_net_input_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
     "vcnn_net_set_batch_device": [c_vp, c_int, c_vp, c_vp, c_vp],
     "vcnn_net_forward_backward": [c_vp, c_int],

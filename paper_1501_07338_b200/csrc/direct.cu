@@ -569,7 +569,6 @@ int pack_weights(const ConvDesc& d, int mode, const float* w, float* pk, cudaStr
 
 // ---- fused SGD + weight packing: one launch per update ---------------------
 namespace {
-constexpr int kMaxPackLayers = 8;
 struct PackLayer {
   int64_t w_off, w_len;  // the layer's weight range in the flat params
   Geo gf, gd;            // fwd / dgrad pack geometry (BN, CG, nblk, ...)

@@ -493,14 +493,29 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   Mark m(n, OTHER_B, -1, OP_SGD);
   // one launch: the update + the direct kernels' weight packs; only layers
   // on the slab fallback still need their plain tf32 copies refreshed
+  // (the fused launch carries at most direct::kMaxPackLayers pack tables;
+  // deeper nets repack the remaining layers from the updated params)
   std::vector<direct::PackSpec> packs;
+  std::vector<const LayerRt*> repack;
   bool slab_copies = false;
   for (LayerRt& l : n->L) {
-    if (l.pf || l.pd || l.ps) packs.push_back({conv_of(l, 1), l.w_off, l.pf, l.pd, l.ps});
+    if (l.pf || l.pd || l.ps) {
+      if ((int)packs.size() < direct::kMaxPackLayers)
+        packs.push_back({conv_of(l, 1), l.w_off, l.pf, l.pd, l.ps});
+      else
+        repack.push_back(&l);
+    }
     slab_copies = slab_copies || l.wf;
   }
   TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
                        n->stream));
+  for (const LayerRt* l : repack) {
+    const ConvDesc d = conv_of(*l, 1);
+    const float* w = n->params + l->w_off;
+    if (l->pf) TRY(direct::pack_weights(d, 0, w, l->pf, n->stream));
+    if (l->pd) TRY(direct::pack_weights(d, 1, w, l->pd, n->stream));
+    if (l->ps) TRY(direct::small_fwd_pack(d, w, l->ps, n->stream));
+  }
   if (!slab_copies) return VCNN_OK;
   for (LayerRt& l : n->L)
     if (l.wf) TRY(tc::prep_weights(conv_of(l, 1), n->params + l.w_off, l.wf, l.wt, n->stream));
@@ -651,6 +666,34 @@ int vcnn_net_spec_chain(const vcnn_net_spec* spec, int* shapes) {
       shapes[3 * i + 1] = w;
       shapes[3 * i + 2] = c;
     }
+  }
+  return VCNN_OK;
+}
+
+// the reference bench's synthetic batch (bench.cpp:29-45): one Rng(seed)
+// stream, X ~ U[0,1) in NCHW linear order, then per-sample labels
+// uniform_int(units) (common.hpp:63-66) or MSE targets ~ U[0,1); host only
+int vcnn_synth_bench_data(const vcnn_net_spec* spec, int batch, uint64_t seed, float* x, int* cls,
+                          float* values) {
+  if (!spec || batch < 0 || !x) return fail(VCNN_ESHAPE, "synth_bench_data: bad arguments");
+  std::vector<int> shapes(3 * (size_t)std::max(spec->nlayers, 1));
+  TRY(vcnn_net_spec_chain(spec, shapes.data()));
+  const int L = spec->nlayers;
+  const int64_t units = L ? (int64_t)shapes[3 * (L - 1)] * shapes[3 * (L - 1) + 1] *
+                                shapes[3 * (L - 1) + 2]
+                          : (int64_t)spec->in_h * spec->in_w * spec->in_c;
+  const bool ce = spec->loss == VCNN_LOSS_SOFTMAX_CE;
+  if (ce ? !cls : !values) return fail(VCNN_ESHAPE, "synth_bench_data: null targets");
+  HostRng rng(seed);
+  const int64_t n = (int64_t)spec->in_h * spec->in_w * spec->in_c * batch;
+  for (int64_t i = 0; i < n; ++i) x[i] = (float)rng.uniform();
+  if (ce) {
+    for (int b = 0; b < batch; ++b) {
+      const int64_t k = (int64_t)(rng.uniform() * (double)units);
+      cls[b] = (int)std::min(k, units - 1);
+    }
+  } else {
+    for (int64_t i = 0; i < units * batch; ++i) values[i] = (float)rng.uniform();
   }
   return VCNN_OK;
 }
@@ -935,6 +978,11 @@ int vcnn_net_set_params(vcnn_net* n, const float* host) {
   TRY(copy_in(n, n->params, host, sizeof(float) * n->nparams));
   TRY(prep_weights(n));
   VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  return VCNN_OK;
+}
+int vcnn_net_params_updated(vcnn_net* n) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  TRY(prep_weights(n));
   return VCNN_OK;
 }
 int vcnn_net_get_grads(vcnn_net* n, float* host) {

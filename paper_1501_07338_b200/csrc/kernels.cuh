@@ -187,7 +187,9 @@ int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bi
 int conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* pk, float* dx,
                const float* yprev, int act_prev, cudaStream_t st);
 // sgd_step fused with the refresh of the conv layers' packs (pf / pd may be
-// null); pack padding must already be zero (pack_weights at creation)
+// null); pack padding must already be zero (pack_weights at creation).  At
+// most kMaxPackLayers layers per launch (the table is a kernel argument).
+constexpr int kMaxPackLayers = 8;
 struct PackSpec {
   ConvDesc d;
   int64_t w_off;

@@ -149,11 +149,18 @@ class Network:
 
     def device_tensors(self):
         """(params, grads, velocity) as torch CUDA views (no copy) -- e.g. to
-        all-reduce the gradient buffer in place."""
+        all-reduce the gradient buffer in place.  `params` is read-only unless
+        params_updated() is called after writing it (the conv kernels read
+        tf32 weight images derived from it)."""
         p, g, v = C.c_void_p(), C.c_void_p(), C.c_void_p()
         check(lib().vcnn_net_device_buffers(self._h, C.byref(p), C.byref(g), C.byref(v)))
         mk = lambda q: torch.as_tensor(_DevBuf(q.value, (self.nparams,), "<f4"), device="cuda")
         return mk(p), mk(g), mk(v)
+
+    def params_updated(self):
+        """Re-derive the conv weight images after params were written through
+        device_tensors()[0] (stream-ordered)."""
+        check(lib().vcnn_net_params_updated(self._h))
 
     def grads_tensor(self):
         """The flat gradient buffer (NetGrads order) as a torch CUDA view:
