@@ -368,6 +368,13 @@ class Trainer {
     std::vector<double> epoch_loss;
     std::vector<float> xb, vb;
     std::vector<int> cb;
+    // a non-finite loss stops BEFORE that batch's sgd_step (training.hpp:77-80):
+    // the one-call device step skips its update while the guard is armed
+    check(vcnn_net_set_nonfinite_guard(net.handle(), 1));
+    struct Disarm {
+      vcnn_net* h;
+      ~Disarm() { vcnn_net_set_nonfinite_guard(h, 0); }
+    } disarm{net.handle()};
     for (int e = 0; e < cfg_.epochs; ++e) {
       rng.shuffle(order);
       double sum = 0;

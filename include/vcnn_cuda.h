@@ -311,6 +311,12 @@ int vcnn_net_train_host_stream(vcnn_net* net, int nsteps, int batch, const float
 int vcnn_net_train_epoch(vcnn_net* net, const float* images, const int* cls,
                          const float* values, int count, const int* order, int batch, float lr,
                          float mom, float* losses);
+/* Trainer::fit's non-finite stop (training.hpp:77-80) on the device: while
+ * enabled, a step whose batch loss is non-finite skips its sgd_step, and so
+ * does every later step until the guard is re-armed (this call again), so the
+ * weights stay those the offending batch ran on.  vcnn_net_train_epoch arms
+ * it for its own duration. */
+int vcnn_net_set_nonfinite_guard(vcnn_net* net, int enable);
 /* end-to-end inference: HOST batch in, HOST output out; synchronous */
 int vcnn_net_forward_host(vcnn_net* net, int batch, const float* x, float* out);
 /* CUDA-graph capture of train_step (per batch size); 0 disables */

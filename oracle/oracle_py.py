@@ -263,6 +263,92 @@ def activate(act, x):
     return f(np.asarray(x, dtype=np.float64))
 
 
+# ------------------------------------------- numpy (BLAS f64) restatement
+# The same conv_forward / conv_backward (layers.hpp:139-195) through numpy's
+# f64 GEMM, for the full-size parity checks (BASELINE shapes: 16x16 / 121-tap
+# kernels, 256-channel sweep cells) where the scalar C restatement would take
+# minutes.  Pinned against the C restatement in tests/test_oracle_golden.py.
+def _act_np(act, x):
+    act = int(act)
+    if act == 1:
+        return np.where(x > 0, x, 0.0)
+    if act == 2:
+        return 1.0 / (1.0 + np.exp(-x))
+    if act == 3:
+        return np.tanh(x)
+    return x
+
+
+def _act_grad_np(act, y):
+    act = int(act)
+    if act == 1:
+        return (y > 0).astype(np.float64)
+    if act == 2:
+        return y * (1 - y)
+    if act == 3:
+        return 1 - y * y
+    return np.ones_like(y)
+
+
+def _patches_np(x, kh, kw, s):
+    """im2col (vectorize.hpp:54-79) as rows: [B*OH*OW][C*kh*kw], (c,ky,kx) order."""
+    from numpy.lib.stride_tricks import sliding_window_view
+    v = sliding_window_view(x, (kh, kw), axis=(2, 3))[:, :, ::s, ::s]  # B,C,OH,OW,kh,kw
+    B, Cc, OH, OW = v.shape[:4]
+    return v.transpose(0, 2, 3, 1, 4, 5).reshape(B * OH * OW, Cc * kh * kw), OH, OW
+
+
+def _chunk(x, kh, kw):
+    """images per chunk so one chunk's patch matrix stays under ~256 MB."""
+    B, Cc, H, W = x.shape
+    per = 8 * Cc * kh * kw * H * W
+    return max(1, min(B, (256 << 20) // max(per, 1)))
+
+
+def conv_forward_np(x, w, b, kh, kw, s, act):
+    x = np.asarray(x, dtype=np.float64)
+    B = x.shape[0]
+    K = w.shape[0]
+    wt = np.asarray(w, np.float64).reshape(K, -1).T
+    b = np.asarray(b, np.float64)
+    outs = []
+    cb = _chunk(x, kh, kw)
+    for i in range(0, B, cb):
+        xi = x[i:i + cb]
+        P, OH, OW = _patches_np(xi, kh, kw, s)
+        Z = P @ wt + b
+        outs.append(Z.reshape(xi.shape[0], OH, OW, K).transpose(0, 3, 1, 2))
+    return _act_np(act, np.concatenate(outs))
+
+
+def conv_backward_np(x, w, y, dy, kh, kw, s, act, need_dx=True):
+    """(dW [K][C*kh*kw], db [K], dX or None); dy is the gradient of the
+    post-activation output y (act' taken from y, layers.hpp:39-48)."""
+    x = np.asarray(x, dtype=np.float64)
+    B, Cc, H, W = x.shape
+    K = w.shape[0]
+    w = np.asarray(w, np.float64).reshape(K, -1)
+    G = np.asarray(dy, np.float64) * _act_grad_np(act, np.asarray(y, np.float64))
+    OH, OW = G.shape[2], G.shape[3]
+    dw = np.zeros((K, Cc * kh * kw))
+    db = np.zeros(K)
+    dx = np.zeros_like(x) if need_dx else None
+    cb = _chunk(x, kh, kw)
+    for i in range(0, B, cb):
+        n = min(cb, B - i)
+        Gm = G[i:i + n].transpose(0, 2, 3, 1).reshape(-1, K)
+        P, _, _ = _patches_np(x[i:i + n], kh, kw, s)
+        dw += Gm.T @ P
+        db += Gm.sum(axis=0)
+        if need_dx:
+            dP = (Gm @ w).reshape(n, OH, OW, Cc, kh, kw)
+            for ky in range(kh):
+                for kx in range(kw):
+                    dx[i:i + n, :, ky:ky + s * (OH - 1) + 1:s, kx:kx + s * (OW - 1) + 1:s] += \
+                        dP[:, :, :, :, ky, kx].transpose(0, 3, 1, 2)
+    return dw, db, dx
+
+
 # ---------------------------------------------------------------- network
 def net_num_params(spec):
     return orc().orc_net_num_params(C.byref(make_net(spec)))
@@ -367,6 +453,9 @@ def ref():
                                               C.c_int, C.c_void_p]
         L.ref_synth_bench_data.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_void_p,
                                            C.c_void_p, C.c_void_p]
+        L.ref_fit.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_double, C.c_double, C.c_int, C.c_int,
+                              C.c_uint64, C.c_int, C.c_void_p, C.c_void_p]
         _ref = L
     return _ref
 
@@ -421,6 +510,22 @@ def ref_net_train_steps_f32(spec, params, x, cls, values, lr, mom, steps):
                                        _dp(c), None if v is None else v.ctypes.data, lr, mom,
                                        steps, _dp(losses)), "ref_net_train_steps_f32")
     return p, losses
+
+
+def ref_fit(spec, params, x, cls, values, lr, mom, batch, epochs, seed, f32=False):
+    """The reference's Trainer<T>(cfg).fit + evaluate_accuracy
+    (training.hpp:50-107): (final params, epoch losses, accuracy or None)."""
+    n = make_net(spec)
+    count = x.shape[0]
+    p = np.ascontiguousarray(params, dtype=np.float64).copy()
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    c = np.ascontiguousarray(cls, dtype=np.int32) if cls is not None else None
+    v = np.ascontiguousarray(values, dtype=np.float64) if values is not None else None
+    el = np.empty(epochs)
+    acc = C.c_double(-1.0)
+    _chk(ref().ref_fit(C.byref(n), count, _dp(p), _dp(x), _dp(c), _dp(v), lr, mom, batch,
+                       epochs, seed, int(bool(f32)), _dp(el), C.byref(acc)), "ref_fit")
+    return p, el, (acc.value if cls is not None else None)
 
 
 def ref_save_model(spec, params, path, f32=True):

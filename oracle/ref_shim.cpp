@@ -290,6 +290,59 @@ int ref_net_train_steps_f32(const orc_net* n, int B, float* params, const float*
   }
 }
 
+// Trainer<double>(cfg).fit + evaluate_accuracy (training.hpp:50-107) over a
+// whole dataset: seeded shuffle carried across epochs, smaller last batch,
+// mean epoch loss.  params in/out (flat), epoch_loss[epochs]; accuracy
+// (nullable) = evaluate_accuracy on the same images after training (class
+// targets only).  f32 = 1 runs Trainer<float> (for drift measurements).
+int ref_fit(const orc_net* n, int count, double* params, const double* x, const int* cls,
+            const double* values, double lr, double mom, int batch, int epochs, uint64_t seed,
+            int f32, double* epoch_loss, double* accuracy) {
+  try {
+    NetworkSpec spec = spec_of(n);
+    TrainConfig cfg;
+    cfg.lr = lr;
+    cfg.momentum = mom;
+    cfg.batch = batch;
+    cfg.epochs = epochs;
+    cfg.seed = seed;
+    auto run = [&](auto zero) {
+      using T = decltype(zero);
+      Network<T> net = build_network<T>(spec);
+      const int64_t np = [&] {
+        int64_t c = 0;
+        for (const auto& l : net.layers) {
+          if (const auto* cv = std::get_if<ConvLayer<T>>(&l)) c += cv->weights.data.size() + cv->bias.size();
+          else if (const auto* p = std::get_if<PoolLayer<T>>(&l)) c += p->bias.size();
+          else c += std::get<FullLayer<T>>(l).weights.data.size() + std::get<FullLayer<T>>(l).bias.size();
+        }
+        return c;
+      }();
+      std::vector<T> pt(params, params + np);
+      flat_to_params(net, pt.data());
+      Tensor<T> xs(Shape::hwcn(n->in_h, n->in_w, n->in_c, count));
+      for (size_t i = 0; i < xs.data.size(); ++i) xs.data[i] = static_cast<T>(x[i]);
+      std::vector<T> vt;
+      if (values) {
+        Shape o = spec.output_shape();
+        vt.assign(values, values + (size_t)o.h() * o.w() * o.c() * count);
+      }
+      Targets<T> t = targets_of<T>(spec, count, cls, values ? vt.data() : nullptr);
+      Trainer<T> tr(cfg);
+      TrainStats<T> st = tr.fit(net, xs, t);
+      for (int e = 0; e < epochs; ++e) epoch_loss[e] = static_cast<double>(st.epoch_loss[e]);
+      params_to_flat(net, pt.data());
+      for (int64_t i = 0; i < np; ++i) params[i] = static_cast<double>(pt[i]);
+      if (accuracy && cls)
+        *accuracy = tr.evaluate_accuracy(net, xs, std::vector<int>(cls, cls + count));
+    };
+    if (f32) run(0.0f); else run(0.0);
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+
 // the reference's own ModelFile v1 writer / reader (io.cpp:265-404):
 // parameters (flat, NetGrads order) <-> file, f32 or f64 networks
 int ref_save_model(const orc_net* n, const double* params, int f32, const char* path) {

@@ -108,6 +108,7 @@ _SIGS = {
     "vcnn_net_set_velocity": [c_vp, c_vp],
     "vcnn_net_device_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
     "vcnn_net_params_updated": [c_vp],
+    "vcnn_net_set_nonfinite_guard": [c_vp, c_int],
     "vcnn_net_input_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
     "vcnn_net_set_batch_device": [c_vp, c_int, c_vp, c_vp, c_vp],
     "vcnn_net_forward_backward": [c_vp, c_int],

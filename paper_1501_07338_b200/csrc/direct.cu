@@ -595,8 +595,18 @@ __device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int
 // (fwd: row n, channel c, s = ky*kw+kx; dgrad: row c, channel n, flipped s)
 __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
                                 const float* __restrict__ g, float lr, float mom, float scale,
-                                const PackTable t) {
+                                const PackTable t, const float* __restrict__ loss,
+                                int* __restrict__ guard) {
   PDL_ENTRY();
+  // Trainer::fit's non-finite stop (training.hpp:77-80): while the guard is
+  // armed, a non-finite batch loss skips this update and every later one, so
+  // the weights stay those the offending batch ran on
+  if (guard && guard[0]) {
+    if (guard[1] || !isfinite(*loss)) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) guard[1] = 1;
+      return;
+    }
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float vi = mom * v[i] + scale * g[i];
@@ -621,7 +631,8 @@ __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restr
 }  // namespace
 
 int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
-             const std::vector<PackSpec>& layers, cudaStream_t st) {
+             const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss,
+             int* guard) {
   PackTable t{};
   for (const PackSpec& p : layers) {
     if (!p.pf && !p.pd && !p.ps) continue;
@@ -644,7 +655,7 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
   int64_t blocks = cdiv(n, 256);
   if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
   if (blocks < 1) blocks = 1;
-  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, w, v, g, lr, mom, scale, t));
+  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

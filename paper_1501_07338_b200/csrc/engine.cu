@@ -140,6 +140,7 @@ struct vcnn_net {
   int g_batch = -1;
   float g_lr = 0, g_mom = 0;
   int kernels_per_step = 0;
+  bool guard = false;  // Trainer non-finite stop armed (err[2..3] on the device)
   // breakdown timer
   bool breakdown = false;
   struct MarkRec {
@@ -508,7 +509,7 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
     slab_copies = slab_copies || l.wf;
   }
   TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
-                       n->stream));
+                       n->stream, n->loss, n->err + 2));
   for (const LayerRt* l : repack) {
     const ConvDesc d = conv_of(*l, 1);
     const float* w = n->params + l->w_off;
@@ -609,6 +610,13 @@ int copy_out(vcnn_net* n, void* host, const void* dev, size_t bytes) {
 int copy_in(vcnn_net* n, void* dev, const void* host, size_t bytes) {
   VCNN_CUDA_TRY(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, n->stream));
   VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  return VCNN_OK;
+}
+
+// the device guard word pair {armed, tripped} read by sgd_pack (stream-ordered)
+int write_guard(vcnn_net* n, int armed) {
+  VCNN_CUDA_TRY(cudaMemsetAsync(n->err + 2, 0, 2 * sizeof(int), n->stream));
+  if (armed) VCNN_CUDA_TRY(cudaMemsetAsync(n->err + 2, 0x01, 1, n->stream));
   return VCNN_OK;
 }
 
@@ -980,6 +988,11 @@ int vcnn_net_set_params(vcnn_net* n, const float* host) {
   VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
   return VCNN_OK;
 }
+int vcnn_net_set_nonfinite_guard(vcnn_net* n, int enable) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  n->guard = enable != 0;
+  return write_guard(n, n->guard ? 1 : 0);
+}
 int vcnn_net_params_updated(vcnn_net* n) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
   TRY(prep_weights(n));
@@ -1160,6 +1173,8 @@ int vcnn_net_train_epoch(vcnn_net* n, const float* images, const int* cls, const
   TRY(check_cfg(lr, mom));
   const bool ce = n->spec.loss == VCNN_LOSS_SOFTMAX_CE;
   if (ce ? !cls : !values) return fail(VCNN_ESHAPE, "train_epoch: targets required");
+  // arm the non-finite guard (err[2] armed, err[3] tripped) for this epoch
+  TRY(write_guard(n, 1));
   int bi = 0;
   for (int start = 0; start < count; start += batch, ++bi) {
     const int nb = count - start < batch ? count - start : batch;
@@ -1169,6 +1184,7 @@ int vcnn_net_train_epoch(vcnn_net* n, const float* images, const int* cls, const
     TRY(train_step(n, nb, lr, mom));
     TRY(launch_store_scalar(n->loss, losses + bi, n->stream));
   }
+  TRY(write_guard(n, n->guard ? 1 : 0));
   return VCNN_OK;
 }
 

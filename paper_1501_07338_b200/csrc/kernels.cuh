@@ -197,8 +197,11 @@ struct PackSpec {
   float* pd;
   float* ps = nullptr;  // small-Kd forward image (small_fwd_pack_floats)
 };
+// guard (nullable): int[2] {armed, tripped}; while armed, a non-finite *loss
+// trips it and the update (and every later one) is skipped
 int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
-             const std::vector<PackSpec>& layers, cudaStream_t st);
+             const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss = nullptr,
+             int* guard = nullptr);
 // weight gradient as shifted-view GEMMs (wgrad.cu): dW [K][C][kh][kw] and db
 // [K] (nullable) from x and the (possibly pool-routed) gradient; per-image
 // partials in ws, fixed-order reduce

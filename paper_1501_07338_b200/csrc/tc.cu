@@ -125,7 +125,20 @@ struct TileCfg {
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int NS = SPLIT3 ? 2 : 1;
   static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * NS;
-  static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  // 3xTF32: the main (hi*hi) products rotate over R TMEM accumulators per
+  // K block and the two correction products (hi*lo, lo*hi) go to a separate
+  // one, so no accumulator sees more than 1/R of the main MMAs and the small
+  // terms are never added into a large accumulator (the tensor core's fp32
+  // accumulation truncates; this keeps the fp32-faithful path within 1e-5
+  // at K ~ 3e4).  Slots are summed in a fixed order in the epilogue.
+  static constexpr int R = !SPLIT3 ? 1 : (BN >= 256 ? 1 : BN == 128 ? 3 : 7);
+  static constexpr uint32_t ACC_COLS = BN < 16 ? 16 : BN;
+  static constexpr uint32_t TMEM_NEED = SPLIT3 ? (uint32_t)(R + 1) * ACC_COLS : ACC_COLS;
+  static constexpr uint32_t TMEM_COLS = TMEM_NEED <= 32    ? 32
+                                        : TMEM_NEED <= 64  ? 64
+                                        : TMEM_NEED <= 128 ? 128
+                                        : TMEM_NEED <= 256 ? 256
+                                                           : 512;
   static constexpr int PA = BM * 8 / NT;  // A chunks per thread per stage
   static constexpr int PB = BN * 8 / NT;  // B chunks per thread per stage
 };
@@ -257,12 +270,16 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
         for (int kk = 0; kk < BK / 8; ++kk) {
           const uint64_t ad = ptx::sw128_kmajor_desc(a_addr + kk * 32);
           const uint64_t bd = ptx::sw128_kmajor_desc(b_addr + kk * 32);
-          ptx::mma_tf32(tmem, ad, bd, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
-          if (SPLIT3) {
+          if constexpr (!SPLIT3) {
+            ptx::mma_tf32(tmem, ad, bd, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+          } else {
+            const uint32_t tm = tmem + (uint32_t)((it % C::R) * C::ACC_COLS);
+            const uint32_t tc = tmem + (uint32_t)(C::R * C::ACC_COLS);
             const uint64_t adl = ptx::sw128_kmajor_desc(a_addr + C::A_BYTES + kk * 32);
             const uint64_t bdl = ptx::sw128_kmajor_desc(b_addr + C::B_BYTES + kk * 32);
-            ptx::mma_tf32(tmem, ad, bdl, IDESC, 1u);
-            ptx::mma_tf32(tmem, adl, bd, IDESC, 1u);
+            ptx::mma_tf32(tm, ad, bd, IDESC, (it >= C::R || kk > 0) ? 1u : 0u);
+            ptx::mma_tf32(tc, ad, bdl, IDESC, (it > 0 || kk > 0) ? 1u : 0u);
+            ptx::mma_tf32(tc, adl, bd, IDESC, 1u);
           }
         }
         ptx::mma_commit(&empty_bar[s]);
@@ -373,6 +390,24 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
   // epilogue: warps 0-3, thread owns accumulator row (warp*32 + lane)
   const int m = m0 + (warp & 3) * 32 + lane;
   const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  // 16 accumulator columns of this row (3xTF32: main slots in order, then the
+  // corrections; slots beyond nkb were never written)
+  auto acc16 = [&](int c, uint32_t (&r)[16]) {
+    ptx::tmem_ld16(trow + (uint32_t)c, r);
+    ptx::tmem_wait_ld();
+    if constexpr (SPLIT3) {
+      const int slots = nkb < C::R ? nkb : C::R;
+      for (int j = 1; j <= slots; ++j) {
+        uint32_t q[16];
+        const int col = j < slots ? j * (int)C::ACC_COLS : C::R * (int)C::ACC_COLS;
+        ptx::tmem_ld16(trow + (uint32_t)(col + c), q);
+        ptx::tmem_wait_ld();
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          r[t] = __float_as_uint(__uint_as_float(r[t]) + __uint_as_float(q[t]));
+      }
+    }
+  };
   if constexpr (Prob::SMEM_EPI) {
     // raw accumulators -> shared memory [n][BM] (the stage ring is idle now)
     float* ep = reinterpret_cast<float*>(smem);
@@ -382,8 +417,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         uint32_t r[16];
-        ptx::tmem_ld16(trow + (uint32_t)c, r);
-        ptx::tmem_wait_ld();
+        acc16(c, r);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           ptx::sts_f32(eb + 4u * ((c + j) * BM + row), nkb > 0 ? __uint_as_float(r[j]) : 0.f);
@@ -398,8 +432,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         uint32_t r[16];
-        ptx::tmem_ld16(trow + (uint32_t)c, r);
-        ptx::tmem_wait_ld();
+        acc16(c, r);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int n = n0 + c + j;
@@ -412,8 +445,7 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
 #pragma unroll 1
       for (int c = 0; c < BN; c += 16) {
         uint32_t r[16];
-        ptx::tmem_ld16(trow + (uint32_t)c, r);
-        ptx::tmem_wait_ld();
+        acc16(c, r);
 #pragma unroll
         for (int j = 0; j < 16; ++j)
           p.store(ec, n0 + c + j, nkb > 0 ? __uint_as_float(r[j]) : 0.f);

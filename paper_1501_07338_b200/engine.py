@@ -162,6 +162,11 @@ class Network:
         device_tensors()[0] (stream-ordered)."""
         check(lib().vcnn_net_params_updated(self._h))
 
+    def set_nonfinite_guard(self, on=True):
+        """Trainer::fit's non-finite stop on the device: while on, a step with
+        a non-finite loss skips its update (and all later ones until re-armed)."""
+        check(lib().vcnn_net_set_nonfinite_guard(self._h, int(bool(on))))
+
     def grads_tensor(self):
         """The flat gradient buffer (NetGrads order) as a torch CUDA view:
         the one buffer a data-parallel step all-reduces (dp.DataParallel)."""
@@ -399,8 +404,10 @@ class Trainer:
         """resident=True: the dataset is uploaded once and every epoch runs on
         the device (vcnn_net_train_epoch: permutation from the reference Rng,
         index-gather kernel, graph-replayed steps, one D2H of the epoch's
-        losses).  The non-finite check then happens per epoch (the reference
-        stops after the offending batch, training.hpp:77-80)."""
+        losses).  A non-finite batch loss trips a device guard that skips
+        that batch's update and every later one, so the weights (and the
+        located layer) are those the offending batch ran on, as in the
+        reference (training.hpp:77-80); the error is raised after the epoch."""
         images = np.ascontiguousarray(images, dtype=np.float32)
         count = images.shape[0]
         if count < 1:
@@ -414,6 +421,16 @@ class Trainer:
         epoch_loss = []
         is_ce = net.spec.loss == LossKind.softmax_ce
         tg = np.asarray(targets)
+        # a non-finite batch loss must stop training BEFORE that batch's
+        # sgd_step (training.hpp:77-80); the step runs fwd+bwd+update in one
+        # call, so the device guard skips the update
+        net.set_nonfinite_guard(True)
+        try:
+            return self._fit_host(net, images, tg, count, rng, order, epoch_loss, is_ce)
+        finally:
+            net.set_nonfinite_guard(False)
+
+    def _fit_host(self, net, images, tg, count, rng, order, epoch_loss, is_ce):
         for epoch in range(self.cfg.epochs):
             rng.shuffle(order)
             loss_sum, batches = 0.0, 0

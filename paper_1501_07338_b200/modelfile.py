@@ -89,66 +89,138 @@ def save_model(path: str, spec: NetworkSpec, params, dtype: str = "f32") -> None
     os.replace(tmp, path)
 
 
+def _act(v: int, path: str) -> Activation:
+    """activation_from_u8 (io.cpp): unknown codes are a ParseError."""
+    try:
+        return Activation(v)
+    except ValueError:
+        raise ParseError(f"model '{path}': unknown activation code {v}") from None
+
+
 def load_model(path: str) -> Tuple[NetworkSpec, np.ndarray, str]:
-    """load_model + network_from_model: (spec, flat parameters, dtype)."""
+    """load_model + network_from_model: (spec, flat parameters, dtype), with
+    the reference reader's checks (io.cpp:309-404): magic, version, checksum,
+    plausible input shape / layer and blob counts, layer fields >= 1, known
+    enum codes, ndims <= 4, byte counts matching dims, no truncation, no
+    trailing bytes -- every failure a ParseError."""
     with open(path, "rb") as f:
         b = f.read()
     if b[:4] != b"VCNN":
         raise ParseError(f"model '{path}': bad magic at offset 0 (expected VCNN)")
-    if len(b) < 17:
-        raise ParseError(f"model '{path}': too short")
+    if len(b) < 8:
+        raise ParseError(f"model '{path}': truncated version")
     (version,) = struct.unpack_from("<I", b, 4)
     if version != VERSION:
         raise ParseError(f"model '{path}': unsupported version {version}")
+    if len(b) < 16:
+        raise ParseError(f"model '{path}': too short for checksum")
     body = len(b) - 8
     (stored,) = struct.unpack_from("<Q", b, body)
     if fnv1a(b[:body]) != stored:
         raise ParseError(f"model '{path}': checksum mismatch")
     off = 8
 
-    def take(fmt):
+    def take(fmt, what):
         nonlocal off
+        n = struct.calcsize("<" + fmt)
+        if off + n > body:
+            raise ParseError(f"model '{path}': truncated {what} at offset {off}")
         v = struct.unpack_from("<" + fmt, b, off)
-        off += struct.calcsize("<" + fmt)
-        if off > body:
-            raise ParseError(f"model '{path}': truncated at offset {off}")
+        off += n
         return v
 
-    (dt,) = take("B")
+    (dt,) = take("B", "dtype")
     dtype = "f32" if dt == 0 else "f64"
-    h, w, c, loss, seed, nl = take("IIIBQI")
+    h, w, c = take("III", "input shape")
+    if min(h, w, c) < 1 or max(h, w, c) > (1 << 20):
+        raise ParseError(f"model '{path}': implausible input shape")
+    loss, seed, nl = take("BQI", "header")
+    if nl > 4096:
+        raise ParseError(f"model '{path}': implausible layer count")
     layers = []
     for i in range(nl):
-        (kind,) = take("B")
+        (kind,) = take("B", "layer kind")
         if kind == 0:
-            maps, kh, kw, st, act = take("IIIIB")
-            layers.append(ConvSpec(maps, kh, kw, st, Activation(act)))
+            maps, kh, kw, st = take("IIII", "conv spec")
+            act = _act(take("B", "conv act")[0], path)
+            if min(maps, kh, kw, st) < 1:
+                raise ParseError(f"model '{path}': invalid conv spec in layer {i}")
+            layers.append(ConvSpec(maps, kh, kw, st, act))
         elif kind == 1:
-            ph, pw, st, mode, bias, act = take("IIIBBB")
-            layers.append(PoolSpec(ph, pw, st, PoolMode(mode), bool(bias), Activation(act)))
+            ph, pw, st, mode, bias = take("IIIBB", "pool spec")
+            if mode > 1:
+                raise ParseError(f"model '{path}': unknown pool mode")
+            act = _act(take("B", "pool act")[0], path)
+            if min(ph, pw, st) < 1:
+                raise ParseError(f"model '{path}': invalid pool spec in layer {i}")
+            layers.append(PoolSpec(ph, pw, st, PoolMode(mode), bool(bias), act))
         elif kind == 2:
-            units, act = take("IB")
-            layers.append(FullSpec(units, Activation(act)))
+            (units,) = take("I", "full units")
+            act = _act(take("B", "full act")[0], path)
+            if units < 1:
+                raise ParseError(f"model '{path}': invalid full spec in layer {i}")
+            layers.append(FullSpec(units, act))
         else:
-            raise ParseError(f"model '{path}': unknown layer kind {kind}")
+            raise ParseError(f"model '{path}': unknown layer kind {kind} at offset {off - 1}")
     spec = NetworkSpec((h, w, c), layers, LossKind.softmax_ce if loss == 0 else LossKind.mse,
                        seed)
-    (nb,) = take("I")
-    parts = []
-    for s in _blob_shapes(spec)[:nb] if nb == len(_blob_shapes(spec)) else []:
-        bdt, nd = take("BI")
-        dims = take("I" * nd)
-        (nbytes,) = take("Q")
+    (nb,) = take("I", "blob count")
+    if nb > 8192:
+        raise ParseError(f"model '{path}': implausible blob count")
+    blobs = []
+    for _ in range(nb):
+        bdt, nd = take("BI", "blob header")
+        if nd > 4:
+            raise ParseError(f"model '{path}': blob with {nd} dims")
+        dims = take("I" * nd, "blob dims")
+        numel = int(np.prod(dims, dtype=np.uint64)) if nd else 1
+        if numel > (1 << 36):
+            raise ParseError(f"model '{path}': blob dimension overflow")
+        (nbytes,) = take("Q", "blob size")
         width = 4 if bdt == 0 else 8
-        if tuple(dims) != tuple(s) or nbytes != int(np.prod(dims)) * width:
-            raise ParseError(f"model '{path}': blob shape {dims} does not match the spec {s}")
-        parts.append(np.frombuffer(b, np.float32 if bdt == 0 else np.float64,
-                                   int(np.prod(dims)), off))
+        if nbytes != numel * width:
+            raise ParseError(f"model '{path}': blob byte count {nbytes} does not match dims "
+                             f"at offset {off - 8}")
+        if off + nbytes > body:
+            raise ParseError(f"model '{path}': truncated blob payload at offset {off}")
+        blobs.append((tuple(dims), np.frombuffer(b, np.float32 if bdt == 0 else np.float64,
+                                                 numel, off)))
         off += nbytes
-    if nb != len(_blob_shapes(spec)):
-        raise ParseError(f"model '{path}': {nb} parameter blobs, the spec needs "
-                         f"{len(_blob_shapes(spec))}")
     if off != body:
-        raise ParseError(f"model '{path}': {body - off} unexpected trailing bytes")
-    flat = np.concatenate(parts) if parts else np.zeros(0, np.float32)
+        raise ParseError(f"model '{path}': {body - off} unexpected trailing bytes at offset {off}")
+    try:
+        want = _blob_shapes(spec)
+    except Exception as e:  # chain validation (network_from_model -> build_network)
+        raise ParseError(f"model '{path}': {e}") from None
+    if len(blobs) != len(want):
+        raise ParseError(f"model '{path}': {len(blobs)} parameter blobs, the spec needs "
+                         f"{len(want)}")
+    for (dims, _), s in zip(blobs, want):
+        if dims != tuple(s):
+            raise ParseError(f"model '{path}': blob shape {dims} does not match the spec {s}")
+    flat = np.concatenate([a for _, a in blobs]) if blobs else np.zeros(0, np.float32)
     return spec, flat, dtype
+
+
+# ---- exact-resume checkpoints (SURVEY 8f row 4) ----------------------------
+# The reference keeps Velocity outside the model file (network.hpp:237-240;
+# Trainer restarts it at zero).  A checkpoint is the reference-readable model
+# file plus a sibling "<path>.vel" in the same v1 format whose blobs are the
+# velocity in NetGrads order, so momentum SGD resumes bit-exactly and the
+# model file itself stays loadable by the reference.
+def save_checkpoint(path: str, spec: NetworkSpec, params, velocity) -> None:
+    save_model(path, spec, params)
+    save_model(path + ".vel", spec, velocity)
+
+
+def load_checkpoint(path: str) -> Tuple[NetworkSpec, np.ndarray, np.ndarray]:
+    """(spec, params, velocity); velocity is zero (the reference's lazy
+    Velocity, network.hpp:247-252) when the model has no .vel sibling."""
+    spec, params, _ = load_model(path)
+    vpath = path + ".vel"
+    if not os.path.exists(vpath):
+        return spec, params, np.zeros_like(params)
+    vspec, vel, _ = load_model(vpath)
+    if _blob_shapes(vspec) != _blob_shapes(spec):
+        raise ParseError(f"checkpoint '{path}': velocity file does not match the model")
+    return spec, params, vel

@@ -18,6 +18,7 @@ from paper_1501_07338_b200.errors import BoundsError, ShapeError, TrainingError
 from paper_1501_07338_b200.spec import Precision
 
 from .util import ALL_PREC, TOL, TOL_STEPS, act_grad_np, act_np, assert_close, ref_f32_drift, f32, normwise
+from .util import assert_close as _assert_close
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
@@ -42,11 +43,22 @@ def _fixture_nets():
     return small_nets()
 
 
-def teacher_forced(net, spec, x, B, tol):
+def teacher_forced(net, spec, x, B, tol, pool_bwd_mode=0, numpy_conv=False):
     """Per-layer parity of one forward_backward pass with every layer fed the
     GPU's own trace (input activations, pre-activation gradients, argmax):
-    isolates kernel numerics from TF32 decision flips.  Checks each layer's
-    output, dW, db and the gradient it hands to the layer below."""
+    isolates kernel numerics from decision flips (TF32 rounding of near-tied
+    max-pool argmaxes / ReLU kinks).  Checks each layer's output, dW, db and
+    the gradient it hands to the layer below, all at `tol` (normwise).
+    numpy_conv: conv layers checked with the BLAS-f64 restatement
+    (oracle_py.conv_*_np, pinned to the C oracle) -- the full-size shapes."""
+    worst = 0.0
+
+    def assert_close(a, b, t, what):  # noqa: F811 -- records the worst error
+        nonlocal worst
+        worst = max(worst, _assert_close(a, b, t, what))
+
+    cf = O.conv_forward_np if numpy_conv else O.conv_forward
+    cb = O.conv_backward_np if numpy_conv else O.conv_backward
     chain = spec.chain()
     h, w, c = spec.input
     params = net.get_params().astype(np.float64)
@@ -61,11 +73,11 @@ def teacher_forced(net, spec, x, B, tol):
         dx = None
         if isinstance(L, S.ConvSpec):
             Wm = Wt.reshape(L.maps, -1)
-            yr = O.conv_forward(a_prev, Wm, bb, L.kh, L.kw, L.stride, int(L.act))
+            yr = cf(a_prev, Wm, bb, L.kh, L.kw, L.stride, int(L.act))
             assert_close(y, yr, tol, f"layer {i} conv out")
-            dw, db, dx = O.conv_backward(a_prev, Wm, y, G, L.kh, L.kw, L.stride, 0, need_dx=i > 0)
-            assert_close(gW, dw, 2 * tol, f"layer {i} conv dW")
-            assert_close(gb, db, 2 * tol, f"layer {i} conv db")
+            dw, db, dx = cb(a_prev, Wm, y, G, L.kh, L.kw, L.stride, 0, need_dx=i > 0)
+            assert_close(gW, dw, tol, f"layer {i} conv dW")
+            assert_close(gb, db, tol, f"layer {i} conv db")
         elif isinstance(L, S.PoolSpec):
             pr, arg = O.pool_forward(a_prev, L.ph, L.pw, L.stride, int(L.mode))
             if L.mode == S.PoolMode.max:
@@ -73,25 +85,26 @@ def teacher_forced(net, spec, x, B, tol):
                     f"layer {i} argmax (same input) not bit-exact"
             if L.bias:
                 pr = pr + bb.reshape(1, -1, 1, 1)
-                assert_close(gb, G.sum(axis=(0, 2, 3)), 2 * tol, f"layer {i} pool db")
+                assert_close(gb, G.sum(axis=(0, 2, 3)), tol, f"layer {i} pool db")
             assert_close(y, act_np(L.act, pr), tol, f"layer {i} pool out")
             if i > 0:
                 dx = O.pool_backward(G, arg if L.mode == S.PoolMode.max else None, a_prev.shape,
-                                     L.ph, L.pw, L.stride, int(L.mode))
+                                     L.ph, L.pw, L.stride, int(L.mode), pool_bwd_mode)
         else:
             Wm = Wt.reshape(L.units, -1)
             yr = O.full_forward(a_prev.reshape(B, -1), Wm, bb, int(L.act))
             assert_close(y.reshape(B, -1), yr, tol, f"layer {i} fc out")
             dw, db, dx = O.full_backward(a_prev.reshape(B, -1), Wm, y.reshape(B, -1),
                                          G.reshape(B, -1), 0, need_dx=i > 0)
-            assert_close(gW, dw, 2 * tol, f"layer {i} fc dW")
-            assert_close(gb, db, 2 * tol, f"layer {i} fc db")
+            assert_close(gW, dw, tol, f"layer {i} fc dW")
+            assert_close(gb, db, tol, f"layer {i} fc db")
         if i > 0:
             prev = spec.layers[i - 1]
             gprev_ref = dx.reshape(a_prev.shape) * act_grad_np(prev.act, a_prev)
             gprev = net.layer_grad(i - 1, B).astype(np.float64).reshape(a_prev.shape)
-            assert_close(gprev, gprev_ref, 2 * tol, f"layer {i} -> {i - 1} gradient")
+            assert_close(gprev, gprev_ref, tol, f"layer {i} -> {i - 1} gradient")
         a_prev = y
+    return worst
 
 
 def test_init_bit_exact_vs_reference():
@@ -127,18 +140,19 @@ def test_net_vs_reference_fixture(path, prec):
             gw, gb = net.layer_params(g, i)
             rw, rb = net.layer_params(d["grads"], i)
             if rw.size:
-                assert_close(gw, rw, 5 * tol, f"layer {i} dW")
+                assert_close(gw, rw, tol, f"layer {i} dW")
             if rb.size and np.abs(rb).max() > 1e-7:
-                assert_close(gb, rb, 5 * tol, f"layer {i} db")
+                assert_close(gb, rb, tol, f"layer {i} db")
     else:
         teacher_forced(net, spec, x, B, tol)
-    # paper_nn pool backward mode (Executor::set_pool_backward_mode)
+    # paper_nn pool backward mode (Executor::set_pool_backward_mode):
+    # whole gradient vs the reference (fp32-faithful modes) and per layer,
+    # teacher-forced, in every mode
     net.set_pool_backward_mode(S.PoolBackwardMode.paper_nn)
     net.forward_backward(B)
     if strict:
-        assert_close(net.get_grads(), d["grads_paper_nn"], 5 * tol, "paper_nn grads")
-    else:
-        assert normwise(net.get_grads(), d["grads_paper_nn"]) < 0.3
+        assert_close(net.get_grads(), d["grads_paper_nn"], tol, "paper_nn grads")
+    teacher_forced(net, spec, x, B, tol, pool_bwd_mode=1)
     net.set_pool_backward_mode(S.PoolBackwardMode.exact)
     # N steps on the production path (fusion on), weights after
     net.set_trace(False)
@@ -151,7 +165,7 @@ def test_net_vs_reference_fixture(path, prec):
                                   float(d["lr"]), float(d["mom"]), int(d["steps"]))
     assert_close(p, d["params_after"], max(TOL_STEPS[prec], 2 * drift), "weights after N steps")
     if strict:
-        assert_close(p - p0, d["params_after"] - p0, max(20 * tol, 2 * udrift),
+        assert_close(p - p0, d["params_after"] - p0, max(tol, 2 * udrift),
                      "update after N steps")
     net.close()
 
@@ -194,7 +208,7 @@ def test_net_vs_oracle_10_steps(name, prec):
         off += n
     assert abs(net.loss() - r["loss"]) <= tol * max(1.0, abs(r["loss"]))
     if strict:
-        assert_close(net.get_grads(), r["grads"], 5 * tol, "grads")
+        assert_close(net.get_grads(), r["grads"], tol, "grads")
     teacher_forced(net, spec, x, B, tol)
     # 10 steps on the production path (fusion on)
     net.set_trace(False)
@@ -209,7 +223,7 @@ def test_net_vs_oracle_10_steps(name, prec):
                                   0.01, 0.9, 10)
     assert_close(pg, p, max(TOL_STEPS[prec], 2 * drift), "weights after 10 steps")
     if strict:
-        assert_close(pg - p0, p - p0, max(20 * tol, 2 * udrift), "update after 10 steps")
+        assert_close(pg - p0, p - p0, max(tol, 2 * udrift), "update after 10 steps")
     else:  # TF32: decision flips allowed, the update direction must agree
         du, dr = (pg - p0).ravel(), (p - p0).ravel()
         assert float(du @ dr) / (np.linalg.norm(du) * np.linalg.norm(dr)) > 0.98
@@ -362,7 +376,7 @@ def test_full_size_step_vs_oracle(name, B):
     teacher_forced(net, spec, x, B, TOL[Precision.tf32])
     net.set_precision(Precision.tf32x3)
     net.forward_backward(B)
-    assert normwise(net.get_grads(), r["grads"]) <= 5 * TOL[Precision.tf32x3]
+    assert normwise(net.get_grads(), r["grads"]) <= TOL[Precision.tf32x3]
     net.close()
 
 
@@ -480,7 +494,7 @@ def test_large_mse_loss_multi_cta(prec):
     assert l0 == l1 and np.array_equal(g0, g1)
     r = O.net_run_batch(spec, p0, f32(x), values=vals)
     assert abs(l0 - r["loss"]) <= TOL[prec] * max(1.0, abs(r["loss"]))
-    assert_close(g0, r["grads"], 5 * TOL[prec], "grads")
+    assert_close(g0, r["grads"], TOL[prec], "grads")
 
 
 def test_host_stream_equals_host_steps():

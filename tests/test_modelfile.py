@@ -67,3 +67,58 @@ def test_corruption_is_rejected(tmp_path):
     open(f, "wb").write(b"XXXX" + bytes(b[4:]))
     with pytest.raises(ParseError, match="magic"):
         load_model(f)
+
+
+def _patched(raw: bytes, off: int, new: bytes) -> bytes:
+    """raw with bytes at `off` replaced and the FNV-1a trailer recomputed."""
+    import struct
+
+    from paper_1501_07338_b200.modelfile import fnv1a
+    b = bytearray(raw[:-8])
+    b[off:off + len(new)] = new
+    return bytes(b) + struct.pack("<Q", fnv1a(bytes(b)))
+
+
+def test_malformed_fields_raise_parse_error(tmp_path):
+    """The reference reader's validation (io.cpp:330-390) with a VALID
+    checksum: every malformed field is a ParseError, never ValueError."""
+    import struct
+    spec = SPECS["mixed"]
+    f = str(tmp_path / "m.vcnn")
+    save_model(f, spec, np.zeros(O.net_num_params(spec), dtype=np.float32))
+    raw = open(f, "rb").read()
+    # header: magic 4 | ver 4 | dtype 1 | h w c 12 | loss 1 | seed 8 | nl 4 -> 34
+    L0 = 34  # first layer: kind 1 | maps kh kw stride 16 | act 1
+    cases = {
+        "implausible input shape": (9, struct.pack("<I", 0)),
+        "implausible layer count": (30, struct.pack("<I", 5000)),
+        "invalid conv spec": (L0 + 1, struct.pack("<I", 0)),
+        "unknown activation": (L0 + 17, b"\x09"),
+        "unknown layer kind": (L0, b"\x07"),
+    }
+    for msg, (off, new) in cases.items():
+        open(f, "wb").write(_patched(raw, off, new))
+        with pytest.raises(ParseError, match=msg):
+            load_model(f)
+    # truncated payload (last blob cut, checksum recomputed)
+    body = raw[:-8]
+    from paper_1501_07338_b200.modelfile import fnv1a
+    cut = body[:-3]
+    open(f, "wb").write(cut + struct.pack("<Q", fnv1a(cut)))
+    with pytest.raises(ParseError):
+        load_model(f)
+
+
+def test_checkpoint_roundtrip_keeps_velocity(tmp_path):
+    from paper_1501_07338_b200.modelfile import load_checkpoint, save_checkpoint
+    spec = SPECS["cifar3"]
+    n = O.net_num_params(spec)
+    rng = np.random.default_rng(4)
+    p, v = rng.standard_normal(n).astype(np.float32), rng.standard_normal(n).astype(np.float32)
+    f = str(tmp_path / "ck.vcnn")
+    save_checkpoint(f, spec, p, v)
+    spec2, p2, v2 = load_checkpoint(f)
+    assert spec2 == spec and np.array_equal(p2, p) and np.array_equal(v2, v)
+    os.remove(f + ".vel")
+    _, _, v3 = load_checkpoint(f)
+    assert not v3.any()

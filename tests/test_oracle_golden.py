@@ -353,3 +353,54 @@ def test_oracle_vs_live_reference_random_nets():
             assert np.abs(a["out"] - b["out"]).max() <= 1e-12
             assert abs(a["loss"] - b["loss"]) <= 1e-12
             assert np.abs(a["grads"] - b["grads"]).max() <= 1e-12 * max(1, np.abs(b["grads"]).max())
+
+
+def test_numpy_conv_restatement_equals_c_oracle():
+    """oracle_py.conv_*_np (BLAS f64, used for the full-size GPU parity
+    checks) == the C restatement on 30 random geometries (incl. stride)."""
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        B, Cc = int(rng.integers(1, 4)), int(rng.integers(1, 5))
+        kh, kw, s = int(rng.integers(1, 5)), int(rng.integers(1, 5)), int(rng.integers(1, 3))
+        Hh, W = kh + int(rng.integers(0, 7)), kw + int(rng.integers(0, 7))
+        K, act = int(rng.integers(1, 6)), int(rng.integers(0, 4))
+        x = rng.uniform(-1, 1, (B, Cc, Hh, W))
+        w = rng.uniform(-1, 1, (K, Cc * kh * kw))
+        b = rng.uniform(-1, 1, K)
+        y = O.conv_forward(x, w, b, kh, kw, s, act)
+        assert np.abs(O.conv_forward_np(x, w, b, kh, kw, s, act) - y).max() <= 1e-12
+        dy = rng.uniform(-1, 1, y.shape)
+        ref = O.conv_backward(x, w, y, dy, kh, kw, s, act)
+        got = O.conv_backward_np(x, w, y, dy, kh, kw, s, act)
+        for a, r in zip(got, ref):
+            assert np.abs(a - r).max() <= 1e-12 * max(1.0, np.abs(r).max())
+
+
+@pytest.mark.skipif(O.ref() is None, reason="oracle/_ref not built (reference sources absent)")
+def test_ref_fit_equals_restated_loop():
+    """The reference's Trainer<double>::fit (ref_fit, training.hpp:60-88) ==
+    the restated loop: Rng(seed) shuffle carried across epochs, smaller last
+    batch, run_batch + sgd_step per batch, mean epoch loss."""
+    spec = S.NetworkSpec((8, 8, 1), [S.ConvSpec(3, 3, 3, 1, A.relu), S.PoolSpec(2, 2, 2),
+                                     S.FullSpec(4, A.identity)], S.LossKind.softmax_ce, 3)
+    n, batch, epochs, seed = 11, 4, 3, 9
+    rng = np.random.default_rng(2)
+    x = rng.uniform(0, 1, (n, 1, 8, 8))
+    cls = rng.integers(0, 4, n).astype(np.int32)
+    p0 = O.net_init(spec)
+    pr, el, acc = O.ref_fit(spec, p0, x, cls, None, 0.05, 0.9, batch, epochs, seed)
+    p, v = p0.copy(), np.zeros_like(p0)
+    r, order, losses = S.Rng(seed), list(range(n)), []
+    for _ in range(epochs):
+        r.shuffle(order)
+        tot, nb = 0.0, 0
+        for st in range(0, n, batch):
+            ids = order[st:st + batch]
+            res = O.net_run_batch(spec, p, x[ids], cls=cls[ids])
+            O.sgd_step(p, v, res["grads"], 0.05, 0.9)
+            tot += res["loss"]
+            nb += 1
+        losses.append(tot / nb)
+    assert np.abs(pr - p).max() <= 1e-12 and np.abs(el - losses).max() <= 1e-12
+    out = O.net_run_batch(spec, p, x, grads=False)["out"]
+    assert acc == np.mean(np.argmax(out, axis=1) == cls)
