@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-infer", action="store_true", help="skip the forward-only pass")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--details", default="", help="write per-op timing JSON here")
+    ap.add_argument("--no-roofline-run", action="store_true",
+                    help="skip the CIFAR-3 b=1024 conv-GEMM roofline pass")
+    ap.add_argument("--no-faithful", action="store_true", help="skip the 3xTF32 pass")
     return ap.parse_args()
 
 
@@ -88,6 +91,69 @@ def op_work(spec, B):
     units = spec.output_units()
     work[(len(spec.layers) - 1, "loss")] = (0.0, 4.0 * (2 * B * units + B))
     return work
+
+
+def op_timing(net, spec, B, steps, load, lr, mom, pk):
+    """Eager steps with CUDA events around every op (breakdown mode): rows
+    per (layer, op) with algorithmic work and rates, sorted by share."""
+    from paper_1501_07338_b200 import spec as S
+    net.enable_graph(False)
+    net.enable_breakdown(True)
+    for i in range(steps):
+        load(i)
+        net.train_step(B, lr, mom)
+    ops = net.read_op_timing()
+    bd = net.read_breakdown()
+    net.enable_breakdown(False)
+    work = op_work(spec, B)
+    # the fused tail kernel (launch_mlp_head / launch_head) is timed as the
+    # loss op: give it the work of every conv / full layer above the last
+    # separately timed one (their forward, both gradients and the loss)
+    timed = [l for (l, o) in ops if o != "loss" and l >= 0]
+    last = max(timed) if timed else -1
+    nl = len(spec.layers)
+    tail = [i for i in range(last + 1, nl) if not isinstance(spec.layers[i], S.PoolSpec)]
+    tail_name = None
+    if (nl - 1, "loss") in ops and tail:
+        f = sum(work.get((i, o), (0.0, 0.0))[0] for i in tail for o in ("fwd", "wgrad", "dgrad"))
+        by = sum(work.get((i, o), (0.0, 0.0))[1] for i in tail for o in ("fwd", "wgrad", "dgrad"))
+        lf, lb = work[(nl - 1, "loss")]
+        work[(nl - 1, "loss")] = (f + lf, by + lb)
+        tail_name = f"tail(layers {tail[0]}-{tail[-1]} fwd+bwd+loss, one kernel)"
+    rows = []
+    tot = sum(s for s, _ in ops.values())
+    for (layer, op), (sec, cnt) in ops.items():
+        f, by = work.get((layer, op), (0.0, 0.0))
+        t = sec / cnt
+        t_tc = f / (pk["tf32_tflops"] * 1e12) if f else 0.0
+        t_hbm = by / (pk["hbm_gbs"] * 1e9) if by else 0.0
+        bound = "tensor" if t_tc >= t_hbm else "hbm"
+        rows.append({"layer": layer, "op": op, "us": t * 1e6, "share": sec / tot,
+                     "flops": f, "bytes": by, "bound": bound,
+                     "tflops": f / t / 1e12 if f else 0.0, "gbs": by / t / 1e9 if by else 0.0,
+                     "roof_us": max(t_tc, t_hbm) * 1e6})
+    rows.sort(key=lambda r: -r["share"])
+    return rows, bd, tail_name, tot
+
+
+def conv_gemm_rows(rows, spec, pk):
+    """Per conv GEMM (separately timed fwd / wgrad / dgrad of a conv layer):
+    achieved TFLOP/s vs the TF32 peak and vs its own roofline
+    min(P_tf32, AI * BW_HBM) with AI from the minimal algorithmic bytes."""
+    from paper_1501_07338_b200 import spec as S
+    out = []
+    for r in rows:
+        if r["layer"] < 0 or r["op"] not in ("fwd", "wgrad", "dgrad") or not r["flops"]:
+            continue
+        if not isinstance(spec.layers[r["layer"]], S.ConvSpec):
+            continue
+        roof = min(pk["tf32_tflops"], r["flops"] / r["bytes"] * pk["hbm_gbs"] * 1e9 / 1e12)
+        out.append({"gemm": f"layer{r['layer']}.{r['op']}", "us": round(r["us"], 2),
+                    "tflops": round(r["tflops"], 2),
+                    "frac_of_peak": round(r["tflops"] / pk["tf32_tflops"], 4),
+                    "roof_tflops": round(roof, 1), "frac_of_roof": round(r["tflops"] / roof, 4),
+                    "bound": r["bound"]})
+    return sorted(out, key=lambda g: g["gemm"])
 
 
 def peaks():
@@ -303,42 +369,23 @@ def main():
             net.load_batch(pool_x[j], values=pool_t[j])
 
     # ---- the step ----
-    graph = None
+    exchange = None
     if world == 1:
         net.enable_graph(not args.no_graph)
 
         def step():
             net.train_step(B, lr, mom)
     else:
-        from paper_1501_07338_b200.dp import DataParallel
+        # data parallel through the C ABI (vcnn_dp_init: NCCL bootstrap, IPC
+        # peer mappings): the graph-replayed step is run_batch(shard) -> ONE
+        # kernel reading every replica's gradient over NVLink (rank-ordered
+        # weighted sum) + SGD + weight packs; NCCL all-reduce if no P2P path
+        from paper_1501_07338_b200.dp import NCCL, P2P, DataParallel
         dp = DataParallel(net)
+        net.enable_graph(not args.no_graph)
 
-        def eager_step():
-            # run_batch(shard) -> NCCL all-reduce over NVLink (fp32 sum of the
-            # one flat gradient buffer) -> replicated sgd_step(grad_scale 1/N)
-            dp.step(B, B * world, lr, mom)
-        step = eager_step
-        if not args.no_graph:
-            try:
-                s = torch.cuda.Stream()
-                s.wait_stream(stream)
-                with torch.cuda.stream(s):
-                    net.set_stream(s)
-                    for _ in range(2):
-                        eager_step()
-                stream.wait_stream(s)
-                graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(graph):
-                    net.set_stream(torch.cuda.current_stream())
-                    eager_step()
-                net.set_stream(stream)
-
-                def step():
-                    graph.replay()
-            except Exception as e:  # keep the eager DP path
-                print(f"[rank {rank}] graph capture failed ({e}); eager DP", file=sys.stderr)
-                net.set_stream(stream)
-                step = eager_step
+        def step():
+            dp.train_step(B, lr, mom)
 
     def barrier():
         torch.cuda.synchronize()
@@ -357,6 +404,25 @@ def main():
         load(i)
         step()
     barrier()
+    if world > 1:
+        # a P2P exchange whose barrier timed out on any rank -> every rank
+        # switches to the NCCL exchange (and says so)
+        ok = 1.0
+        try:
+            dp.status()
+        except Exception as e:  # noqa: BLE001
+            print(f"[rank {rank}] P2P exchange failed ({e}); NCCL fallback", file=sys.stderr)
+            ok = 0.0
+        t = torch.tensor([ok], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if t.item() < 1 and dp.mode == P2P:
+            dp.set_mode(NCCL)
+            for i in range(args.warmup):
+                load(i)
+                step()
+            barrier()
+        exchange = "p2p (one fused NVLink peer-reduce + SGD kernel)" if dp.mode == P2P \
+            else "nccl all-reduce + sgd"
 
     # ---- timed region: device events per step, a fresh batch from HBM each ----
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -371,6 +437,7 @@ def main():
             ev[i][1].record(stream)
         barrier()
     launches = _lib.lib().vcnn_launch_count() - launches0
+    kps = net.kernels_per_step()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     total_s = max_over_ranks(sum(step_ms) / 1e3)
     value = world * B * args.steps / total_s
@@ -417,48 +484,18 @@ def main():
                "api": "vcnn_net_train_host_stream (H2D of step i+1 overlaps step i)"
                if world == 1 else "H2D + graph step + D2H loss per step"}
 
+    if world > 1:  # the single-replica passes below must not wait on peers
+        barrier()
+        dp.close()
+        barrier()
+
     # ---- per-op timing pass (eager, CUDA events around every op) ----
     pk = peaks()
     roof = None
     details = {}
+    conv_gemm = None
     if rank == 0:
-        net.enable_graph(False)
-        net.enable_breakdown(True)
-        for i in range(args.steps):
-            load(i)
-            net.train_step(B, lr, mom)
-        ops = net.read_op_timing()
-        bd = net.read_breakdown()
-        net.enable_breakdown(False)
-        work = op_work(spec, B)
-        # the fused tail kernel (launch_mlp_head / launch_head) is timed as the
-        # loss op: give it the work of every conv / full layer above the last
-        # separately timed one (their forward, both gradients and the loss)
-        from paper_1501_07338_b200 import spec as S
-        timed = [l for (l, o) in ops if o != "loss" and l >= 0]
-        last = max(timed) if timed else -1
-        nl = len(spec.layers)
-        tail = [i for i in range(last + 1, nl) if not isinstance(spec.layers[i], S.PoolSpec)]
-        tail_name = None
-        if (nl - 1, "loss") in ops and tail:
-            f = sum(work.get((i, o), (0.0, 0.0))[0] for i in tail for o in ("fwd", "wgrad", "dgrad"))
-            by = sum(work.get((i, o), (0.0, 0.0))[1] for i in tail for o in ("fwd", "wgrad", "dgrad"))
-            lf, lb = work[(nl - 1, "loss")]
-            work[(nl - 1, "loss")] = (f + lf, by + lb)
-            tail_name = f"tail(layers {tail[0]}-{tail[-1]} fwd+bwd+loss, one kernel)"
-        rows = []
-        tot = sum(s for s, _ in ops.values())
-        for (layer, op), (sec, cnt) in ops.items():
-            f, by = work.get((layer, op), (0.0, 0.0))
-            t = sec / cnt
-            t_tc = f / (pk["tf32_tflops"] * 1e12) if f else 0.0
-            t_hbm = by / (pk["hbm_gbs"] * 1e9) if by else 0.0
-            bound = "tensor" if t_tc >= t_hbm else "hbm"
-            rows.append({"layer": layer, "op": op, "us": t * 1e6, "share": sec / tot,
-                         "flops": f, "bytes": by, "bound": bound,
-                         "tflops": f / t / 1e12 if f else 0.0, "gbs": by / t / 1e9 if by else 0.0,
-                         "roof_us": max(t_tc, t_hbm) * 1e6})
-        rows.sort(key=lambda r: -r["share"])
+        rows, bd, tail_name, tot = op_timing(net, spec, B, args.steps, load, lr, mom, pk)
         top = rows[0]
         if top["bound"] == "tensor":
             roof = {"bound": "tensor", "achieved": top["tflops"], "peak": pk["tf32_tflops"],
@@ -483,11 +520,57 @@ def main():
                      "share_of_step": top["share"], "us_per_launch": top["us"],
                      "peak_src": pk["tf32_src"] if top["bound"] == "tensor" else pk["src"]})
         step_roof_us = sum(r["roof_us"] for r in rows)
-        details = {"ops": rows, "breakdown_s": bd, "step_roofline_us": step_roof_us,
-                   "eager_step_us": tot / args.steps * 1e6, "peaks": pk}
+        conv_gemm = conv_gemm_rows(rows, spec, pk)
+        # the same step unfused (trace kept: every conv / pool / full layer its
+        # own kernels) for the reference's BreakdownTimer components (Fig. 6)
+        net.set_trace(True)
+        _, bd_unfused, _, _ = op_timing(net, spec, B, args.steps, load, lr, mom, pk)
+        net.set_trace(False)
+        details = {"ops": rows, "breakdown_s": bd, "breakdown_unfused_s": bd_unfused,
+                   "step_roofline_us": step_roof_us, "eager_step_us": tot / args.steps * 1e6,
+                   "peaks": pk, "conv_gemm_roofline": conv_gemm}
+        # the conv GEMMs at the roofline batch (CIFAR-3 b=1024)
+        if args.config == "cifar3" and not args.no_roofline_run and world == 1:
+            RB = 1024
+            rnet = Network(spec, RB, prec, stream=stream)
+            rx, rc, rv = S.synth_bench_data(spec, RB, 11)
+            rxt = torch.from_numpy(rx.reshape(RB, -1)).to(dev)
+            rtt = torch.from_numpy(rc if is_ce else rv).to(dev)
+
+            def rload(i):
+                rnet.load_batch(rxt, cls=rtt if is_ce else None, values=None if is_ce else rtt)
+            for i in range(3):
+                rload(i)
+                rnet.train_step(RB, lr, mom)
+            rrows, _, _, _ = op_timing(rnet, spec, RB, 5, rload, lr, mom, pk)
+            details["conv_gemm_roofline_b1024"] = conv_gemm_rows(rrows, spec, pk)
+            rnet.close()
         if args.details:
             with open(args.details, "w") as f:
                 json.dump(details, f, indent=1)
+
+    # ---- the fp32-faithful mode (3xTF32) on the same workload ----
+    faithful = None
+    if rank == 0 and world == 1 and args.precision == "tf32" and not args.no_faithful:
+        net.set_precision(S.Precision.tf32x3)
+        net.enable_graph(not args.no_graph)
+        for i in range(args.warmup):
+            load(i)
+            step()
+        torch.cuda.synchronize()
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for i in range(args.steps):
+            fev[i][0].record(stream)
+            load(args.warmup + i)
+            step()
+            fev[i][1].record(stream)
+        torch.cuda.synchronize()
+        fsec = sum(a.elapsed_time(b) for a, b in fev) / 1e3
+        faithful = {"precision": "tf32x3", "value": B * args.steps / fsec, "unit": "img/s",
+                    "ms_per_step": 1e3 * fsec / args.steps,
+                    "note": "fp32-faithful split-TF32 GEMMs (parity gated at 1e-5)"}
+        net.set_precision(prec)
 
     # ---- test mode (paper Table 4): forward-only img/s, graph-replayed ----
     infer = None
@@ -526,7 +609,6 @@ def main():
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model")}
 
     if rank == 0:
-        kps = net.kernels_per_step()
         line = {
             "metric": METRIC, "value": value, "unit": "img/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
@@ -540,11 +622,20 @@ def main():
             "gpu_launches": int(launches), "kernels_per_step": kps,
             "clocks": clk.result(),
             "step_roofline_us": details.get("step_roofline_us"),
+            "conv_gemm_roofline": conv_gemm,
+            "conv_gemm_roofline_b1024": details.get("conv_gemm_roofline_b1024"),
+            "fp32_faithful": faithful,
+            "dp_exchange": exchange,
             # BreakdownTimer components (variants.hpp:249-274, paper Fig. 6):
             # seconds per step from the event-timed eager pass
             "breakdown_ms_per_step": (
                 {k: 1e3 * v / args.steps for k, v in details["breakdown_s"].items()}
                 if details.get("breakdown_s") else None),
+            # the same components with every layer in its own kernels (the
+            # production step fuses pool into conv and the tail into one kernel)
+            "breakdown_unfused_ms_per_step": (
+                {k: 1e3 * v / args.steps for k, v in details["breakdown_unfused_s"].items()}
+                if details.get("breakdown_unfused_s") else None),
             "infer": infer,
         }
         print(json.dumps(line))

@@ -342,6 +342,53 @@ int vcnn_net_read_breakdown(vcnn_net* net, double* seconds8);
  * (layer -1 = whole-net ops); seconds and launch counts since enable */
 int vcnn_net_read_op_timing(vcnn_net* net, double* seconds, int64_t* counts);
 
+/* ------------------------------------------------------------------------ */
+/* L7 data parallelism: replicas of one network on the GPUs of   */
+/* one box, minibatch sharded, one gradient exchange per step at            */
+/* Trainer::fit's run_batch -> sgd_step boundary (training.hpp:76-81)       */
+/* ------------------------------------------------------------------------ */
+typedef struct vcnn_dp vcnn_dp;
+/* exchange: one fused kernel per replica reading every replica's gradient
+ * over NVLink peer mappings (rank-ordered sum + SGD + conv weight packs), or
+ * NCCL all-reduce + sgd */
+enum { VCNN_DP_P2P = 0, VCNN_DP_NCCL = 1 };
+#define VCNN_DP_ID_BYTES 128
+#define VCNN_DP_HANDLE_BYTES 256
+/* ncclGetUniqueId (rank 0; the caller broadcasts the 128 bytes) */
+int vcnn_dp_unique_id(void* id);
+/* process-per-GPU: NCCL communicator from `id`, exchange of the replicas'
+ * gradient / signal buffer IPC handles over it, P2P mappings; attaches the
+ * group to `net`: from then on vcnn_net_sgd_step / vcnn_net_train_step do the
+ * exchange.  Collective: every rank calls it. */
+int vcnn_dp_init(vcnn_net* net, int world, int rank, const void* id, vcnn_dp** out);
+/* the same in three steps, for hosts that exchange the handles themselves
+ * (any all-gather): create, publish VCNN_DP_HANDLE_BYTES, connect with all
+ * ranks' handles in rank order (+ an optional NCCL id for the fallback) */
+int vcnn_dp_create(vcnn_net* net, int world, int rank, vcnn_dp** out);
+int vcnn_dp_handle(const vcnn_dp* dp, void* handle);
+int vcnn_dp_connect(vcnn_dp* dp, const void* handles, const void* id);
+/* one process, `world` replicas (same or different devices) linked by
+ * direct pointers.  barrier = 1: replicas step independently (each on its
+ * own stream) and synchronise inside the exchange kernel, exactly as across
+ * processes; barrier = 0: G logical shards stepped together by
+ * vcnn_dp_group_train_step (event-ordered, no device barrier). */
+int vcnn_dp_group(vcnn_net* const* nets, int world, int barrier, vcnn_dp** out);
+int vcnn_dp_group_train_step(vcnn_dp* const* dps, int world, const int* batches, float lr,
+                             float mom);
+int vcnn_dp_set_mode(vcnn_dp* dp, int mode);
+int vcnn_dp_get_mode(const vcnn_dp* dp, int* mode);
+/* per-rank sample counts of the current global batch (weights B_p / B);
+ * default: equal shards */
+int vcnn_dp_set_shards(vcnn_dp* dp, const int* batches);
+/* the exchange + sgd_step alone (after vcnn_net_forward_backward) */
+int vcnn_dp_allreduce_sgd(vcnn_dp* dp, float lr, float mom);
+/* forward_backward + exchange + sgd_step (CUDA-graph replayed when enabled) */
+int vcnn_dp_train_step(vcnn_dp* dp, int batch, float lr, float mom);
+/* synchronises; VCNN_ENCCL if an exchange barrier timed out */
+int vcnn_dp_status(vcnn_dp* dp);
+/* detaches from the net and frees the group's resources */
+int vcnn_dp_destroy(vcnn_dp* dp);
+
 #ifdef __cplusplus
 }
 #endif

@@ -109,6 +109,20 @@ _SIGS = {
     "vcnn_net_device_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
     "vcnn_net_params_updated": [c_vp],
     "vcnn_net_set_nonfinite_guard": [c_vp, c_int],
+    "vcnn_dp_unique_id": [c_vp],
+    "vcnn_dp_init": [c_vp, c_int, c_int, c_vp, C.POINTER(c_vp)],
+    "vcnn_dp_create": [c_vp, c_int, c_int, C.POINTER(c_vp)],
+    "vcnn_dp_handle": [c_vp, c_vp],
+    "vcnn_dp_connect": [c_vp, c_vp, c_vp],
+    "vcnn_dp_group": [c_vp, c_int, c_int, c_vp],
+    "vcnn_dp_group_train_step": [c_vp, c_int, c_vp, c_float, c_float],
+    "vcnn_dp_set_mode": [c_vp, c_int],
+    "vcnn_dp_get_mode": [c_vp, P_int],
+    "vcnn_dp_set_shards": [c_vp, c_vp],
+    "vcnn_dp_allreduce_sgd": [c_vp, c_float, c_float],
+    "vcnn_dp_train_step": [c_vp, c_int, c_float, c_float],
+    "vcnn_dp_status": [c_vp],
+    "vcnn_dp_destroy": [c_vp],
     "vcnn_net_input_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
     "vcnn_net_set_batch_device": [c_vp, c_int, c_vp, c_vp, c_vp],
     "vcnn_net_forward_backward": [c_vp, c_int],

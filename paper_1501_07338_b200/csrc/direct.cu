@@ -590,6 +590,30 @@ __device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int
          (kk >> 2) * 32 + (r & 7) * 4 + (kk & 3);
 }
 
+// one element of sgd_step with the (already scaled) gradient gi, plus the
+// conv weight packs that element feeds
+__device__ __forceinline__ void update_pack(int64_t i, float gi, float* __restrict__ w,
+                                            float* __restrict__ v, float lr, float mom,
+                                            const PackTable& t) {
+  const float vi = mom * v[i] + gi;
+  const float wi = w[i] - lr * vi;
+  v[i] = vi;
+  w[i] = wi;
+  for (int l = 0; l < t.n; ++l) {
+    const PackLayer& L = t.L[l];
+    const int64_t k = i - L.w_off;
+    if (k < 0 || k >= L.w_len) continue;
+    const int khw = L.kh * L.kw, kd = L.C * khw;
+    const int k32 = (int)k;  // w_len < 2^31 (checked on the host): 32-bit divisions
+    const int nn = k32 / kd, rem = k32 - nn * kd;
+    const int c = rem / khw, s = rem - c * khw;
+    const float q = ptx::to_tf32(wi);
+    if (L.ps) L.ps[nn * L.wst + rem] = q;
+    if (L.pf) L.pf[pack_index(L.gf, nn, c, s)] = q;
+    if (L.pd) L.pd[pack_index(L.gd, c, nn, khw - 1 - s)] = q;
+  }
+}
+
 // sgd_step (network.hpp:242-273): v = mom*v + scale*g; w -= lr*v; and the
 // updated conv weights are written straight into the direct kernels' packs
 // (fwd: row n, channel c, s = ky*kw+kx; dgrad: row c, channel n, flipped s)
@@ -608,32 +632,89 @@ __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restr
     }
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float vi = mom * v[i] + scale * g[i];
-    const float wi = w[i] - lr * vi;
-    v[i] = vi;
-    w[i] = wi;
-    for (int l = 0; l < t.n; ++l) {
-      const PackLayer& L = t.L[l];
-      const int64_t k = i - L.w_off;
-      if (k < 0 || k >= L.w_len) continue;
-      const int khw = L.kh * L.kw, kd = L.C * khw;
-      const int k32 = (int)k;  // w_len < 2^31 (checked on the host): 32-bit divisions
-      const int nn = k32 / kd, rem = k32 - nn * kd;
-      const int c = rem / khw, s = rem - c * khw;
-      const float q = ptx::to_tf32(wi);
-      if (L.ps) L.ps[nn * L.wst + rem] = q;
-      if (L.pf) L.pf[pack_index(L.gf, nn, c, s)] = q;
-      if (L.pd) L.pd[pack_index(L.gd, c, nn, khw - 1 - s)] = q;
+       i += (int64_t)gridDim.x * blockDim.x)
+    update_pack(i, scale * g[i], w, v, lr, mom, t);
+}
+
+// ---- data parallelism: one-shot peer reduce + SGD + packs -----------------
+// Trainer::fit's exchange point (training.hpp:76-81) for W replicas, one
+// kernel per replica: every block owns one contiguous slice of the flat
+// gradient; it (1) signals every peer's block b that this replica's
+// gradient is final (its backward finished before this launch) and waits for
+// all peers' signals, (2) reads the slice from every replica's gradient
+// buffer -- peers through NVLink P2P mappings -- and sums it in RANK ORDER
+// (each term weighted by B_p / B_global), so all replicas compute the same
+// bits, (3) applies momentum SGD + the conv weight packs to its own
+// parameters, and (4) signals "done reading" and waits for every peer's, so
+// no replica overwrites its gradient (next backward) while a peer reads it.
+// Signals are monotonically increasing epochs; a barrier that waits longer
+// than the timeout sets *err and gives up (the host reports VCNN_ENCCL)
+// instead of hanging the device.
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// warp 0, lane p < world: signal peer p's slot [phase][rank][b], wait for
+// peer p's signal in my slot [phase][p][b]
+__device__ __forceinline__ void dp_barrier(const DpPeers& P, int phase, uint32_t e) {
+  const int lane = threadIdx.x;
+  if (lane < P.world) {
+    const int64_t row = (int64_t)P.nslot * P.world;
+    st_release_sys(P.sig[lane] + phase * row + (int64_t)P.rank * P.nslot + blockIdx.x, e);
+    const uint32_t* mine = P.my_sig + phase * row + (int64_t)lane * P.nslot + blockIdx.x;
+    const uint64_t t0 = globaltimer_ns();
+    while ((int32_t)(ld_acquire_sys(mine) - e) < 0) {
+      if (globaltimer_ns() - t0 > (uint64_t)P.timeout_ns) {
+        atomicExch(P.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void dp_sgd_pack_kernel(int64_t n, int64_t chunk, float* __restrict__ w,
+                                   float* __restrict__ v, float lr, float mom, const PackTable t,
+                                   const DpPeers P) {
+  PDL_ENTRY();
+  uint32_t e = 0;
+  if (P.barrier) {
+    if (threadIdx.x < 32) {
+      e = P.epoch[blockIdx.x] + 1;
+      dp_barrier(P, 0, e);
+    }
+    __syncthreads();
+  }
+  const int64_t lo = blockIdx.x * chunk, hi = lo + chunk < n ? lo + chunk : n;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    float sum = P.scale[0] * P.g[0][i];
+    for (int p = 1; p < P.world; ++p) sum = fmaf(P.scale[p], P.g[p][i], sum);
+    update_pack(i, sum, w, v, lr, mom, t);
+  }
+  if (P.barrier) {
+    __syncthreads();  // every read of the peers' slice is done
+    if (threadIdx.x < 32) {
+      dp_barrier(P, 1, e);
+      if (threadIdx.x == 0) P.epoch[blockIdx.x] = e;
     }
   }
 }
 }  // namespace
 
-int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
-             const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss,
-             int* guard) {
-  PackTable t{};
+namespace {
+int pack_table(const std::vector<PackSpec>& layers, PackTable& t) {
+  t = PackTable{};
   for (const PackSpec& p : layers) {
     if (!p.pf && !p.pd && !p.ps) continue;
     if (t.n == kMaxPackLayers) return fail(VCNN_ECONFIG, "sgd_pack: too many conv layers");
@@ -652,10 +733,39 @@ int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom,
     if (p.pf && !plan(p.d, 0, 0, 0, 0, L.gf)) return fail(VCNN_ESHAPE, "sgd_pack: fwd plan");
     if (p.pd && !plan(p.d, 1, 0, 0, 0, L.gd)) return fail(VCNN_ESHAPE, "sgd_pack: dgrad plan");
   }
+  return VCNN_OK;
+}
+}  // namespace
+
+int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+             const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss,
+             int* guard) {
+  PackTable t;
+  if (int s = pack_table(layers, t)) return s;
   int64_t blocks = cdiv(n, 256);
   if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
   if (blocks < 1) blocks = 1;
   VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int dp_blocks(int64_t n) {
+  int64_t b = cdiv(n, 2048);
+  if (b > kMaxDpSlots) b = kMaxDpSlots;
+  if (b > sm_count()) b = sm_count();
+  return b < 1 ? 1 : (int)b;
+}
+
+int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
+                const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st) {
+  PackTable t;
+  if (int s = pack_table(layers, t)) return s;
+  if (peers.world < 1 || peers.world > kMaxWorld) return fail(VCNN_ECONFIG, "dp: world size");
+  const int blocks = peers.nslot;
+  if (blocks < 1 || blocks > kMaxDpSlots) return fail(VCNN_ECONFIG, "dp: block count");
+  const int64_t chunk = cdiv(n, blocks);
+  VCNN_CUDA_TRY(launch_pdl(dp_sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, chunk, w, v, lr, mom, t, peers));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

@@ -120,6 +120,8 @@ struct vcnn_net {
   struct GraphEntry {
     int batch;
     float lr, mom;
+    const DpLink* dp;
+    int dpv;
     cudaGraphExec_t exec;
     int kernels;
   };
@@ -139,8 +141,11 @@ struct vcnn_net {
   } pipe;
   int g_batch = -1;
   float g_lr = 0, g_mom = 0;
+  const DpLink* g_dp = nullptr;
+  int g_dpv = 0;
   int kernels_per_step = 0;
   bool guard = false;  // Trainer non-finite stop armed (err[2..3] on the device)
+  DpLink* dp = nullptr;  // attached data-parallel group (vcnn_dp_*), or none
   // breakdown timer
   bool breakdown = false;
   struct MarkRec {
@@ -508,8 +513,22 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
     }
     slab_copies = slab_copies || l.wf;
   }
-  TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
-                       n->stream, n->loss, n->err + 2));
+  DpLink* dp = n->dp;
+  if (!dp || dp->world == 1) {
+    TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
+                         n->stream, n->loss, n->err + 2));
+  } else if (dp->mode == VCNN_DP_P2P) {
+    // one kernel: rank-ordered sum of every replica's gradient (peers over
+    // NVLink) + SGD + packs
+    TRY(direct::dp_sgd_pack(n->nparams, n->params, n->vel, lr, mom, packs, dp->peers,
+                            n->stream));
+  } else {
+    // NCCL fallback: weight, all-reduce (sum) in place, replicated update
+    if (!dp->equal) TRY(dp_scale(n->nparams, n->grads, dp->local_w, n->stream));
+    TRY(dp->allreduce(dp, n->grads, n->nparams, n->stream));
+    TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom,
+                         dp->equal ? scale / (float)dp->world : scale, packs, n->stream));
+  }
   for (const LayerRt* l : repack) {
     const ConvDesc d = conv_of(*l, 1);
     const float* w = n->params + l->w_off;
@@ -557,10 +576,13 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
   TRY(check_batch(n, batch));
   TRY(check_cfg(lr, mom));
   if (!n->use_graph || n->breakdown) return eager_step(n, batch, lr, mom);
-  if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom) {
+  const int dpv = n->dp ? n->dp->version : 0;
+  if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom ||
+      n->g_dp != n->dp || n->g_dpv != dpv) {
     n->gexec = nullptr;
     for (auto& e : n->graphs)
-      if (e.batch == batch && e.lr == lr && e.mom == mom) {
+      if (e.batch == batch && e.lr == lr && e.mom == mom && e.dp == n->dp &&
+          e.dpv == (n->dp ? n->dp->version : 0)) {
         n->gexec = e.exec;
         n->kernels_per_step = e.kernels;
       }
@@ -569,6 +591,8 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     n->g_batch = batch;
     n->g_lr = lr;
     n->g_mom = mom;
+    n->g_dp = n->dp;
+    n->g_dpv = dpv;
   } else {
     if (n->graphs.size() >= 4) drop_graph(n);
     if (!n->cap_stream)
@@ -591,10 +615,13 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     e = cudaGraphInstantiate(&n->gexec, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
-    n->graphs.push_back({batch, lr, mom, n->gexec, n->kernels_per_step});
+    n->graphs.push_back(
+        vcnn_net::GraphEntry{batch, lr, mom, n->dp, dpv, n->gexec, n->kernels_per_step});
     n->g_batch = batch;
     n->g_lr = lr;
     n->g_mom = mom;
+    n->g_dp = n->dp;
+    n->g_dpv = dpv;
   }
   VCNN_CUDA_TRY(cudaGraphLaunch(n->gexec, n->stream));
   g_launches.fetch_add(n->kernels_per_step);
@@ -632,6 +659,16 @@ int check_errflag(vcnn_net* n) {
 }
 
 }  // namespace
+
+namespace vcnn_b200 {
+int engine_attach_dp(vcnn_net* n, DpLink* link) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  drop_graph(n);
+  n->dp = link;
+  return VCNN_OK;
+}
+cudaStream_t engine_stream(vcnn_net* n) { return n ? n->stream : nullptr; }
+}  // namespace vcnn_b200
 
 extern "C" {
 

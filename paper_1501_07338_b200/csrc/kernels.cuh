@@ -165,6 +165,41 @@ struct PoolFuse {
   int32_t* arg = nullptr;
 };
 
+// data-parallel exchange + update (dp.cu): the replicas' gradient buffers
+// (peers through P2P mappings), their signal buffers [2][world][nslot] u32,
+// per-rank weights B_p / B_global; barrier = 0 when the caller orders the
+// replicas itself (one stream, G logical shards on one device)
+constexpr int kMaxWorld = 8;
+constexpr int kMaxDpSlots = 256;
+struct DpPeers {
+  const float* g[kMaxWorld];
+  uint32_t* sig[kMaxWorld];
+  float scale[kMaxWorld];
+  uint32_t* my_sig;
+  uint32_t* epoch;  // [nslot], this replica's
+  int* err;
+  int64_t timeout_ns;
+  int world, rank, nslot, barrier;
+};
+// a data-parallel group attached to a net (dp.cu): the engine's sgd step
+// becomes the group exchange + update
+struct DpLink {
+  int world = 1;
+  int mode = 0;  // VCNN_DP_P2P / VCNN_DP_NCCL
+  DpPeers peers{};
+  bool equal = true;    // all shards the same size (NCCL path: scale 1/world)
+  float local_w = 1.f;  // this rank's B_p / B_global
+  int version = 0;      // bumped when shard weights / mode change (graph key)
+  // NCCL fallback: in-place sum all-reduce of the flat gradient
+  int (*allreduce)(DpLink* l, float* buf, int64_t n, cudaStream_t st) = nullptr;
+  void* comm = nullptr;
+};
+int dp_scale(int64_t n, float* buf, float s, cudaStream_t st);
+// engine hooks for dp.cu (engine.cu): attach (or detach with null) a group
+// to a net -- its sgd step becomes the exchange; drops cached step graphs
+int engine_attach_dp(vcnn_net* n, DpLink* link);
+cudaStream_t engine_stream(vcnn_net* n);
+
 // ---- direct (shifted-view) stride-1 conv forward / dgrad (direct.cu, TF32) ----
 namespace direct {
 bool fwd_ok(const ConvDesc& d, int pool);
@@ -202,6 +237,9 @@ struct PackSpec {
 int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss = nullptr,
              int* guard = nullptr);
+int dp_blocks(int64_t n);
+int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
+                const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st);
 // weight gradient as shifted-view GEMMs (wgrad.cu): dW [K][C][kh][kw] and db
 // [K] (nullable) from x and the (possibly pool-routed) gradient; per-image
 // partials in ws, fixed-order reduce

@@ -67,6 +67,8 @@ class Network:
     # ---- lifetime ----
     def close(self):
         if getattr(self, "_h", None):
+            for d in getattr(self, "_dps", []):  # data-parallel groups attached to it
+                d.close()
             lib().vcnn_net_destroy(self._h)
             self._h = None
 
@@ -400,7 +402,7 @@ class Trainer:
         self.precision = Precision(precision)
         self.use_graph = use_graph
 
-    def fit(self, net: Network, images, targets, resident=False):
+    def fit(self, net: Network, images, targets, resident=False, dp=None):
         """resident=True: the dataset is uploaded once and every epoch runs on
         the device (vcnn_net_train_epoch: permutation from the reference Rng,
         index-gather kernel, graph-replayed steps, one D2H of the epoch's
@@ -412,6 +414,8 @@ class Trainer:
         count = images.shape[0]
         if count < 1:
             raise TrainingError("fit: empty dataset")
+        if dp is not None and dp.world > 1:
+            return self._fit_dp(net, images, targets, dp)
         if resident:
             return self._fit_resident(net, images, targets)
         net.set_precision(self.precision)
@@ -450,6 +454,44 @@ class Trainer:
                 loss_sum += loss
                 batches += 1
             epoch_loss.append(loss_sum / batches)
+        return epoch_loss
+
+    def _fit_dp(self, net: Network, images, targets, dp):
+        """Data-parallel fit: every rank draws the same seeded
+        permutation and trains on its contiguous slice of each global batch
+        (dp.epoch_shards); the net's update is the group exchange weighted by
+        the shard sizes, so the replicas follow the single-GPU trajectory.
+        The epoch loss is the mean of the global-batch losses
+        (sum_p B_p/B * loss_p, gathered over torch.distributed)."""
+        import torch.distributed as dist
+
+        from .dp import epoch_shards
+        net.set_precision(self.precision)
+        net.enable_graph(self.use_graph)
+        count = images.shape[0]
+        is_ce = net.spec.loss == LossKind.softmax_ce
+        tg = np.asarray(targets)
+        rng = Rng(self.cfg.seed)
+        order = list(range(count))
+        epoch_loss = []
+        for epoch in range(self.cfg.epochs):
+            rng.shuffle(order)
+            total, batches = 0.0, 0
+            for ids, sizes in epoch_shards(order, self.cfg.batch, dp.rank, dp.world):
+                dp.set_shards(sizes)
+                kw = (dict(cls=tg[ids].astype(np.int32)) if is_ce
+                      else dict(values=tg[ids].reshape(len(ids), -1)))
+                loss = net.train_step_host(images[ids], lr=self.cfg.lr,
+                                           momentum=self.cfg.momentum, **kw)
+                t = torch.tensor([loss * len(ids) / sum(sizes)], dtype=torch.float64,
+                                 device="cuda" if dist.get_backend() == "nccl" else "cpu")
+                dist.all_reduce(t)
+                g = float(t.item())
+                if not np.isfinite(g):
+                    raise TrainingError(f"non-finite loss at epoch {epoch}, batch {batches}")
+                total += g
+                batches += 1
+            epoch_loss.append(total / batches)
         return epoch_loss
 
     def _fit_resident(self, net: Network, images, targets):
