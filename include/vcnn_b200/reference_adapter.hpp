@@ -97,6 +97,17 @@ class Executor {
                                      : PoolBackwardMode::exact);
   }
   vcnn::PoolBackwardMode pool_backward_mode() const { return mode_; }
+  vcnn::Variant variant() const { return vcnn::Variant::imp6; }
+
+  // Executor::set_timer (variants.hpp:341): per-component device time (CUDA
+  // events around every layer op, conv / pool / full / other x fwd / bwd)
+  // added to the reference's BreakdownTimer after each call.  While a timer
+  // is set the device runs every layer in its own kernels (no conv+pool /
+  // tail fusion), so the components separate as in the reference's Imp-6.
+  void set_timer(vcnn::BreakdownTimer* t) {
+    timer_ = t;
+    if (dev_) configure_timing(*dev_);
+  }
 
   vcnn::Tensor<float> forward(const vcnn::Network<float>& net, const vcnn::Tensor<float>& batch) {
     return run_batch(net, batch, nullptr).output;
@@ -115,7 +126,15 @@ class Executor {
       else t.values = targets->values.data;
       tp = &t;
     }
+    double before[8] = {0};
+    if (timer_) check(vcnn_net_read_breakdown(dev.handle(), before));
     RunResult r = exec_.run_batch(dev, batch.data.data(), n, tp);
+    if (timer_) {
+      double after[8] = {0};
+      check(vcnn_net_read_breakdown(dev.handle(), after));
+      for (int c = 0; c < 8; ++c)
+        timer_->add(static_cast<vcnn::Component>(c), after[c] - before[c]);
+    }
     vcnn::RunResult<float> out;
     const vcnn::Shape o = net.spec.output_shape();
     out.output = vcnn::Tensor<float>(vcnn::Shape::hwcn(o.h(), o.w(), o.c(), n));
@@ -137,6 +156,7 @@ class Executor {
                           : n;
       dev_ = std::make_unique<Network>(spec_of(net.spec), cap, prec_);
       spec_ = net.spec;
+      configure_timing(*dev_);
     }
     return *dev_;
   }
@@ -166,7 +186,12 @@ class Executor {
     }
     return true;
   }
+  void configure_timing(Network& dev) {
+    check(vcnn_net_set_trace(dev.handle(), timer_ ? 1 : 0));
+    check(vcnn_net_enable_breakdown(dev.handle(), timer_ ? 1 : 0));
+  }
   Precision prec_;
+  vcnn::BreakdownTimer* timer_ = nullptr;
   vcnn_b200::Executor exec_;
   vcnn::PoolBackwardMode mode_ = vcnn::PoolBackwardMode::exact;
   std::unique_ptr<Network> dev_;

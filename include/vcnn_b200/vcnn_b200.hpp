@@ -21,8 +21,10 @@
 // reference_adapter.hpp.
 #pragma once
 
+#include <array>
 #include <cmath>
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <variant>
@@ -348,6 +350,70 @@ inline std::vector<int> predict_classes(const std::vector<float>& out, int n) {
   return cls;
 }
 
+// Data parallelism (vcnn_dp_*): the gradient exchange inserted
+// between run_batch and sgd_step (training.hpp:76-81).  Attached to its
+// Network: from construction on, the net's sgd step (and train steps) are the
+// group exchange -- by default ONE kernel per replica reading every replica's
+// gradient over NVLink peer mappings (rank-ordered sum weighted by B_p / B,
+// SGD, weight packs), else NCCL all-reduce.  Contiguous shards of each
+// global batch (Imp-2 chunking, variants.hpp:442-443).
+class DataParallel {
+ public:
+  using Id = std::array<uint8_t, VCNN_DP_ID_BYTES>;
+  // rank 0 creates the NCCL id; the host broadcasts the bytes to every rank
+  static Id unique_id() {
+    Id id{};
+    check(vcnn_dp_unique_id(id.data()));
+    return id;
+  }
+  // process-per-GPU (collective: every rank constructs it)
+  DataParallel(Network& net, int world, int rank, const Id& id) : world_(world), rank_(rank) {
+    check(vcnn_dp_init(net.handle(), world, rank, id.data(), &h_));
+  }
+  // `world` replicas in one process (one device or several); barrier = false:
+  // step them together with Trainer::fit_group / vcnn_dp_group_train_step
+  static std::vector<std::unique_ptr<DataParallel>> group(const std::vector<Network*>& nets,
+                                                          bool barrier = false) {
+    std::vector<vcnn_net*> hs;
+    for (Network* n : nets) hs.push_back(n->handle());
+    std::vector<vcnn_dp*> out(nets.size(), nullptr);
+    check(vcnn_dp_group(hs.data(), (int)hs.size(), barrier ? 1 : 0, out.data()));
+    std::vector<std::unique_ptr<DataParallel>> g;
+    for (size_t r = 0; r < out.size(); ++r)
+      g.emplace_back(new DataParallel(out[r], (int)out.size(), (int)r));
+    return g;
+  }
+  DataParallel(const DataParallel&) = delete;
+  DataParallel& operator=(const DataParallel&) = delete;
+  ~DataParallel() {
+    if (h_) vcnn_dp_destroy(h_);
+  }
+  int world() const { return world_; }
+  int rank() const { return rank_; }
+  vcnn_dp* handle() const { return h_; }
+  void set_mode(int mode) { check(vcnn_dp_set_mode(h_, mode)); }
+  void set_shards(const std::vector<int>& batches) { check(vcnn_dp_set_shards(h_, batches.data())); }
+  void status() { check(vcnn_dp_status(h_)); }
+  // [lo, hi) of rank's contiguous shard of a global batch
+  static std::pair<int, int> shard(int global_batch, int rank, int world) {
+    return {(int)((int64_t)global_batch * rank / world),
+            (int)((int64_t)global_batch * (rank + 1) / world)};
+  }
+  static std::vector<int> shard_sizes(int global_batch, int world) {
+    std::vector<int> s((size_t)world);
+    for (int r = 0; r < world; ++r) {
+      auto [lo, hi] = shard(global_batch, r, world);
+      s[(size_t)r] = hi - lo;
+    }
+    return s;
+  }
+
+ private:
+  DataParallel(vcnn_dp* h, int world, int rank) : h_(h), world_(world), rank_(rank) {}
+  vcnn_dp* h_ = nullptr;
+  int world_ = 1, rank_ = 0;
+};
+
 // Trainer (training.hpp:50-124): seeded shuffle per epoch (Rng::shuffle,
 // common.hpp:84-90), batches of cfg.batch with a smaller last batch, one
 // device train step per batch (graph-replayed), NaN -> TrainingError.
@@ -355,8 +421,13 @@ class Trainer {
  public:
   explicit Trainer(TrainConfig cfg) : cfg_(cfg) { cfg_.validate(); }
 
+  // dp (optional, process-per-GPU): every rank draws the same permutation and
+  // trains on its contiguous slice of each global batch of cfg.batch samples;
+  // the update is the group exchange, so the replicas follow the single-GPU
+  // trajectory.  The returned losses are then this rank's shard losses
+  // weighted by B_p / B (sum them over the ranks for the global epoch loss).
   std::vector<double> fit(Network& net, const std::vector<float>& images,
-                          const Targets<float>& targets) {
+                          const Targets<float>& targets, DataParallel* dp = nullptr) {
     const int64_t per = net.input_size();
     const int count = (int)(images.size() / (size_t)per);
     if (count < 1) throw TrainingError("fit: empty dataset");
@@ -379,8 +450,18 @@ class Trainer {
       rng.shuffle(order);
       double sum = 0;
       int batches = 0;
-      for (int start = 0; start < count; start += cfg_.batch) {
-        const int n = std::min(cfg_.batch, count - start);
+      for (int gstart = 0; gstart < count; gstart += cfg_.batch) {
+        int start = gstart, n = std::min(cfg_.batch, count - gstart);
+        double w = 1.0;
+        if (dp && dp->world() > 1) {  // this rank's slice of the global batch
+          const int gb = n;
+          if (gb < dp->world()) throw ShapeError("fit: a global batch smaller than the world");
+          auto [lo, hi] = DataParallel::shard(gb, dp->rank(), dp->world());
+          dp->set_shards(DataParallel::shard_sizes(gb, dp->world()));
+          start = gstart + lo;
+          n = hi - lo;
+          w = (double)n / gb;
+        }
         xb.resize((size_t)(n * per));
         cb.resize((size_t)n);
         vb.resize((size_t)(n * units));
@@ -398,6 +479,81 @@ class Trainer {
         check(vcnn_net_train_step_host(net.handle(), n, xb.data(), ce ? cb.data() : nullptr,
                                        ce ? nullptr : vb.data(), (float)cfg_.lr,
                                        (float)cfg_.momentum, &loss));
+        if (!std::isfinite(loss))
+          throw TrainingError("non-finite loss at epoch " + std::to_string(e) + ", batch " +
+                              std::to_string(batches));
+        sum += w * loss;
+        ++batches;
+      }
+      epoch_loss.push_back(sum / batches);
+    }
+    return epoch_loss;
+  }
+
+  // single process, G replicas (one per device, or G logical shards of one
+  // device) created by DataParallel::group(nets, false): per global batch every
+  // replica gets its contiguous shard and one vcnn_dp_group_train_step runs
+  // them all; the epoch loss is the mean of the global-batch losses
+  // (sum_p B_p / B * loss_p), as the single-GPU Trainer reports it
+  std::vector<double> fit_group(const std::vector<Network*>& nets,
+                                const std::vector<std::unique_ptr<DataParallel>>& dps,
+                                const std::vector<float>& images, const Targets<float>& targets) {
+    const int G = (int)nets.size();
+    if (G < 1 || (int)dps.size() != G) throw ConfigError("fit_group: one DataParallel per net");
+    const int64_t per = nets[0]->input_size();
+    const int count = (int)(images.size() / (size_t)per);
+    if (count < 1) throw TrainingError("fit: empty dataset");
+    const bool ce = nets[0]->spec().loss == LossKind::softmax_ce;
+    const int64_t units = nets[0]->output_units();
+    std::vector<int> order((size_t)count);
+    for (int i = 0; i < count; ++i) order[(size_t)i] = i;
+    Mt64 rng(cfg_.seed);
+    std::vector<double> epoch_loss;
+    std::vector<vcnn_dp*> hs;
+    for (auto& d : dps) hs.push_back(d->handle());
+    std::vector<float> xb, vb;
+    std::vector<int> cb;
+    for (int e = 0; e < cfg_.epochs; ++e) {
+      rng.shuffle(order);
+      double sum = 0;
+      int batches = 0;
+      for (int gstart = 0; gstart < count; gstart += cfg_.batch) {
+        const int gb = std::min(cfg_.batch, count - gstart);
+        if (gb < G) throw ShapeError("fit_group: a global batch smaller than the group");
+        const std::vector<int> sizes = DataParallel::shard_sizes(gb, G);
+        for (int r = 0; r < G; ++r) {  // stage each replica's shard
+          const int lo = DataParallel::shard(gb, r, G).first, n = sizes[(size_t)r];
+          xb.resize((size_t)(n * per));
+          cb.resize((size_t)n);
+          vb.resize((size_t)(n * units));
+          for (int j = 0; j < n; ++j) {
+            const int id = order[(size_t)(gstart + lo + j)];
+            std::copy(images.begin() + (size_t)id * per, images.begin() + (size_t)(id + 1) * per,
+                      xb.begin() + (size_t)j * per);
+            if (ce) cb[(size_t)j] = targets.classes[(size_t)id];
+            else
+              std::copy(targets.values.begin() + (size_t)id * units,
+                        targets.values.begin() + (size_t)(id + 1) * units,
+                        vb.begin() + (size_t)j * units);
+          }
+          if (ce)
+            for (int c : cb)
+              if (c < 0 || c >= units) throw BoundsError("loss: class index out of range");
+          float *dx = nullptr, *dv = nullptr;
+          int* dc = nullptr;
+          check(vcnn_net_input_buffers(nets[(size_t)r]->handle(), &dx, &dc, &dv));
+          check(vcnn_copy_h2d(dx, xb.data(), sizeof(float) * xb.size()));
+          if (ce) check(vcnn_copy_h2d(dc, cb.data(), sizeof(int) * cb.size()));
+          else check(vcnn_copy_h2d(dv, vb.data(), sizeof(float) * vb.size()));
+        }
+        check(vcnn_dp_group_train_step(hs.data(), G, sizes.data(), (float)cfg_.lr,
+                                       (float)cfg_.momentum));
+        double loss = 0;
+        for (int r = 0; r < G; ++r) {
+          float l = 0;
+          check(vcnn_net_get_loss(nets[(size_t)r]->handle(), &l));
+          loss += (double)sizes[(size_t)r] / gb * l;
+        }
         if (!std::isfinite(loss))
           throw TrainingError("non-finite loss at epoch " + std::to_string(e) + ", batch " +
                               std::to_string(batches));

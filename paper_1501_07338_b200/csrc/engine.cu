@@ -307,6 +307,9 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
 // launch_mlp_head), 1 when the last is a small full layer (launch_head),
 // else 0 (separate forward / loss / backward kernels).
 int tail_fused(const vcnn_net* n, int B) {
+  // profiling (trace + breakdown, e.g. Executor::set_timer): every layer in
+  // its own kernels, so the components separate as in the reference
+  if (n->keep_trace && n->breakdown) return 0;
   const size_t nl = n->L.size();
   const LayerRt& l = n->L.back();
   if (l.spec.kind != VCNN_LAYER_FULL) return 0;

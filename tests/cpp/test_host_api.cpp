@@ -104,6 +104,39 @@ int main() {
   auto hist = tr.fit(tn, imgs, Targets<float>::from_classes(labels));
   EXPECT(hist.back() < hist.front(), "fit lowers the loss");
   EXPECT(tr.evaluate_accuracy(tn, imgs, labels) > 0.9, "accuracy > 0.9");
+
+  // data parallelism in one process: 2 replicas (logical shards of one
+  // device) trained by Trainer::fit_group follow the single-net Trainer on
+  // the same global batches (3xTF32), and stay bit-identical to each other
+  {
+    const int n2 = 40, gb = 16;  // batches 16, 16, 8
+    TrainConfig dc;
+    dc.lr = 0.05;
+    dc.momentum = 0.9;
+    dc.batch = gb;
+    dc.epochs = 2;
+    dc.seed = 9;
+    auto tg = Targets<float>::from_classes(std::vector<int>(labels.begin(), labels.begin() + n2));
+    std::vector<float> im(imgs.begin(), imgs.begin() + (size_t)n2 * 36);
+    Network single(ts, gb, Precision::tf32x3);
+    auto h1 = Trainer(dc).fit(single, im, tg);
+    Network r0(ts, gb / 2, Precision::tf32x3), r1(ts, gb / 2, Precision::tf32x3);
+    std::vector<Network*> reps{&r0, &r1};
+    auto dps = DataParallel::group(reps);
+    auto h2 = Trainer(dc).fit_group(reps, dps, im, tg);
+    double le = 0;
+    for (size_t e = 0; e < h1.size(); ++e) le = std::fmax(le, std::fabs(h1[e] - h2[e]) / h1[e]);
+    EXPECT(h2.size() == 2 && le < 1e-5, "fit_group epoch losses == single-net fit");
+    auto ps = single.params(), p0 = r0.params(), p1 = r1.params();
+    double pe = 0, pm = 0;
+    bool same = p0 == p1;
+    for (size_t i = 0; i < ps.size(); ++i) {
+      pe = std::fmax(pe, std::fabs(p0[i] - ps[i]));
+      pm = std::fmax(pm, std::fabs(ps[i]));
+    }
+    EXPECT(same, "replicas bit-identical");
+    EXPECT(pe / pm < 1e-5, "fit_group weights == single-net weights");
+  }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL OK", failures);
   return failures ? 1 : 0;
 }
