@@ -138,6 +138,14 @@ int vcnn_matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b,
 /* matmul_transB: C[m][n] = A[m][k] * B[n][k]^T (tensor.hpp:154-174) */
 int vcnn_matmul_transB(int64_t m, int64_t k, int64_t n, const float* a, const float* b,
                        float* c, int precision, void* stream);
+/* general GEMM (matmul / matmul_transB / transpose, tensor.hpp:131-182, with
+ * the conv_affine / full-layer epilogue, layers.hpp:99-105, :230-247):
+ * C[m][n] = act(sum_k op(A)[m][k] op(B)[k][n] + bias[n]); op(A) = A [m][k]
+ * (lda) or, trans_a, A^T of A [k][m]; op(B) = B [k][n] (ldb) or, trans_b,
+ * B^T of B [n][k]; C row stride ldc; bias nullable */
+int vcnn_gemm(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, const float* a,
+              int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, const float* bias,
+              int act, int precision, void* stream);
 /* accumulate_by_index (tensor.hpp:228-266): out[t] = reducer over
  * {values[s] : (s,t) in map}, pairs consumed in map order (deterministic);
  * empty buckets 0. */

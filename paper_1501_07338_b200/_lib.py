@@ -65,6 +65,8 @@ _SIGS = {
     "vcnn_synth_bench_data": [C.POINTER(NetSpecC), c_int, C.c_uint64, c_vp, c_vp, c_vp],
     "vcnn_matmul": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
     "vcnn_matmul_transB": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_int, c_vp],
+    "vcnn_gemm": [c_int, c_int, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
+                  c_int, c_int, c_vp],
     "vcnn_accumulate_by_index": [c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_int, c_vp, c_vp],
     "vcnn_accumulate_max_arg": [c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp],
     "vcnn_im2col": [C.POINTER(ConvGeometryC), c_vp, c_vp, c_vp],

@@ -197,6 +197,28 @@ int vcnn_matmul_transB(int64_t m, int64_t k, int64_t n, const float* a, const fl
   return launch_matmul(m, k, n, a, b, c, true, precision, ws, st);
 }
 
+// the general GEMM of the C ABI: op(A) [m][k], op(B) [k][n],
+// C [m][n] with leading dimensions, + bias[n] + activation
+int vcnn_gemm(int trans_a, int trans_b, int64_t m, int64_t n, int64_t k, const float* a,
+              int64_t lda, const float* b, int64_t ldb, float* c, int64_t ldc, const float* bias,
+              int act, int precision, void* stream) {
+  TRY(check_prec(precision));
+  if (m < 0 || k < 0 || n < 0) return fail(VCNN_ESHAPE, "matrix extents must be non-negative");
+  if (act < VCNN_ACT_IDENTITY || act > VCNN_ACT_TANH) return fail(VCNN_ECONFIG, "unknown activation");
+  if (ldc < n || lda < (trans_a ? m : k) || ldb < (trans_b ? k : n))
+    return fail(VCNN_ESHAPE, "gemm: leading dimension smaller than the row length");
+  TRY(require_device());
+  if (m == 0 || n == 0) return VCNN_OK;
+  const int64_t as_m = trans_a ? 1 : lda, as_k = trans_a ? lda : 1;
+  const int64_t bs_k = trans_b ? 1 : ldb, bs_n = trans_b ? ldb : 1;
+  cudaStream_t st = as_stream(stream);
+  if (precision == VCNN_PREC_FP32 || k == 0)
+    return simt::gemm(m, n, k, a, as_m, as_k, b, bs_k, bs_n, c, ldc, bias, act, st);
+  WORKSPACE(ws, tc::matmul_workspace(m, k, n));
+  return tc::gemm(m, n, k, a, as_m, as_k, b, bs_k, bs_n, c, ldc, bias, act,
+                  precision == VCNN_PREC_3XTF32, ws, st);
+}
+
 int vcnn_accumulate_by_index(const float* values, int64_t source_len, const int64_t* source,
                              const int64_t* target, int64_t pairs, int64_t target_len,
                              int reducer, float* out, void* stream) {

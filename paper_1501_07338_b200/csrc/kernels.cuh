@@ -141,6 +141,9 @@ int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float*
                const float* yprev, int act_prev, cudaStream_t st);
 int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
            bool transB, cudaStream_t st);
+int gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t as_m, int64_t as_k,
+         const float* b, int64_t bs_k, int64_t bs_n, float* c, int64_t ldc, const float* bias,
+         int act, cudaStream_t st);
 }  // namespace simt
 
 // Source of a conv layer's pre-activation output gradient G [B][K][OH][OW]:
@@ -303,6 +306,9 @@ int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float*
                cudaStream_t st);
 int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,
            bool transB, bool split3, const Workspace& ws, cudaStream_t st);
+int gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t as_m, int64_t as_k,
+         const float* b, int64_t bs_k, int64_t bs_n, float* c, int64_t ldc, const float* bias,
+         int act, bool split3, const Workspace& ws, cudaStream_t st);
 // scratch the launchers above need (split-K partials, explicit-dgrad dP)
 size_t conv_workspace(const ConvDesc& d);
 size_t full_workspace(int B, int in, int out);

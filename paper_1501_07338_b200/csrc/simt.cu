@@ -666,6 +666,24 @@ __global__ void matmul_simt(int64_t m, int64_t k, int64_t n, const float* __rest
   }
 }
 
+// general strided GEMM, fp32 FMA in ascending k (the reference matmul's
+// order, tensor.hpp:131-174) + bias[n] + activation
+__global__ void gemm_simt(int64_t m, int64_t n, int64_t k, const float* __restrict__ a,
+                          int64_t as_m, int64_t as_k, const float* __restrict__ b, int64_t bs_k,
+                          int64_t bs_n, float* __restrict__ c, int64_t ldc,
+                          const float* __restrict__ bias, int act) {
+  PDL_ENTRY();
+  const int64_t total = m * n;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t % n, i = t / n;
+    float acc = 0.f;
+    for (int64_t q = 0; q < k; ++q) acc += a[i * as_m + q * as_k] * b[q * bs_k + j * bs_n];
+    if (bias) acc += bias[j];
+    c[i * ldc + j] = act_fwd(act, acc);
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1151,6 +1169,14 @@ int full_dgrad(int B, int in, int out, const float* gpre, const float* w, float*
                const float* yprev, int act_prev, cudaStream_t st) {
   VCNN_CUDA_TRY(launch_pdl(full_dgrad_simt, dim3(grid_for((int64_t)B * in)), dim3(kThreads), 0, st, B, in, out, gpre, w, dx,
                                                                   yprev, act_prev));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
+int gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t as_m, int64_t as_k,
+         const float* b, int64_t bs_k, int64_t bs_n, float* c, int64_t ldc, const float* bias,
+         int act, cudaStream_t st) {
+  VCNN_CUDA_TRY(launch_pdl(gemm_simt, dim3(grid_for(m * n)), dim3(kThreads), 0, st, m, n, k, a, as_m, as_k, b, bs_k, bs_n, c, ldc, bias, act));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

@@ -1270,7 +1270,7 @@ struct DenseProb : KRange {
   __device__ __forceinline__ void store(int m, int n, float v) const {
     if (m >= M || n >= N) return;
     switch (epi) {
-      case EPI_BIAS_ACT: c[m * ldc + n] = epi_act(act, v + bias[n]); break;
+      case EPI_BIAS_ACT: c[m * ldc + n] = epi_act(act, bias ? v + bias[n] : v); break;
       case EPI_DACT: {
         const int64_t i = m * ldc + n;
         c[i] = yprev ? v * epi_dact(act, __ldg(yprev + i)) : v;
@@ -1817,6 +1817,18 @@ int slab_conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* wt, float
   p.sc_off = s.sc_off;
   p.sc_n = s.sc_n;
   return run(p, s.pl, false, Workspace{}, st, s.slab);
+}
+
+// C[m][n] (ldc) = act(sum_k A(m,k) B(k,n) + bias[n]); A(m,k) = a[m*as_m + k*as_k],
+// B(k,n) = b[k*bs_k + n*bs_n]
+int gemm(int64_t m, int64_t n, int64_t k, const float* a, int64_t as_m, int64_t as_k,
+         const float* b, int64_t bs_k, int64_t bs_n, float* c, int64_t ldc, const float* bias,
+         int act, bool split3, const Workspace& ws, cudaStream_t st) {
+  if (!fits_i32(m) || !fits_i32(n) || !fits_i32(k))
+    return fail(VCNN_ESHAPE, "gemm: extent exceeds 2^31");
+  return run(dense_prob((int)m, (int)n, (int)k, a, as_m, as_k, b, bs_n, bs_k, -1, EPI_BIAS_ACT, c,
+                        ldc, bias, act, nullptr, nullptr),
+             make_plan(m, n, k, 0), split3, ws, st);
 }
 
 int matmul(int64_t m, int64_t k, int64_t n, const float* a, const float* b, float* c,

@@ -89,6 +89,26 @@ def matmul_transB(a, b, precision=Precision.tf32):
     return c
 
 
+def gemm(a, b, trans_a=False, trans_b=False, bias=None, act=Activation.identity,
+         precision=Precision.tf32):
+    """vcnn_gemm: act(op(a) @ op(b) + bias) (op = transpose when trans_*)."""
+    a = _cuda(a, name="a")
+    b = _cuda(b, name="b")
+    m, k = (a.shape[1], a.shape[0]) if trans_a else (a.shape[0], a.shape[1])
+    kb, n = (b.shape[1], b.shape[0]) if trans_b else (b.shape[0], b.shape[1])
+    if kb != k:
+        raise ShapeError(f"gemm: inner extents {k} and {kb} differ")
+    if bias is not None:
+        bias = _cuda(bias, name="bias")
+        if bias.numel() != n:
+            raise ShapeError("gemm: bias must have n entries")
+    c = _empty(m, n)
+    check(lib().vcnn_gemm(int(trans_a), int(trans_b), m, n, k, _p(a), a.shape[1], _p(b),
+                          b.shape[1], _p(c), n, _p(bias) if bias is not None else None,
+                          int(act), int(precision), _stream()))
+    return c
+
+
 def accumulate_by_index(values, source, target, target_len, reducer="sum"):
     """accumulate_by_index (tensor.hpp:228-266)."""
     values = _cuda(values, name="values")

@@ -263,3 +263,27 @@ def test_geometry_errors():
         ops.pool_geometry(2, 2, 1, 1, 3, 3, 1)
     with pytest.raises(ShapeError):
         ops.conv_forward(T(np.zeros((1, 3, 3, 3))), T(np.zeros((1, 4))), T(np.zeros(1)), 2, 2)
+
+
+@pytest.mark.parametrize("prec", ALL_PREC, ids=lambda p: p.name)
+def test_gemm_transposes_bias_act(prec):
+    """vcnn_gemm: every trans_a / trans_b combination, bias + act
+    epilogue, vs the oracle's matmul / matmul_transB on explicit transposes."""
+    rng = np.random.default_rng(9)
+    m, k, n = 37, 300, 45
+    for ta in (False, True):
+        for tb in (False, True):
+            # pre-activations O(1) (a saturated tanh hides nothing but turns the
+            # normwise error of the output into an absolute one)
+            a = (rng.uniform(-1, 1, (k, m) if ta else (m, k)) * 3 / np.sqrt(k)).astype(np.float32)
+            b = rng.uniform(-1, 1, (n, k) if tb else (k, n)).astype(np.float32)
+            bias = rng.uniform(-1, 1, n).astype(np.float32)
+            am = f32(a).T if ta else f32(a)
+            bm = f32(b).T if tb else f32(b)
+            ref = O.matmul(np.ascontiguousarray(am), np.ascontiguousarray(bm))
+            for act in (A.identity, A.relu, A.tanh):
+                c = ops.gemm(T(a), T(b), ta, tb, T(bias), act, prec)
+                want = O.activate(act, ref + f32(bias))
+                assert_close(H(c), want, TOL[prec], f"gemm ta={ta} tb={tb} {act.name}")
+    c = ops.gemm(T([[1.0, 2.0], [3.0, 4.0]]), T([[5.0], [6.0]]), precision=prec)
+    assert H(c).ravel().tolist() == [17, 39]
