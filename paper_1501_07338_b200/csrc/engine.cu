@@ -567,6 +567,13 @@ void drop_graph(vcnn_net* n) {
 
 int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   const int64_t before = g_launches.load();
+  struct PdlScope {  // breakdown mode: ops timed one at a time
+    bool saved;
+    explicit PdlScope(bool off) : saved(pdl_enabled()) {
+      if (off) pdl_enabled() = false;
+    }
+    ~PdlScope() { pdl_enabled() = saved; }
+  } pdl_scope(n->breakdown);
   const int tail = tail_fused(n, batch);
   TRY(run_forward(n, batch, tail));
   TRY(run_backward(n, batch, tail));
