@@ -26,6 +26,10 @@
 // gradient may be routed on the fly from a fused pool (GradSrc), epilogue
 // multiplies the upstream activation derivative -- conv_backward_core dX
 // (layers.hpp:179) + apply_activation_grad (layers.hpp:57-61).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
 #include <string>
 #include <type_traits>
 #include <vector>
@@ -58,6 +62,9 @@ struct Geo {
   int off_b, off_raw, off_win, off_a, smem;  // shared-memory layout (bytes)
   int off_yp;              // dgrad: the image's yprev planes (act' in the epilogue), -1: none
   int raw_n, win_n;        // floats: raw input image, window scratch (routed dgrad)
+  int tma;                 // 1: the slab arrives by ONE tensor TMA from a tf32 NHWC copy
+  int rows;                // tma: staged super-grid rows (NP = rows * Wg)
+  int wchunk, nbuf;        // weights streamed per kernel row ky: bytes per row, ring depth
 };
 
 // pack layout per N block: [s = ky*kw+kx][cg][BN/8][2][8][4] (K-major
@@ -67,7 +74,7 @@ __host__ __device__ inline int64_t pack_floats_per_block(const Geo& g) {
   return (int64_t)g.kh * g.kw * g.CG * g.BN * 8;
 }
 
-bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
+bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int tma = 0) {
   g = Geo{};
   if (d.s != 1) return false;
   g.mode = mode;
@@ -101,6 +108,16 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   g.CG = (int)cdiv(g.Cin, 8);
   const int maxsh = (g.kh - 1) * g.Wg + g.kw - 1;
   g.NP = (int)cdiv(maxsh + BM, 8) * 8;
+  if (tma) {
+    // the tensor map box [2*CG quads][rows][Wg][4 channels] is the slab itself
+    // (positions P = row * Wg + x, out-of-image positions zero-filled by TMA)
+    if (mode == 1 && pool) return false;  // a routed gradient is scattered in smem
+    if (g.Cin % 4 || g.Wg > 256 || 2 * g.CG > 256) return false;
+    g.tma = 1;
+    g.rows = (int)cdiv(maxsh + BM, g.Wg);
+    if (g.rows > 256) return false;
+    g.NP = g.rows * g.Wg;
+  }
   // the input image and the window arrays go in with single bulk copies
   if ((g.Cin * g.Hin * g.Win) % 4 != 0) return false;
   if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
@@ -108,8 +125,8 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   // dgrad always reserves window scratch for a >= 2x2 pool, so the routed
   // and unrouted plans (and the weight pack) share one BN
   if (mode == 1) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
-  const int a_bytes = g.CG * 2 * g.NP * 16 + 4 * g.NP;  // slab + position table
-  const int raw_bytes = 4 * g.raw_n;
+  const int a_bytes = g.CG * 2 * g.NP * 16 + (g.tma ? 0 : 4 * g.NP);  // slab + position table
+  const int raw_bytes = g.tma ? 0 : 4 * g.raw_n;
   const int win_bytes = 2 * 4 * g.win_n;
   if (raw_bytes > 96 * 1024) return false;
   // dgrad: stage the whole image's yprev (C x H x W) with one bulk copy so
@@ -117,7 +134,12 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
   const int yp_floats = mode == 1 ? g.Cout * g.Hout * g.Wout : 0;
   const int yp_bytes = (yp_floats % 4 == 0 && 4 * yp_floats <= 48 * 1024) ? 4 * yp_floats : 0;
   for (int bn = g.Cout > 128 ? 128 : (int)((g.Cout + 15) / 16 * 16); bn >= 16; bn -= 16) {
-    const int b_bytes = g.kh * g.kw * g.CG * bn * 32;
+    // the pack streams through a 2-deep ring of kernel rows (ky) instead of
+    // being staged whole: the CTA fits 2-3 times per SM, so one CTA's MMAs
+    // overlap the others' staging and epilogues
+    const int wchunk = g.kw * g.CG * bn * 32;
+    const int nbuf = g.kh >= 2 ? 2 : 1;
+    const int b_bytes = nbuf * wchunk;
     // the epilogue tile [bn][128] reuses raw + window + A (all dead by then)
     const int ep_bytes = bn * EPS * 4;
     const int tail = raw_bytes + win_bytes + a_bytes > ep_bytes ? raw_bytes + win_bytes + a_bytes
@@ -127,11 +149,13 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g) {
     if (stage_yp) total += yp_bytes;
     if ((size_t)total + 512 <= kSmemOptin) {
       g.BN = bn;
+      g.wchunk = wchunk;
+      g.nbuf = nbuf;
       g.nblk = (int)cdiv(g.Cout, bn);
       g.off_b = 0;
       g.off_raw = b_bytes;
       g.off_win = g.off_raw + raw_bytes;
-      g.off_a = g.off_win + win_bytes;
+      g.off_a = g.off_win + win_bytes;  // (tma: == off_raw, the epilogue tile reuses the slab)
       g.off_yp = stage_yp ? b_bytes + tail : -1;
       g.smem = total;
       return (int64_t)g.B * g.tpi < (1 << 24);
@@ -191,7 +215,8 @@ struct BwdEpi {
   int act_prev;
 };
 
-struct Args {
+struct alignas(64) Args {
+  CUtensorMap tmap;    // tma mode: the NHWC tf32 input, dims (4, W, H, C/4, B)
   Geo g;
   const float* in;     // x (fwd) or materialised G (dgrad), NCHW
   GradSrc gs;          // dgrad: routed gradient (gs.pool)
@@ -336,14 +361,24 @@ __device__ unsigned long long g_dphase[8][8];
   } while (0)
 #endif
 
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, int c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+      "r"(ptx::smem_u32(bar))
+      : "memory");
+}
+
 template <int TMEM_COLS>
-__global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
+__global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constant__ Args a) {
   pdl_launch_dependents();
   const Geo& g = a.g;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  __shared__ uint64_t load_bar, done_bar;
+  __shared__ uint64_t load_bar, done_bar, wfull[2], wempty[2];
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, nb = blockIdx.y;
@@ -363,20 +398,32 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
   const int64_t pk_per = pack_floats_per_block(g);
   const bool routed = g.mode == 1 && a.gs.pool;
   const int wsz = routed ? a.gs.POH * a.gs.POW * g.Cin : 0;
+  const float* pack = a.pack + nb * pk_per;
   if (tid == 0) {
     ptx::mbar_init(&load_bar, 1);
     ptx::mbar_init(&done_bar, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&wfull[i], 1);
+      ptx::mbar_init(&wempty[i], 1);
+    }
     ptx::fence_mbar_init();
-    uint32_t bytes = (uint32_t)(pk_per * 4);
-    ptx::mbar_expect_tx(&load_bar, bytes);
-    ptx::bulk_g2s(s_b, a.pack + nb * pk_per, bytes, &load_bar);
+    // kernel rows 0 (and 1) of the pack into the ring
+    for (int ky = 0; ky < g.nbuf; ++ky) {
+      ptx::mbar_arrive_expect_tx(&wfull[ky], (uint32_t)g.wchunk);
+      ptx::bulk_g2s(s_b + (uint32_t)(ky * g.wchunk), pack + (int64_t)ky * (g.wchunk / 4),
+                    (uint32_t)g.wchunk, &wfull[ky]);
+    }
     if (g.off_yp >= 0 && a.be.yprev) {
       const uint32_t yb = 4u * (uint32_t)(g.Cout * g.Hout * g.Wout);
       ptx::mbar_expect_tx(&load_bar, yb);
       ptx::bulk_g2s(sbase + g.off_yp, a.be.yprev + (int64_t)b * g.Cout * g.Hout * g.Wout, yb,
                     &load_bar);
     }
-    if (!routed) {
+    if (g.tma) {  // the whole slab, one tensor copy (zero fill outside the image)
+      const uint32_t ab = 16u * (uint32_t)(2 * g.CG * g.NP);
+      ptx::mbar_expect_tx(&load_bar, ab);
+      tma_load_5d(s_a, &a.tmap, 0, -g.pad_x, r0 - g.pad_y, 0, b, &load_bar);
+    } else if (!routed) {
       const uint32_t rb = 4u * (uint32_t)(g.Cin * g.Hin * g.Win);
       ptx::mbar_expect_tx(&load_bar, rb);
       ptx::bulk_g2s(s_raw, a.in + (int64_t)b * g.Cin * g.Hin * g.Win, rb, &load_bar);
@@ -409,7 +456,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
   // position -> offset in the staged image (-1 outside it), one division per
   // position; then thread -> (position, channel%4), 8 positions x 16 B per
   // 128-byte warp store (conflict-free)
-  {
+  if (!g.tma) {
     int* pos_off = reinterpret_cast<int*>(smem + g.off_a) + g.CG * 2 * g.NP * 4;
     for (int P = tid; P < g.NP; P += NT) {
       const int yy = r0 + P / g.Wg - g.pad_y, xx = P % g.Wg - g.pad_x;
@@ -467,11 +514,13 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
     // descriptors advance by plain additions on the start-address field
     // (16-byte units): A by the shift and the channel group, B by its block
     const uint64_t a0 = ptx::interleave_desc(s_a, half, 128u);
-    const uint64_t b0 = ptx::interleave_desc(s_b, 128u, 256u);
     const uint64_t a_cg = (uint64_t)(2u * half >> 4), b_blk = (uint64_t)(g.BN * 32 >> 4);
-    uint64_t bd = b0;
     uint32_t acc = 0;
     for (int ky = 0; ky < g.kh; ++ky) {
+      const int buf = g.nbuf == 2 ? (ky & 1) : 0;
+      ptx::mbar_wait(&wfull[buf], (uint32_t)(g.nbuf == 2 ? (ky >> 1) : ky) & 1u);
+      ptx::tc_fence_after();
+      uint64_t bd = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u);
       for (int kx = 0; kx < g.kw; ++kx) {
         uint64_t ad = a0 + (uint64_t)(ky * g.Wg + kx);
         for (int cg = 0; cg < g.CG; ++cg) {
@@ -481,8 +530,18 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const Args a) {
           bd += b_blk;
         }
       }
+      ptx::mma_commit(&wempty[buf]);  // this kernel row's pack slot is free once read
     }
     ptx::mma_commit(&done_bar);
+  } else if (warp == 1 && ptx::elect_one()) {
+    // refill the ring: kernel row ky once row ky - nbuf's MMAs have read its slot
+    for (int ky = g.nbuf; ky < g.kh; ++ky) {
+      const int buf = g.nbuf == 2 ? (ky & 1) : 0;
+      ptx::mbar_wait(&wempty[buf], (uint32_t)((ky - g.nbuf) / g.nbuf) & 1u);
+      ptx::mbar_arrive_expect_tx(&wfull[buf], (uint32_t)g.wchunk);
+      ptx::bulk_g2s(s_b + (uint32_t)(buf * g.wchunk), pack + (int64_t)ky * (g.wchunk / 4),
+                    (uint32_t)g.wchunk, &wfull[buf]);
+    }
   }
   __syncwarp();
   if (warp == 0) ptx::mbar_wait(&done_bar, 0);  // the other warps park at the barrier
@@ -788,6 +847,10 @@ namespace {
 constexpr int FT = 256;   // 8 warps
 constexpr int kTilesPerWarp = 2;
 constexpr int kTilesPerCta = (FT / 32) * kTilesPerWarp;
+// row stride (floats) of the CTA's pooled [map][window] stage: one pad word so
+// both the [map][window] (NCHW) and the [window][map] (NHWC) reads are
+// conflict-free
+constexpr int kSoStride = kTilesPerCta * 4 + 1;
 struct FGeo {
   int B, C, H, W, K, kh, kw, OH, OW;
   int Kd, nks, nnt;   // columns, K steps (8), N tiles (8 maps)
@@ -828,7 +891,7 @@ bool fplan_small(const ConvDesc& d, int pool, FGeo& g) {
   g.S = (g.nmt + kTilesPerCta - 1) / kTilesPerCta;
   g.off_w = (4 * (d.C + 1) * hw + 127) & ~127;
   g.off_o = (g.off_w + 4 * g.nnt * 8 * g.wst + 127) & ~127;
-  const int ob = 8 * d.K * kTilesPerCta * 4;  // pooled values + args of the CTA's windows
+  const int ob = 8 * d.K * kSoStride;  // pooled values + args of the CTA's windows
   g.smem = g.off_o + ob + 128;
   if (g.smem > 227 * 1024) return false;
   return true;
@@ -843,6 +906,7 @@ struct FSArgs {
   float* y;        // [B][K][OH][OW] (unpooled)
   float* py;       // [B][K][POH][POW] (pooled)
   int32_t* parg;
+  float* pyn;      // nullable: [B][POH*POW][K] pooled, tf32 (the next direct conv's TMA input)
 };
 
 __device__ __forceinline__ void mma_tf32_m16n8k8(float (&c)[4], uint32_t a0, uint32_t a1,
@@ -1021,9 +1085,8 @@ __global__ void __launch_bounds__(FT) conv_small_fwd_kernel(const FSArgs a) {
         if (wi < PP && n < g.K) {
           const int q = (2 * wpy + (bi >> 1)) * g.OW + 2 * wpx + (bi & 1);
           const int wl = wloc0 + p * 4 + (gq & 3);
-          so[n * kTilesPerCta * 4 + wl] = best;
-          reinterpret_cast<int32_t*>(so)[(g.K + n) * kTilesPerCta * 4 + wl] =
-              (b * g.K + n) * ohw + q;
+          so[n * kSoStride + wl] = best;
+          reinterpret_cast<int32_t*>(so)[(g.K + n) * kSoStride + wl] = (b * g.K + n) * ohw + q;
         }
       }
     }
@@ -1037,9 +1100,14 @@ __global__ void __launch_bounds__(FT) conv_small_fwd_kernel(const FSArgs a) {
       const int n = i / CW, r = i - n * CW;
       if (r >= nw) continue;
       const int64_t o = ((int64_t)b * g.K + n) * PP + w0 + r;
-      a.py[o] = so[n * CW + r];
-      a.parg[o] = reinterpret_cast<const int32_t*>(so)[(g.K + n) * CW + r];
+      a.py[o] = so[n * kSoStride + r];
+      a.parg[o] = reinterpret_cast<const int32_t*>(so)[(g.K + n) * kSoStride + r];
     }
+    if (a.pyn)  // channels innermost: one contiguous run of K per window
+      for (int i = tid; i < g.K * nw; i += FT) {
+        const int r = i / g.K, n = i - r * g.K;
+        a.pyn[((int64_t)b * PP + w0 + r) * g.K + n] = ptx::to_tf32(so[n * kSoStride + r]);
+      }
   }
 }
 
@@ -1112,6 +1180,7 @@ int conv_fwd_small(const ConvDesc& d, const float* x, const float* w, const floa
   a.y = y;
   a.py = pf.y;
   a.parg = pf.arg;
+  a.pyn = pf.y_nhwc;
   switch (act) {
     case VCNN_ACT_RELU: return launch_small_fwd<VCNN_ACT_RELU>(a, st);
     case VCNN_ACT_SIGMOID: return launch_small_fwd<VCNN_ACT_SIGMOID>(a, st);
@@ -1120,11 +1189,59 @@ int conv_fwd_small(const ConvDesc& d, const float* x, const float* w, const floa
   }
 }
 
+// ---- tf32 NHWC inputs for the tensor-TMA slab ----------------------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+}  // namespace
+
+bool fwd_tma_ok(const ConvDesc& d, int pool) {
+  Geo g;
+  return plan(d, 0, pool, 0, 0, g, 1);
+}
+
+size_t nhwc_map_bytes() { return sizeof(CUtensorMap); }
+
+// the forward slab's tensor map over x_nhwc [B][H][W][C] (tf32 values):
+// dims (4 channels, W, H, C/4, B), box (4, Wg, rows, 2*CG, 1)
+int make_nhwc_map(const ConvDesc& d, const float* x_nhwc, void* map) {
+  Geo g;
+  if (!plan(d, 0, 0, 0, 0, g, 1)) return fail(VCNN_ESHAPE, "nhwc map: geometry not supported");
+  auto enc = encode_fn();
+  if (!enc) return fail(VCNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[5] = {4, (cuuint64_t)d.W, (cuuint64_t)d.H, (cuuint64_t)(d.C / 4),
+                              (cuuint64_t)d.B};
+  const cuuint64_t strides[4] = {(cuuint64_t)d.C * 4, (cuuint64_t)d.W * d.C * 4, 16,
+                                 (cuuint64_t)d.H * d.W * d.C * 4};
+  const cuuint32_t box[5] = {4, (cuuint32_t)g.Wg, (cuuint32_t)g.rows, (cuuint32_t)(2 * g.CG), 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = enc(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5,
+                   const_cast<float*>(x_nhwc), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(VCNN_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return VCNN_OK;
+}
+
 int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bias, int act,
-             float* y, const PoolFuse& pf, cudaStream_t st) {
+             float* y, const PoolFuse& pf, cudaStream_t st, const void* nhwc_map) {
   Args a{};
-  if (!plan(d, 0, pf.pool, pf.POH, pf.POW, a.g))
+  if (nhwc_map && plan(d, 0, pf.pool, pf.POH, pf.POW, a.g, 1)) {
+    std::memcpy(&a.tmap, nhwc_map, sizeof(CUtensorMap));
+  } else if (!plan(d, 0, pf.pool, pf.POH, pf.POW, a.g)) {
     return fail(VCNN_ESHAPE, "direct conv forward: geometry not supported");
+  }
   a.in = x;
   a.pack = pk;
   a.fe.bias = bias;

@@ -17,6 +17,7 @@
 // activation passes.  A whole train step can be captured once into a CUDA
 // graph and replayed.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -44,6 +45,13 @@ struct LayerRt {
   float* pf = nullptr;
   float* pd = nullptr;
   float* ps = nullptr;  // small-Kd forward weight image (tf32, padded)
+  // tensor-TMA input path: a pool output also kept as tf32 NHWC (written by
+  // the producing fused conv+pool kernel; `nhwc_fresh` = written this step),
+  // and the consuming conv's tensor map over it
+  float* nhwc = nullptr;
+  bool nhwc_fresh = false;
+  bool has_tmap = false;
+  alignas(64) unsigned char tmap[128] = {};
 };
 
 // host Rng identical to the reference (common.hpp:51-66): mt19937_64 with
@@ -281,6 +289,9 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
                            n->precision, n->ws, st);
   if (!fpool && k1::fwd_ok(d))  // K = 1: exact fp32 direct conv (N = 1 GEMM)
     return k1::conv_fwd(d, in, W, b, l.spec.act, l.out, st);
+  // the input as a tf32 NHWC copy written this step by the producer: the
+  // direct kernel stages its slab with one tensor TMA
+  const void* map = (i >= 1 && l.has_tmap && n->L[i - 1].nhwc_fresh) ? l.tmap : nullptr;
   if (fpool) {
     LayerRt& p = n->L[i + 1];
     PoolFuse pf;
@@ -289,16 +300,19 @@ int conv_forward(vcnn_net* n, size_t i, int B, const float* in, int fpool) {
     pf.POW = p.out_w;
     pf.y = p.out;
     pf.arg = p.arg;
-    if (direct::small_fwd_ok(d, fpool))
+    if (direct::small_fwd_ok(d, fpool)) {
+      pf.y_nhwc = p.nhwc;
+      p.nhwc_fresh = p.nhwc != nullptr;
       return direct::conv_fwd_small(d, in, W, b, l.spec.act, nullptr, pf, st, l.ps);
+    }
     if (l.pf && direct::fwd_ok(d, fpool))
-      return direct::conv_fwd(d, in, l.pf, b, l.spec.act, nullptr, pf, st);
+      return direct::conv_fwd(d, in, l.pf, b, l.spec.act, nullptr, pf, st, map);
     return tc::slab_conv_fwd(d, in, l.wf, b, l.spec.act, nullptr, pf, st);
   }
   if (n->precision == VCNN_PREC_TF32 && direct::small_fwd_ok(d, 0))
     return direct::conv_fwd_small(d, in, W, b, l.spec.act, l.out, PoolFuse{}, st, l.ps);
   if (n->precision == VCNN_PREC_TF32 && l.pf && direct::fwd_ok(d, 0))
-    return direct::conv_fwd(d, in, l.pf, b, l.spec.act, l.out, PoolFuse{}, st);
+    return direct::conv_fwd(d, in, l.pf, b, l.spec.act, l.out, PoolFuse{}, st, map);
   return launch_conv_fwd(d, in, W, b, l.spec.act, l.out, n->precision, n->ws, st, l.wf);
 }
 
@@ -324,6 +338,7 @@ int tail_fused(const vcnn_net* n, int B) {
 
 int run_forward(vcnn_net* n, int B, int skip_top = 0) {
   const cudaStream_t st = n->stream;
+  for (LayerRt& l : n->L) l.nhwc_fresh = false;
   const size_t nl = n->L.size() - (size_t)skip_top;
   for (size_t i = 0; i < nl; ++i) {
     LayerRt& l = n->L[i];
@@ -882,6 +897,22 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
       if (need > wsb) wsb = need;
     }
   }
+  // conv i fed by pool i-1 of a small-Kd conv+pool pair (i-2): the pair also
+  // writes the pooled output as tf32 NHWC, which conv i stages with one TMA
+  const bool tma_off = getenv("VCNN_NO_TMA_SLAB") != nullptr;  // A/B experiments
+  for (size_t i = 2; i < n->L.size() && !s && !tma_off; ++i) {
+    LayerRt& c = n->L[i];
+    LayerRt& p = n->L[i - 1];
+    const LayerRt& q = n->L[i - 2];
+    if (c.spec.kind != VCNN_LAYER_CONV || !c.pf || p.spec.kind != VCNN_LAYER_POOL ||
+        q.spec.kind != VCNN_LAYER_CONV || conv_is_dense(c))
+      continue;
+    if (!direct::small_fwd_ok(conv_of(q, max_batch), p.spec.kh)) continue;
+    const ConvDesc dc = conv_of(c, max_batch);
+    if (!direct::fwd_tma_ok(dc, 0) || direct::nhwc_map_bytes() > sizeof(c.tmap)) continue;
+    s = dalloc((void**)&p.nhwc, sizeof(float) * (size_t)(p.out_per * max_batch));
+    if (!s && direct::make_nhwc_map(dc, p.nhwc, c.tmap) == VCNN_OK) c.has_tmap = true;
+  }
   if (wsb) {
     s = s ? s : dalloc((void**)&n->ws.ptr, wsb);
     n->ws.bytes = wsb;
@@ -935,6 +966,7 @@ int vcnn_net_destroy(vcnn_net* n) {
     cudaFree(l.pf);
     cudaFree(l.pd);
     cudaFree(l.ps);
+    cudaFree(l.nhwc);
   }
   cudaFree(n->params);
   cudaFree(n->grads);

@@ -166,6 +166,7 @@ struct PoolFuse {
   int POH = 0, POW = 0;
   float* y = nullptr;
   int32_t* arg = nullptr;
+  float* y_nhwc = nullptr;  // small-Kd forward: also the pooled output as tf32 NHWC
 };
 
 // data-parallel exchange + update (dp.cu): the replicas' gradient buffers
@@ -220,8 +221,13 @@ bool dgrad_ok(const ConvDesc& d, int pool = 0, int POH = 0, int POW = 0);
 // prepacked tf32 weights: mode 0 forward, 1 dgrad (0 floats: not supported)
 size_t pack_floats(const ConvDesc& d, int mode);
 int pack_weights(const ConvDesc& d, int mode, const float* w, float* pk, cudaStream_t st);
+// nhwc_map (nullable, nhwc_map_bytes()): the input as a tf32 NHWC copy
+// through a tensor map (make_nhwc_map): the slab is one TMA, no build
 int conv_fwd(const ConvDesc& d, const float* x, const float* pk, const float* bias, int act,
-             float* y, const PoolFuse& pf, cudaStream_t st);
+             float* y, const PoolFuse& pf, cudaStream_t st, const void* nhwc_map = nullptr);
+bool fwd_tma_ok(const ConvDesc& d, int pool);
+size_t nhwc_map_bytes();
+int make_nhwc_map(const ConvDesc& d, const float* x_nhwc, void* map);
 int conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* pk, float* dx,
                const float* yprev, int act_prev, cudaStream_t st);
 // sgd_step fused with the refresh of the conv layers' packs (pf / pd may be
