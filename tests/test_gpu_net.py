@@ -399,7 +399,7 @@ def test_big_batch_and_presets_run():
         net.close()
 
 
-@pytest.mark.parametrize("name,B", [("cifar3", 128), ("cifar3", 37), ("lenet-caffe", 100),
+@pytest.mark.parametrize("name,B", [("cifar3", 128), ("cifar3", 37), ("cifar3", 512), ("lenet-caffe", 100),
                                     ("scale1-analog", 8)])
 def test_fused_path_bitwise_equals_trace_path(name, B):
     """conv->max-pool fusion (pool in the conv epilogue, pool backward routed
