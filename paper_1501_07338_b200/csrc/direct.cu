@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -64,7 +65,10 @@ struct Geo {
   int raw_n, win_n;        // floats: raw input image, window scratch (routed dgrad)
   int tma;                 // 1: the slab arrives by ONE tensor TMA from a tf32 NHWC copy
   int rows;                // tma: staged super-grid rows (NP = rows * Wg)
-  int wchunk, nbuf;        // weights streamed per kernel row ky: bytes per row, ring depth
+  int wchunk, nbuf;        // weights streamed in chunks of SC shifts: bytes per chunk, ring depth
+  int SC, nchunk;          // shifts (ky,kx) per chunk, chunks
+  int seg, nseg, segw;     // 1-D row segments (kh == 1, rows wider than a tile): segments
+                           // per output row, outputs per segment
 };
 
 // pack layout per N block: [s = ky*kw+kx][cg][BN/8][2][8][4] (K-major
@@ -72,6 +76,12 @@ struct Geo {
 // SBO = 256 B between 8-row groups)
 __host__ __device__ inline int64_t pack_floats_per_block(const Geo& g) {
   return (int64_t)g.kh * g.kw * g.CG * g.BN * 8;
+}
+
+// bytes of pack chunk c (the last chunk may hold fewer shifts)
+__host__ __device__ inline uint32_t chunk_bytes(const Geo& g, int c) {
+  const int s1 = (c + 1) * g.SC < g.kh * g.kw ? (c + 1) * g.SC : g.kh * g.kw;
+  return (uint32_t)((s1 - c * g.SC) * g.CG * g.BN * 32);
 }
 
 bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int tma = 0) {
@@ -88,13 +98,24 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     g.Cin = d.K, g.Hin = d.OH, g.Win = d.OW, g.Cout = d.C;
     g.Wg = d.W + d.kw - 1, g.Hout = d.H, g.Wout = d.W, g.pad_y = d.kh - 1, g.pad_x = d.kw - 1;
   }
-  if (g.Wg > BM || g.Hout < 1) return false;
+  if (g.Hout < 1) return false;
+  if (g.Wg > BM) {
+    // rows wider than a tile: a 1-D kernel (kh == 1, e.g. the 1x121 layer of
+    // the deconvolution net) tiles each output row into segments of <= 128
+    // positions; the slab is the row segment plus the kw-1 halo, staged
+    // straight from global memory
+    if (d.kh != 1 || pool || tma || g.Wg > 4096) return false;
+    g.seg = 1;
+  }
   // a forward view with < 4 input channels pads the MMA K (8 channels) by 2x
   // or more; those layers go to the small-Kd kernel or the generic implicit GEMM
   if (mode == 0 && g.Cin < 4) return false;
-  int R = BM / g.Wg;
+  int R = g.seg ? 1 : BM / g.Wg;
   if (R > g.Hout) R = g.Hout;
-  if (pool && mode == 0) {  // the forward epilogue pools whole windows of its tile
+  if (g.seg) {
+    g.nseg = (int)cdiv(g.Wout, BM);
+    g.segw = (int)cdiv(g.Wout, g.nseg);
+  } else if (pool && mode == 0) {  // the forward epilogue pools whole windows of its tile
     R = (R / pool) * pool;
     if (R < 1) return false;
     // balanced: as few tiles as before, window rows spread evenly over them
@@ -104,9 +125,9 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     R = (int)cdiv(g.Hout, cdiv(g.Hout, R));  // balanced row blocks
   }
   g.R = R;
-  g.tpi = (int)cdiv(g.Hout, R);
+  g.tpi = (int)cdiv(g.Hout, R) * (g.seg ? g.nseg : 1);
   g.CG = (int)cdiv(g.Cin, 8);
-  const int maxsh = (g.kh - 1) * g.Wg + g.kw - 1;
+  const int maxsh = g.seg ? g.kw - 1 : (g.kh - 1) * g.Wg + g.kw - 1;
   g.NP = (int)cdiv(maxsh + BM, 8) * 8;
   if (tma) {
     // the tensor map box [2*CG quads][rows][Wg][4 channels] is the slab itself
@@ -119,26 +140,31 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     g.NP = g.rows * g.Wg;
   }
   // the input image and the window arrays go in with single bulk copies
-  if ((g.Cin * g.Hin * g.Win) % 4 != 0) return false;
+  if (!g.seg && (g.Cin * g.Hin * g.Win) % 4 != 0) return false;
   if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
   g.raw_n = g.Cin * g.Hin * g.Win;
   // dgrad always reserves window scratch for a >= 2x2 pool, so the routed
   // and unrouted plans (and the weight pack) share one BN
-  if (mode == 1) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
-  const int a_bytes = g.CG * 2 * g.NP * 16 + (g.tma ? 0 : 4 * g.NP);  // slab + position table
-  const int raw_bytes = g.tma ? 0 : 4 * g.raw_n;
+  if (mode == 1 && !g.seg) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
+  const int a_bytes = g.CG * 2 * g.NP * 16 + (g.tma || g.seg ? 0 : 4 * g.NP);  // slab + table
+  const int raw_bytes = g.tma || g.seg ? 0 : 4 * g.raw_n;
   const int win_bytes = 2 * 4 * g.win_n;
   if (raw_bytes > 96 * 1024) return false;
   // dgrad: stage the whole image's yprev (C x H x W) with one bulk copy so
   // the epilogue's activation derivative reads shared memory
-  const int yp_floats = mode == 1 ? g.Cout * g.Hout * g.Wout : 0;
+  const int yp_floats = mode == 1 && !g.seg ? g.Cout * g.Hout * g.Wout : 0;
   const int yp_bytes = (yp_floats % 4 == 0 && 4 * yp_floats <= 48 * 1024) ? 4 * yp_floats : 0;
   for (int bn = g.Cout > 128 ? 128 : (int)((g.Cout + 15) / 16 * 16); bn >= 16; bn -= 16) {
     // the pack streams through a 2-deep ring of kernel rows (ky) instead of
     // being staged whole: the CTA fits 2-3 times per SM, so one CTA's MMAs
     // overlap the others' staging and epilogues
-    const int wchunk = g.kw * g.CG * bn * 32;
-    const int nbuf = g.kh >= 2 ? 2 : 1;
+    const int shift_bytes = g.CG * bn * 32;
+    int SC = g.kw;  // one kernel row per chunk, or for a huge 1-D kernel ~30 KB
+    if (g.seg) SC = (int)std::max<int64_t>(1, (30 * 1024) / shift_bytes);
+    if (SC > g.kh * g.kw) SC = g.kh * g.kw;
+    const int nchunk = (int)cdiv(g.kh * g.kw, SC);
+    const int wchunk = SC * shift_bytes;
+    const int nbuf = nchunk >= 2 ? 2 : 1;
     const int b_bytes = nbuf * wchunk;
     // the epilogue tile [bn][128] reuses raw + window + A (all dead by then)
     const int ep_bytes = bn * EPS * 4;
@@ -151,6 +177,8 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
       g.BN = bn;
       g.wchunk = wchunk;
       g.nbuf = nbuf;
+      g.SC = SC;
+      g.nchunk = nchunk;
       g.nblk = (int)cdiv(g.Cout, bn);
       g.off_b = 0;
       g.off_raw = b_bytes;
@@ -230,7 +258,7 @@ struct alignas(64) Args {
 // map, so no thread divides by a runtime extent; stores along a row are
 // coalesced.
 template <int ACT>
-__device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) {
+__device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, int x0) {
   const Geo& g = a.g;
   const FwdEpi& e = a.fe;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,11 +266,13 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
   const int nmaps = g.Cout - n0 < g.BN ? g.Cout - n0 : g.BN;
   const int64_t ohw = (int64_t)g.Hout * g.Wout;
   const int64_t plane0 = (int64_t)b * g.Cout + n0;
+  // output columns [x0, x1) of the tile; accumulator row = r * Wg + x - x0
+  const int x1 = g.seg ? (x0 + g.segw < g.Wout ? x0 + g.segw : g.Wout) : g.Wout;
   if (e.y) {
     for (int r = warp; r < nr; r += NT / 32)
-      for (int x = lane; x < g.Wout; x += 32) {
+      for (int x = x0 + lane; x < x1; x += 32) {
         float* yp = e.y + plane0 * ohw + (int64_t)(r0 + r) * g.Wout + x;
-        const uint32_t ep = eb + 4u * (r * g.Wg + x);
+        const uint32_t ep = eb + 4u * (r * g.Wg + x - x0);
         for (int n = 0; n < nmaps; ++n)
           yp[n * ohw] = actf<ACT>(ptx::lds_f32(ep + 4u * (n * EPS)) + __ldg(e.bias + n0 + n));
       }
@@ -295,12 +325,14 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
 // warp = channel slice; the yprev loads of 16 (position, channel) pairs are
 // in flight together (read-only path).
 template <int ACT>
-__device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) {
+__device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, int x0) {
   const Geo& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nr = g.Hout - r0 < g.R ? g.Hout - r0 : g.R;
   const int nch = g.Cout - n0 < g.BN ? g.Cout - n0 : g.BN;
-  const int npix = nr * g.Wout;
+  const int x1 = g.seg ? (x0 + g.segw < g.Wout ? x0 + g.segw : g.Wout) : g.Wout;
+  const int wid = x1 - x0;  // output columns of the tile
+  const int npix = nr * wid;
   const int64_t hw = (int64_t)g.Hout * g.Wout;
   const int64_t plane0 = (int64_t)b * g.Cout + n0;
   const float* yp = a.be.yprev;
@@ -308,9 +340,9 @@ __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0) 
   const bool ys = yp && g.off_yp >= 0;
   const uint32_t s_yp = eb - (uint32_t)g.off_raw + (uint32_t)(g.off_yp < 0 ? 0 : g.off_yp);
   for (int p = lane; p < npix; p += 32) {
-    const int r = p / g.Wout, x = p - r * g.Wout;
+    const int r = p / wid, x = x0 + (p - r * wid);
     const int64_t o = plane0 * hw + (int64_t)(r0 + r) * g.Wout + x;
-    const uint32_t ep = eb + 4u * (r * g.Wg + x);
+    const uint32_t ep = eb + 4u * (r * g.Wg + x - x0);
     const int lo = (r0 + r) * g.Wout + x;  // offset inside one channel plane
     for (int c0 = warp; c0 < nch; c0 += 4 * 16) {
       float yv[16];
@@ -382,7 +414,9 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, nb = blockIdx.y;
-  const int b = tile / g.tpi, r0 = (tile - b * g.tpi) * g.R;
+  const int b = tile / g.tpi, tt = tile - b * g.tpi;
+  const int ry = g.seg ? tt / g.nseg : tt, r0 = ry * g.R;
+  const int x0 = g.seg ? (tt - ry * g.nseg) * g.segw : 0;
   const int n0 = nb * g.BN;
   const uint32_t sbase = ptx::smem_u32(smem);
   const uint32_t s_b = sbase + g.off_b, s_raw = sbase + g.off_raw, s_win = sbase + g.off_win,
@@ -407,11 +441,12 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       ptx::mbar_init(&wempty[i], 1);
     }
     ptx::fence_mbar_init();
-    // kernel rows 0 (and 1) of the pack into the ring
-    for (int ky = 0; ky < g.nbuf; ++ky) {
-      ptx::mbar_arrive_expect_tx(&wfull[ky], (uint32_t)g.wchunk);
-      ptx::bulk_g2s(s_b + (uint32_t)(ky * g.wchunk), pack + (int64_t)ky * (g.wchunk / 4),
-                    (uint32_t)g.wchunk, &wfull[ky]);
+    // pack chunks 0 (and 1) into the ring
+    for (int c = 0; c < g.nbuf; ++c) {
+      const uint32_t bytes = chunk_bytes(g, c);
+      ptx::mbar_arrive_expect_tx(&wfull[c], bytes);
+      ptx::bulk_g2s(s_b + (uint32_t)(c * g.wchunk), pack + (int64_t)c * (g.wchunk / 4), bytes,
+                    &wfull[c]);
     }
     if (g.off_yp >= 0 && a.be.yprev) {
       const uint32_t yb = 4u * (uint32_t)(g.Cout * g.Hout * g.Wout);
@@ -423,6 +458,8 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       const uint32_t ab = 16u * (uint32_t)(2 * g.CG * g.NP);
       ptx::mbar_expect_tx(&load_bar, ab);
       tma_load_5d(s_a, &a.tmap, 0, -g.pad_x, r0 - g.pad_y, 0, b, &load_bar);
+    } else if (g.seg) {
+      // (the row segment is staged by all threads below)
     } else if (!routed) {
       const uint32_t rb = 4u * (uint32_t)(g.Cin * g.Hin * g.Win);
       ptx::mbar_expect_tx(&load_bar, rb);
@@ -456,7 +493,27 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   // position -> offset in the staged image (-1 outside it), one division per
   // position; then thread -> (position, channel%4), 8 positions x 16 B per
   // 128-byte warp store (conflict-free)
-  if (!g.tma) {
+  if (g.seg) {
+    // slab position P = input column x0 + P - pad_x of row r0 - pad_y (zero
+    // outside the image); thread -> (channel quad, P): 4 coalesced row loads,
+    // one 16-byte store
+    const int yy = r0 - g.pad_y;
+    const int64_t plane = (int64_t)g.Hin * g.Win;
+    const float* src = a.in + (int64_t)b * g.Cin * plane + (int64_t)yy * g.Win;
+    const bool row_ok = yy >= 0 && yy < g.Hin;
+    for (int j = tid; j < 2 * g.CG * g.NP; j += NT) {
+      const int cq = j / g.NP, P = j - cq * g.NP;
+      const int xx = x0 + P - g.pad_x;
+      const bool ok = row_ok && xx >= 0 && xx < g.Win;
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = cq * 4 + u;
+        v[u] = (ok && c < g.Cin) ? ptx::to_tf32(__ldg(src + c * plane + xx)) : 0.f;
+      }
+      ptx::sts_f32x4(s_a + 16u * (uint32_t)j, make_float4(v[0], v[1], v[2], v[3]));
+    }
+  } else if (!g.tma) {
     int* pos_off = reinterpret_cast<int*>(smem + g.off_a) + g.CG * 2 * g.NP * 4;
     for (int P = tid; P < g.NP; P += NT) {
       const int yy = r0 + P / g.Wg - g.pad_y, xx = P % g.Wg - g.pad_x;
@@ -516,12 +573,14 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     const uint64_t a0 = ptx::interleave_desc(s_a, half, 128u);
     const uint64_t a_cg = (uint64_t)(2u * half >> 4), b_blk = (uint64_t)(g.BN * 32 >> 4);
     uint32_t acc = 0;
-    for (int ky = 0; ky < g.kh; ++ky) {
-      const int buf = g.nbuf == 2 ? (ky & 1) : 0;
-      ptx::mbar_wait(&wfull[buf], (uint32_t)(g.nbuf == 2 ? (ky >> 1) : ky) & 1u);
+    int ky = 0, kx = 0;  // shift s = ky * kw + kx, advanced incrementally
+    for (int c = 0; c < g.nchunk; ++c) {
+      const int buf = g.nbuf == 2 ? (c & 1) : 0;
+      ptx::mbar_wait(&wfull[buf], (uint32_t)(g.nbuf == 2 ? (c >> 1) : c) & 1u);
       ptx::tc_fence_after();
       uint64_t bd = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u);
-      for (int kx = 0; kx < g.kw; ++kx) {
+      const int s1 = (c + 1) * g.SC < g.kh * g.kw ? (c + 1) * g.SC : g.kh * g.kw;
+      for (int sft = c * g.SC; sft < s1; ++sft) {
         uint64_t ad = a0 + (uint64_t)(ky * g.Wg + kx);
         for (int cg = 0; cg < g.CG; ++cg) {
           ptx::mma_tf32(tmem, ad, bd, idesc, acc);
@@ -529,18 +588,23 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
           ad += a_cg;
           bd += b_blk;
         }
+        if (++kx == g.kw) {
+          kx = 0;
+          ++ky;
+        }
       }
-      ptx::mma_commit(&wempty[buf]);  // this kernel row's pack slot is free once read
+      ptx::mma_commit(&wempty[buf]);  // this chunk's pack slot is free once read
     }
     ptx::mma_commit(&done_bar);
   } else if (warp == 1 && ptx::elect_one()) {
-    // refill the ring: kernel row ky once row ky - nbuf's MMAs have read its slot
-    for (int ky = g.nbuf; ky < g.kh; ++ky) {
-      const int buf = g.nbuf == 2 ? (ky & 1) : 0;
-      ptx::mbar_wait(&wempty[buf], (uint32_t)((ky - g.nbuf) / g.nbuf) & 1u);
-      ptx::mbar_arrive_expect_tx(&wfull[buf], (uint32_t)g.wchunk);
-      ptx::bulk_g2s(s_b + (uint32_t)(buf * g.wchunk), pack + (int64_t)ky * (g.wchunk / 4),
-                    (uint32_t)g.wchunk, &wfull[buf]);
+    // refill the ring: chunk c once chunk c - nbuf's MMAs have read its slot
+    for (int c = g.nbuf; c < g.nchunk; ++c) {
+      const int buf = g.nbuf == 2 ? (c & 1) : 0;
+      ptx::mbar_wait(&wempty[buf], (uint32_t)((c - g.nbuf) / g.nbuf) & 1u);
+      const uint32_t bytes = chunk_bytes(g, c);
+      ptx::mbar_arrive_expect_tx(&wfull[buf], bytes);
+      ptx::bulk_g2s(s_b + (uint32_t)(buf * g.wchunk), pack + (int64_t)c * (g.wchunk / 4), bytes,
+                    &wfull[buf]);
     }
   }
   __syncwarp();
@@ -569,10 +633,11 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     for (int i = tid; i < 256; i += NT) g_dump[3][i] = ptx::lds_f32(s_raw + 4u * i);
 #endif
   if (g.mode == 0)
-    with_act(a.fe.act, [&](auto A) { fwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0); });
+    with_act(a.fe.act,
+             [&](auto A) { fwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0, x0); });
   else
     with_act(a.be.act_prev,
-             [&](auto A) { bwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0); });
+             [&](auto A) { bwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0, x0); });
   DPHASE(5);
   __syncthreads();
   if (warp == 0) ptx::tmem_dealloc(tmem, TMEM_COLS);
