@@ -435,6 +435,7 @@ def ref():
         L = C.CDLL(p)
         L.ref_bench_create.restype = C.c_void_p
         L.ref_bench_create.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_double]
+        L.ref_bench_set_variant.argtypes = [C.c_void_p, C.c_int]
         L.ref_bench_step.restype = C.c_float
         L.ref_bench_step.argtypes = [C.c_void_p, C.c_int]
         L.ref_bench_get_params.argtypes = [C.c_void_p, C.c_void_p]

@@ -524,6 +524,11 @@ void* ref_bench_create(const orc_net* n, int B, uint64_t data_seed, double lr, d
   }
 }
 
+// the reference's vectorization ladder (Variant::imp1..imp6, variants.hpp:71-242)
+void ref_bench_set_variant(void* h, int variant) {
+  static_cast<BenchState*>(h)->exec = Executor<float>(variant_of(variant));
+}
+
 // One training step (forward + backward + update); returns the loss.
 float ref_bench_step(void* h, int train) {
   auto* st = static_cast<BenchState*>(h);

@@ -409,7 +409,11 @@ __global__ void __launch_bounds__(NTH, 1) tc_gemm_kernel(const Prob p) {
     }
   };
   if constexpr (Prob::SMEM_EPI) {
-    // raw accumulators -> shared memory [n][BM] (the stage ring is idle now)
+    // raw accumulators -> shared memory [n][BM] (the stage ring is idle now:
+    // every stage was consumed by the MMAs done_bar tracked; the CTA barrier
+    // also orders the producers' last stage writes for tools that do not
+    // follow mbarrier / tcgen05.commit ordering, e.g. racecheck)
+    __syncthreads();
     float* ep = reinterpret_cast<float*>(smem);
     if (warp < 4) {
       const uint32_t eb = ptx::smem_u32(ep);
@@ -1451,7 +1455,7 @@ bool explicit_dgrad(const ConvDesc& d) {
   // implicit dgrad multiplies H*W/(OH*OW) times the algorithmic work; the
   // explicit one writes and re-reads the kd x pixels dP matrix (1.2 GB for
   // deconv-121's 1x121 layer: 2.0 ms GEMM + 1.4 ms col2im)
-  return (int64_t)d.H * d.W > 4 * (int64_t)d.OH * d.OW;
+  return (int64_t)d.H * d.W > 4 * (int64_t)d.OH * d.OW && fits_i32(d.kd() * d.pixels());
 }
 
 Plan plan_conv_fwd(const ConvDesc& d) { return make_plan(d.pixels(), d.K, d.kd(), 1); }
@@ -1498,8 +1502,12 @@ size_t matmul_workspace(int64_t m, int64_t k, int64_t n) {
 // ============================================================================
 // public tc:: launchers
 // ============================================================================
+// the implicit GEMMs index x, G / y and W with 32-bit offsets (no patch
+// matrix is materialised, so its size is not a limit); the explicit dgrad's
+// dP buffer is checked where it is used
 static int check_conv(const ConvDesc& d, const char* what) {
-  if (!fits_i32(d.in_size()) || !fits_i32(d.out_size()) || !fits_i32(d.kd() * d.pixels()))
+  if (!fits_i32(d.in_size()) || !fits_i32(d.out_size()) || !fits_i32(d.pixels()) ||
+      !fits_i32((int64_t)d.B * d.H * d.W) || !fits_i32(d.kd() * d.K))
     return fail(VCNN_ESHAPE, std::string(what) + ": tensor exceeds 2^31 elements");
   return VCNN_OK;
 }
@@ -1535,6 +1543,8 @@ int conv_dgrad(const ConvDesc& d, const float* gpre, const float* w, float* dx,
   if (int s = check_conv(d, "conv_dgrad")) return s;
   if (explicit_dgrad(d)) {
     // dP = W^T G (exactly the algorithmic MACs), then col2im gather (+ act')
+    if (!fits_i32(d.kd() * d.pixels()))
+      return fail(VCNN_ESHAPE, "conv_dgrad: patch gradient exceeds 2^31 elements");
     const size_t dp_bytes = align_up(sizeof(float) * (size_t)(d.kd() * d.pixels()));
     if (!ws.ptr || ws.bytes < dp_bytes) return fail(VCNN_ECUDA, "conv_dgrad: workspace too small");
     ConvDPProb p;

@@ -117,6 +117,18 @@ bool wplan(const ConvDesc& d, const GradSrc& gs, WGeo& g) {
 }
 
 #ifdef VCNN_PHASE_TIMING
+__device__ unsigned long long g_sphase[4][8];
+#define SPHASE(i)                                                              \
+  do {                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 4) g_sphase[blockIdx.x][i] = clock64(); \
+  } while (0)
+#else
+#define SPHASE(i) \
+  do {            \
+  } while (0)
+#endif
+
+#ifdef VCNN_PHASE_TIMING
 __device__ unsigned long long g_wphase[4][8];
 #define WPHASE(i)                                                             \
   do {                                                                        \
@@ -475,6 +487,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
   const int b = blockIdx.x, hw = g.H * g.W, ohw = g.ohw;
   const bool routed = a.gs.pool != 0;
   const uint32_t s_x = ptx::smem_u32(sx), s_win = ptx::smem_u32(smem + g.off_win);
+  SPHASE(0);
 
   if (tid == 0) {
     ptx::mbar_init(&load_bar, 1);
@@ -491,7 +504,9 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     sq[q] = oy * g.W + (qq - oy * g.OW);
   }
   __syncthreads();
+  SPHASE(1);
   pdl_wait();
+  SPHASE(2);
   if (tid == 0) {
     const uint32_t xb = 4u * (uint32_t)(g.C * hw);
     uint32_t tx = xb;
@@ -513,6 +528,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     }
   }
   ptx::mbar_wait(&load_bar, 0);
+  SPHASE(3);
   if (routed) {  // dP scattered to the argmax positions (global index - image base)
     const float* wv = reinterpret_cast<const float*>(smem + g.off_win);
     const int* wa = reinterpret_cast<const int*>(smem + g.off_win) + g.wsz;
@@ -524,6 +540,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
   }
   for (int i = tid; i < g.C * hw; i += ST) sx[i] = ptx::to_tf32(sx[i]);
   __syncthreads();
+  SPHASE(4);
 
   // ---- per lane: N-tile column offsets (c,ky,kx) -> c*hw + ky*W + kx ----
   const int gq = lane >> 2, t = lane & 3;
@@ -570,6 +587,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     }
   }
   __syncthreads();  // G is dead: the warps' partial tiles go over it
+  SPHASE(5);
   const int tw = MT * 16 * NT * 8;  // floats per warp tile [m][n]
   float* red = sg + warp * tw;
 #pragma unroll
@@ -592,6 +610,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     for (int w = 0; w < ST / 32; ++w) s += sg[w * tw + m * NT * 8 + j];
     part[j < g.Kd ? m * g.Kd + j : g.K * g.Kd + m] = s;
   }
+  SPHASE(6);
 }
 
 }  // namespace
@@ -687,6 +706,12 @@ int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float
 }  // namespace vcnn_b200
 
 #ifdef VCNN_PHASE_TIMING
+extern "C" int vcnn_debug_sphases(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_sphase, sizeof(unsigned long long) * 32) ==
+                 cudaSuccess
+             ? 0
+             : 4;
+}
 extern "C" int vcnn_debug_wphases(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_wphase, sizeof(unsigned long long) * 32) ==
                  cudaSuccess

@@ -48,3 +48,16 @@ try:
               "total", t[6] - t[0])
 except AttributeError:
     pass
+
+# the small-Kd weight gradient of conv1 (wgrad.cu wgrad_small_kernel)
+try:
+    L.vcnn_debug_sphases.argtypes = [C.c_void_p]
+    sb = (C.c_ulonglong * 32)()
+    L.vcnn_debug_sphases(sb)
+    sn = ["init", "pdl-wait", "load-issue+wait", "scatter+round", "mma", "reduce+store"]
+    for r in range(4):
+        t = [sb[r * 8 + i] for i in range(8)]
+        print(f"wgrad_small cta {r} " + " ".join(f"{n}={t[i + 1] - t[i]}" for i, n in enumerate(sn)),
+              "total", t[6] - t[0])
+except AttributeError:
+    pass

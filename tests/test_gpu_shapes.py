@@ -126,3 +126,27 @@ def test_sweep_bench_spec_at_batch(cell, B, prec):
     net, x, _, _ = _run(spec, B, prec)
     teacher_forced(net, spec, x, B, TOL[prec], numpy_conv=True)
     net.close()
+
+
+@pytest.mark.parametrize("cell,B", [((256, 7), 256), ((64, 11), 1024)], ids=str)
+def test_sweep_cells_beyond_2e31_patch_elements(cell, B):
+    """Sweep cells whose patch matrix (kd x pixels) exceeds 2^31 elements run
+    on the implicit GEMMs (no patch is materialised): one training step is
+    finite and the forward of an image equals the same image run alone."""
+    import torch
+    c, k = cell
+    spec = S.single_conv(channels=c, k=k)
+    x, _, v = S.synth_bench_data(spec, B, 8)
+    net = Network(spec, B)
+    _load(net, spec, x, None, v)
+    net.forward(B)
+    y_full = net.output(B)[:1]
+    net.forward_backward(B)
+    assert np.isfinite(net.loss()) and np.isfinite(net.get_grads()).all()
+    one = Network(spec, 1)
+    one.load_batch(torch.as_tensor(x[:1].reshape(1, -1), device="cuda"),
+                   values=torch.as_tensor(v[:1], device="cuda"))
+    one.forward(1)
+    assert_close(y_full, one.output(1), 1e-4, "image 0 in the big batch vs alone")
+    net.close()
+    one.close()
