@@ -403,7 +403,9 @@ __global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
 // tcgen05 slab kernel spends 5/8 of its A rows on channel padding and
 // serialises staging and MMA; here staging is one bulk copy + one scatter
 // and the MMAs run at 512 FMA/clk/SM from registers.
-constexpr int ST = 256;  // threads
+constexpr int SKG = 8;   // K groups: warps w, w + 8, ... share K steps and split N
+constexpr int SNH = 2;   // N parts (4 measured slower: 17 vs 15.7 us)
+constexpr int ST = 32 * SKG * SNH;  // threads
 constexpr int kSmallMaxCols = 96;
 
 struct SGeo {
@@ -443,7 +445,7 @@ bool splan(const ConvDesc& d, const GradSrc& gs, SGeo& g) {
   g.off_g = 0;
   const int gbytes = 4 * g.mt * 16 * g.Qs;
   const int ntb = g.nt <= 4 ? 4 : g.nt <= 8 ? 8 : 12;  // the kernel's NT bucket
-  const int red_bytes = 4 * (ST / 32) * g.mt * 16 * ntb * 8;  // reuses G
+  const int red_bytes = 4 * SKG * g.mt * 16 * ntb * 8;  // reuses G
   g.off_x = ((gbytes > red_bytes ? gbytes : red_bytes) + 127) & ~127;
   g.off_q = (g.off_x + 4 * g.xfl + 127) & ~127;
   g.off_win = (g.off_q + 4 * g.Q8 + 127) & ~127;
@@ -543,27 +545,31 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
   SPHASE(4);
 
   // ---- per lane: N-tile column offsets (c,ky,kx) -> c*hw + ky*W + kx ----
+  // warp -> (K group kg, N half nh): N tiles [nh*NTW, nh*NTW + NTW)
+  constexpr int NTW = (NT + SNH - 1) / SNH;
+  const int kg = warp % SKG, nh = warp / SKG;
   const int gq = lane >> 2, t = lane & 3;
-  int coff[NT];
+  int coff[NTW];
 #pragma unroll
-  for (int jt = 0; jt < NT; ++jt) {
+  for (int jl = 0; jl < NTW; ++jl) {
+    const int jt = nh * NTW + jl;
     const int j = jt * 8 + gq;
     if (j < g.Kd) {
       const int c = j / (g.kh * g.kw), r = j - c * g.kh * g.kw, ky = r / g.kw;
-      coff[jt] = c * hw + ky * g.W + (r - ky * g.kw);
+      coff[jl] = c * hw + ky * g.W + (r - ky * g.kw);
     } else {
-      coff[jt] = (j == g.Kd ? g.C + 1 : g.C) * hw;  // ones (bias) / zero column
+      coff[jl] = (j == g.Kd ? g.C + 1 : g.C) * hw;  // ones (bias) / zero column
     }
   }
-  float acc[MT][NT][4];
+  float acc[MT][NTW][4];
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-    for (int jt = 0; jt < NT; ++jt)
+    for (int jl = 0; jl < NTW; ++jl)
 #pragma unroll
-      for (int u = 0; u < 4; ++u) acc[mi][jt][u] = 0.f;
-  const int nt = g.nt;
-  for (int ks = warp; ks < g.ksteps; ks += ST / 32) {
+      for (int u = 0; u < 4; ++u) acc[mi][jl][u] = 0.f;
+  const int nt = g.nt - nh * NTW;  // N tiles of this half
+  for (int ks = kg; ks < g.ksteps; ks += SKG) {
     const int q0 = ks * 8 + t;
     uint32_t af[MT][4];
 #pragma unroll
@@ -576,29 +582,31 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     }
     const int p0 = sq[q0], p1 = sq[q0 + 4];
 #pragma unroll
-    for (int jt = 0; jt < NT; ++jt) {
-      if (jt < nt) {
-        const uint32_t b0 = __float_as_uint(sx[coff[jt] + p0]);
-        const uint32_t b1 = __float_as_uint(sx[coff[jt] + p1]);
+    for (int jl = 0; jl < NTW; ++jl) {
+      if (jl < nt) {
+        const uint32_t b0 = __float_as_uint(sx[coff[jl] + p0]);
+        const uint32_t b1 = __float_as_uint(sx[coff[jl] + p1]);
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
-          mma_tf32_sync(acc[mi][jt], af[mi][0], af[mi][1], af[mi][2], af[mi][3], b0, b1);
+          mma_tf32_sync(acc[mi][jl], af[mi][0], af[mi][1], af[mi][2], af[mi][3], b0, b1);
       }
     }
   }
-  __syncthreads();  // G is dead: the warps' partial tiles go over it
+  __syncthreads();  // G is dead: the K groups' partial tiles go over it
   SPHASE(5);
-  const int tw = MT * 16 * NT * 8;  // floats per warp tile [m][n]
-  float* red = sg + warp * tw;
+  const int tw = MT * 16 * NT * 8;  // floats per K-group tile [m][n]
+  float* red = sg + kg * tw;
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-    for (int jt = 0; jt < NT; ++jt) {
+    for (int jl = 0; jl < NTW; ++jl) {
+      const int jt = nh * NTW + jl;
+      if (jt >= NT) continue;
       const int m = mi * 16 + gq, n = jt * 8 + 2 * t;
-      red[m * NT * 8 + n] = acc[mi][jt][0];
-      red[m * NT * 8 + n + 1] = acc[mi][jt][1];
-      red[(m + 8) * NT * 8 + n] = acc[mi][jt][2];
-      red[(m + 8) * NT * 8 + n + 1] = acc[mi][jt][3];
+      red[m * NT * 8 + n] = acc[mi][jl][0];
+      red[m * NT * 8 + n + 1] = acc[mi][jl][1];
+      red[(m + 8) * NT * 8 + n] = acc[mi][jl][2];
+      red[(m + 8) * NT * 8 + n + 1] = acc[mi][jl][3];
     }
   __syncthreads();
   float* part = a.part + (int64_t)b * g.pstride;
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     const int m = i / cols, j = i - m * cols;
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < ST / 32; ++w) s += sg[w * tw + m * NT * 8 + j];
+    for (int w = 0; w < SKG; ++w) s += sg[w * tw + m * NT * 8 + j];
     part[j < g.Kd ? m * g.Kd + j : g.K * g.Kd + m] = s;
   }
   SPHASE(6);
