@@ -13,18 +13,11 @@
 // layer and the loss).  Exchanges go through distributed shared memory:
 // K-split partials of x W_H^T are reduced by the row owner in rank order,
 // the rows of gH are all-gathered, dW_O partials are reduced slice-wise in
-// rank order.  The three contractions run on the tcgen05 tensor cores (TF32,
-// fp32 accumulators in TMEM, one elected thread issuing): every operand is
-// staged (tf32-rounded) in the K-major no-swizzle layout [k/4][rows][4]
-// (8-row x 16-byte core matrices, LBO = rows*16, SBO = 128 B), M = 128 rows
-// (the batch, or the CTA's input columns), results read back with
-// tcgen05.ld by all 16 warps (4 lane quadrants x 4 column groups).  Every
-// reduction in a fixed order (deterministic).  Replaces 6-8 launches on the
-// critical path.
+// rank order.  fp32 SIMT with 4x4 register tiles; every reduction in a fixed
+// order (deterministic).  Replaces 6-8 launches on the critical path.
 #include <cooperative_groups.h>
 
 #include "kernels.cuh"
-#include "tc_ptx.cuh"
 
 namespace vcnn_b200 {
 
@@ -38,17 +31,11 @@ constexpr int kThreadsM = 512;
 struct Dims {
   int B, in, h, out;
   int R, Kc;                  // batch rows / input columns per CTA (Kc % 4 == 0)
-  int Kp, Hp, Np, Bk;         // GEMM extents: K of x W_H^T (Kc to 8), hidden (to 16),
-                              // dx N (Kc to 16), K of dW_H (B to 8)
-  int sH;                     // row stride of the hidden rows: multiple of 4, odd in 16B units
+  int Bp, Hp, Kp;             // padded: Bp, Hp to 16 (mma M), Kp to 8 (mma K / N)
+  int sK, sH;                 // row strides: multiples of 4 floats, odd in 16B units
   int per5;                   // dW_O | db_O elements reduced per CTA
-  // smem offsets (floats); operand tiles in the K-major [k/4][rows][4] layout
-  int oA1, oB1;               // x[:, mine] [Kp/4][128][4], W_H[:, mine] [Kp/4][Hp][4]
-  int oA2;                    // gH [Hp/4][128][4]   (over A1/B1 once x W_H^T is done)
-  int oB2;                    // W_H[:, mine]^T [Hp/4][Np][4]
-  int oXT;                    // x[:, mine]^T [Bk/4][128][4]
-  int oGT;                    // gH^T [Bk/4][Hp][4]
-  int oPs, oW5, ohs, og5, ogl, op5, odb, obH, obO, oy5, otg;
+  // smem offsets (floats)
+  int oxr, owr, oPs, oG, oW5, ohs, og5, ogl, op5, obH, obO, oy5, otg;
   int total;
 };
 
@@ -56,36 +43,30 @@ __host__ __device__ inline int up4(int v) { return (v + 3) & ~3; }
 __host__ __device__ inline int up8(int v) { return (v + 7) & ~7; }
 __host__ __device__ inline int up16(int v) { return (v + 15) & ~15; }
 // a row stride of v floats (v % 4 == 0) whose 16-byte units are odd: float4
-// accesses of 8 consecutive rows hit distinct banks
+// accesses of 8 consecutive rows, and mma fragment loads (8 rows x 4 columns)
+// hit distinct banks
 __host__ __device__ inline int odd16(int v) { return (v >> 2) & 1 ? v : v + 4; }
-// offset (floats) of element (row, k) of a K-major [k/4][rows][4] tile
-__host__ __device__ inline int kmaj(int row, int k, int rows) {
-  return ((k >> 2) * rows + row) * 4 + (k & 3);
-}
 
 __host__ __device__ inline Dims dims_of(int B, int in, int h, int out) {
   Dims d;
   d.B = B; d.in = in; d.h = h; d.out = out;
   d.R = (B + kC - 1) / kC;
   d.Kc = up4((in + kC - 1) / kC);
-  d.Kp = up8(d.Kc); d.Hp = up16(h); d.Np = up16(d.Kc); d.Bk = up8(B);
+  d.Bp = up16(B); d.Hp = up16(h); d.Kp = up8(d.Kc);
+  d.sK = odd16(d.Kp);
   d.sH = odd16(d.Hp);
   d.per5 = (out * (h + 1) + kC - 1) / kC;
   int o = 0;
-  const int a1b1 = 128 * d.Kp + d.Hp * d.Kp, a2 = 128 * d.Hp;
-  d.oA1 = o; d.oB1 = o + 128 * d.Kp; d.oA2 = o;
-  o += a1b1 > a2 ? a1b1 : a2;
-  d.oB2 = o; o += d.Hp * d.Np;
-  d.oXT = o; o += 128 * d.Bk;
-  d.oGT = o; o += d.Hp * d.Bk;
+  d.oxr = o; o += d.Bp * d.sK;        // x[:, mine]   [Bp][sK]
+  d.owr = o; o += d.Hp * d.sK;        // W_H[:, mine] [Hp][sK]
   d.oPs = o; o += kC * d.R * d.sH;    // pushed partials of my rows [src rank][R][sH]
+  d.oG = o;  o += d.Bp * d.sH;        // gH, all rows (pushed by the row owners) [Bp][sH]
   d.oW5 = o; o += out * (h + 1);      // W_O [out][h+1]
   d.ohs = o; o += d.R * (h + 1);      // h rows [R][h+1]
   d.og5 = o; o += d.R * out;          // y / gO rows [R][out]
   o = up4(o);
-  d.ogl = o; o += d.R * d.sH;         // my gH rows [R][sH] (fp32)
+  d.ogl = o; o += d.R * d.sH;         // my gH rows [R][sH] (float4 pushes)
   d.op5 = o; o += kC * d.per5;        // pushed dW_O | db_O partials [src rank][per5]
-  d.odb = o; o += kC * d.Hp;          // pushed db_H partials [src rank][Hp] (rank 0)
   d.obH = o; o += h;                  // b_H
   d.obO = o; o += out;                // b_O
   d.oy5 = o; o += d.R * out;          // y rows (stored after the exchange)
@@ -133,65 +114,117 @@ __device__ __forceinline__ void cluster_wait() {
 __device__ __noinline__ float actf(int act, float x) { return act_fwd(act, x); }
 __device__ __noinline__ float actg(int act, float y) { return act_grad_from_out(act, y); }
 
-__device__ __forceinline__ float rtf32(float f) { return ptx::to_tf32(f); }
+__device__ __forceinline__ uint32_t tf32(float f) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(f));
+  return r;
+}
 
-// one K-major [k/4][rows][4] descriptor per K step of 8 (two 4-column halves
-// LBO = rows*16 apart, 8-row core matrices SBO = 128 B apart)
-__device__ __forceinline__ uint64_t kdesc(uint32_t base, int rows, int kstep) {
-  return ptx::interleave_desc(base + (uint32_t)(kstep * 2 * rows * 16), (uint32_t)(rows * 16),
-                              128u);
+// One warp's m16 x (NG x n8) tile of C += A B over ksteps k8 steps with
+// mma.sync TF32 (the tensor-core path for these small per-CTA GEMMs; fp32
+// accumulate).  A(m, k) = A[m*am + k*ak], B(k, n) = Bm[n*bn + k*bk]; the
+// fragment layouts are the PTX m16n8k8 .row.col ones: lane = 4g + t,
+// a = {(g,t), (g+8,t), (g,t+4), (g+8,t+4)}, b = {(t,g), (t+4,g)},
+// c = {(g,2t), (g,2t+1), (g+8,2t), (g+8,2t+1)}.
+template <int NG, bool B_TF32 = false>  // B_TF32: B already rounded in smem
+__device__ __forceinline__ void warp_mma(float (&c)[NG][4], const float* A, int am, int ak,
+                                         const float* Bm, int bn, int bk, int m0, int n0,
+                                         int nvalid, int ksteps, int lane) {
+  const int g = lane >> 2, t = lane & 3;
+  const float* pa = A + (m0 + g) * am + t * ak;
+  const float* pb = Bm + (n0 + g) * bn + t * bk;
+  for (int ks = 0; ks < ksteps; ++ks) {
+    const int k = ks * 8;
+    const uint32_t a0 = tf32(pa[k * ak]), a1 = tf32(pa[8 * am + k * ak]);
+    const uint32_t a2 = tf32(pa[(k + 4) * ak]), a3 = tf32(pa[8 * am + (k + 4) * ak]);
+#pragma unroll
+    for (int j = 0; j < NG; ++j) {
+      if (j < nvalid) {
+        const float f0 = pb[j * 8 * bn + k * bk], f1 = pb[j * 8 * bn + (k + 4) * bk];
+        const uint32_t b0 = B_TF32 ? __float_as_uint(f0) : tf32(f0);
+        const uint32_t b1 = B_TF32 ? __float_as_uint(f1) : tf32(f1);
+        asm volatile(
+            "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+            "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(c[j][0]), "+f"(c[j][1]), "+f"(c[j][2]), "+f"(c[j][3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      }
+    }
+  }
+}
+
+// stage rows [0, nrows) x columns [k0, k0+nc) of a row-major [*][ld] matrix
+// into smem [Rp][s] (zero padded to Rp rows and Kp columns)
+__device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, int ld, int nrows,
+                                           int Rp, int k0, int nc, int Kp, bool vec, int tid,
+                                           int nt, bool round = false) {
+  if (vec) {  // float4: Kp, k0, ld multiples of 4, src 16B aligned
+    const int q = Kp >> 2, n = Rp * q;
+    constexpr int kU = 4;
+    for (int base = 0; base < n; base += kU * nt) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = base + u * nt + tid, r = i / q, k = 4 * (i - r * q);
+        v[u] = (r < nrows && k < nc)
+                   ? __ldg(reinterpret_cast<const float4*>(src + (size_t)r * ld + k0 + k))
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = base + u * nt + tid, r = i / q, k = 4 * (i - r * q);
+        float4 w = v[u];
+        if (round) {
+          w.x = __uint_as_float(tf32(w.x));
+          w.y = __uint_as_float(tf32(w.y));
+          w.z = __uint_as_float(tf32(w.z));
+          w.w = __uint_as_float(tf32(w.w));
+        }
+        if (i < n) *reinterpret_cast<float4*>(dst + r * s + k) = w;
+      }
+    }
+  } else {
+    const int n = Rp * Kp;
+#pragma unroll 1
+    for (int i = tid; i < n; i += nt) {
+      const int r = i / Kp, k = i - r * Kp;
+      const float v = (r < nrows && k < nc) ? __ldg(src + (size_t)r * ld + k0 + k) : 0.f;
+      dst[r * s + k] = round ? __uint_as_float(tf32(v)) : v;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   HPHASE(0);
   // every CTA of the cluster has started before anyone writes into its smem
   cluster_arrive_relaxed();
-  const Dims d = dims_of(a.B, a.in, a.h, a.out);
-  const int B = a.B, in = a.in, h = a.h, out = a.out;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = nt >> 5;
-  extern __shared__ __align__(128) float sm[];
-  __shared__ uint64_t mma_bar[2];
-  __shared__ uint32_t tmem_base_sh;
-  if (warp == 0) {  // accumulators: x W_H^T [0, Hp), dx [64, 64+Np), dW_H^T after
-    ptx::tmem_alloc(&tmem_base_sh, 256);
-    ptx::tmem_relinquish();
-  }
-  if (tid == 32) {
-    ptx::mbar_init(&mma_bar[0], 1);
-    ptx::mbar_init(&mma_bar[1], 1);
-    ptx::fence_mbar_init();
-  }
-  // zero the operand tiles (padding rows / columns; independent of the
-  // predecessor): A1, B1, B2, XT, GT (peers push gH^T into GT only after the
-  // first cluster barrier)
-  for (int i = tid; i < (d.oGT + d.Hp * d.Bk - d.oA1) / 4; i += nt)
-    reinterpret_cast<float4*>(sm + d.oA1)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   PDL_ENTRY();
   HPHASE(1);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  float* A1 = sm + d.oA1;
-  float* B1 = sm + d.oB1;
-  float* B2 = sm + d.oB2;
-  float* XT = sm + d.oXT;
+  const Dims d = dims_of(a.B, a.in, a.h, a.out);
+  const int B = a.B, in = a.in, h = a.h, out = a.out;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = nt >> 5;
+  extern __shared__ __align__(16) float sm[];
+  float* xr = sm + d.oxr;
+  float* wr = sm + d.owr;
   float* Ps = sm + d.oPs;
+  float* G = sm + d.oG;
   float* W5 = sm + d.oW5;
   float* hs = sm + d.ohs;
   float* g5 = sm + d.og5;
   float* gl = sm + d.ogl;
   float* p5 = sm + d.op5;
-  float* pdb = sm + d.odb;
   float* sbH = sm + d.obH;
   float* sbO = sm + d.obO;
   float* y5 = sm + d.oy5;
   float* tg = sm + d.otg;
   __shared__ float lossp[kC];
   __shared__ float rowloss[kThreadsM / 32];
-  const int lh = h + 1, sH = d.sH;
-  const uint32_t s_base = ptx::smem_u32(sm);
+  const int lh = h + 1, sK = d.sK, sH = d.sH;
 
-  // ---- stage my input columns of x and W_H as MMA operands (tf32), all of W_O ----
+  // ---- stage my input columns of x and W_H (zero padded), all of W_O ----
   const int k0 = rank * d.Kc < in ? rank * d.Kc : in;
   const int nc = k0 + d.Kc <= in ? d.Kc : in - k0;
   // the small operands phase 2 reads (W_O, b_H, b_O, my rows' targets) are
@@ -218,81 +251,46 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     if (i < out) return sbO + i;
     return tg + (i - out);
   };
+  // (one straight-line copy each: this kernel runs once per step, so its
+  // instruction footprint is fetched cold -- code size is latency here)
   const float sv0 = tid < nsmall ? small_src(tid) : 0.f;
   const float sv1 = tid + nt < nsmall ? small_src(tid + nt) : 0.f;
-  __syncthreads();  // the zero fill is complete before the data lands
-  {
-    // x rows b, columns c: A1 (b, c) and XT (c, b); W_H rows o: B1 (o, c) and
-    // B2 (c, o).  4 columns per item (float4 when the rows allow it).
-    const int q = (nc + 3) >> 2, nx = B * q, nw = h * q;
-#pragma unroll 1
-    for (int i = tid; i < nx + nw; i += nt) {
-      const bool isx = i < nx;
-      const int ii = isx ? i : i - nx, r = ii / q, c = 4 * (ii - r * q);
-      const float* src = (isx ? a.x + (size_t)r * in : a.WH + (size_t)r * in) + k0 + c;
-      float v[4];
-      if (a.vec && c + 4 <= nc) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(src));
-        v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
-      } else {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = c + u < nc ? __ldg(src + u) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = rtf32(v[u]);
-      if (isx) {
-        *reinterpret_cast<float4*>(A1 + kmaj(r, c, 128)) = make_float4(v[0], v[1], v[2], v[3]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) XT[kmaj(c + u, r, 128)] = v[u];
-      } else {
-        *reinterpret_cast<float4*>(B1 + kmaj(r, c, d.Hp)) = make_float4(v[0], v[1], v[2], v[3]);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) B2[kmaj(c + u, r, d.Np)] = v[u];
-      }
-    }
-  }
+  stage_cols(xr, sK, a.x, in, B, d.Bp, k0, nc, d.Kp, a.vec, tid, nt);
+  stage_cols(wr, sK, a.WH, in, h, d.Hp, k0, nc, d.Kp, a.vec, tid, nt, true);  // MMA-only: tf32
   if (tid < nsmall) *small_dst(tid) = sv0;
   if (tid + nt < nsmall) *small_dst(tid + nt) = sv1;
 #pragma unroll 1
   for (int i = tid + 2 * nt; i < nsmall; i += nt) *small_dst(i) = small_src(i);
+  for (int i = tid; i < (d.Bp - B) * sH; i += nt) G[B * sH + i] = 0.f;  // pad rows
   if (tid < kThreadsM / 32) rowloss[tid] = 0.f;
-  ptx::fence_proxy_async_smem();  // generic stores -> the MMAs' async proxy
-  ptx::tc_fence_before();
   __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  const uint32_t tH = tmem, tX = tmem + 64, tW = tmem + 64 + (uint32_t)d.Np;
   HPHASE(2);
 
-  // ---- 1: partial x[:, mine] W_H[:, mine]^T on the tensor cores (M = the
-  //         128 batch rows, N = Hp hidden units, K = my columns), pushed to the
+  // ---- 1: partial x[:, mine] W_H[:, mine]^T on the tensor cores (m16 = 16
+  //         batch rows, n = 4 x n8 hidden units per warp tile), pushed to the
   //         row owner's slot [rank] ----
-  if (warp == 0 && ptx::elect_one()) {
-    const uint32_t idesc = ptx::idesc_tf32(128, d.Hp);
-    for (int ks = 0; ks < (d.Kp >> 3); ++ks)
-      ptx::mma_tf32(tH, kdesc(s_base + 4u * d.oA1, 128, ks), kdesc(s_base + 4u * d.oB1, d.Hp, ks),
-                    idesc, ks > 0 ? 1u : 0u);
-    ptx::mma_commit(&mma_bar[0]);
-  }
-  __syncwarp();
   cluster_wait();
-  ptx::mbar_wait(&mma_bar[0], 0);
-  ptx::tc_fence_after();
   {
-    const int qd = warp & 3, cgp = warp >> 2;  // lane quadrant, 16-column group
-    const int b = qd * 32 + lane;
-    for (int c0 = cgp * 16; c0 < d.Hp; c0 += (nwarps >> 2) * 16) {
-      uint32_t r[16];
-      ptx::tmem_ld16(tH + ((uint32_t)(qd * 32) << 16) + (uint32_t)c0, r);
-      ptx::tmem_wait_ld();
-      if (b < B) {
-        const int owner = b / d.R;
-        float* dst = cluster.map_shared_rank(Ps, owner) + (rank * d.R + (b - owner * d.R)) * sH + c0;
+    const int mt = d.Bp >> 4, nN = d.Hp >> 3, ngr = (nN + 3) >> 2;
+    for (int tile = warp; tile < mt * ngr; tile += nwarps) {
+      const int im = tile / ngr, ig = tile - im * ngr;
+      const int m0 = im * 16, n0 = ig * 32;
+      const int nv = nN - ig * 4 < 4 ? nN - ig * 4 : 4;
+      float c[4][4] = {};
+      warp_mma<4, true>(c, xr, sK, 1, wr, sK, 1, m0, n0, nv, d.Kp >> 3, lane);
+      const int g = lane >> 2, t = lane & 3;
 #pragma unroll
-        for (int j = 0; j < 16; j += 4)
-          *reinterpret_cast<float4*>(dst + j) =
-              make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
-                          __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+      for (int hf = 0; hf < 2; ++hf) {
+        const int b = m0 + g + 8 * hf;
+        if (b >= B) continue;
+        const int owner = b / d.R;
+        float* dst = cluster.map_shared_rank(Ps, owner) + (rank * d.R + (b - owner * d.R)) * sH;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int o = n0 + j * 8 + 2 * t;
+          if (j < nv && o < h)  // o even, h may be odd: o + 1 < Hp always
+            *reinterpret_cast<float2*>(dst + o) = make_float2(c[j][2 * hf], c[j][2 * hf + 1]);
+        }
       }
     }
   }
@@ -419,64 +417,20 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   }
   __syncthreads();
   HPHASE(13);
-  // db_H partial of my rows -> rank 0's slot [rank]; my gH rows (tf32) into
-  // every CTA's gH (A2) and gH^T (GT) operand tiles
-  for (int i = tid; i < d.Hp; i += nt) {
-    float acc = 0.f;
-#pragma unroll 1
-    for (int b = 0; b < nr; ++b) acc += gl[b * sH + i];
-    *cluster.map_shared_rank(pdb + rank * d.Hp + i, 0) = acc;
-  }
+  // push my gH rows into every CTA's G (float4)
   {
-    const int q = d.Hp >> 2, na2 = nr * q;  // A2: float4 over 4 hidden units
-    const int nb4 = (nr + 3) >> 2, ngt = d.Hp * nb4;  // GT: float4 over 4 batch rows
-    const int per = na2 + ngt;
+    const int q = d.Hp >> 2, n = nr * q * kC;
 #pragma unroll 1
-    for (int t = tid; t < per * kC; t += nt) {
-      const int c = t / per, u = t - c * per;
-      if (u < na2) {
-        const int b = u / q, k = 4 * (u - b * q);
-        const float* g = gl + b * sH + k;
-        *reinterpret_cast<float4*>(cluster.map_shared_rank(sm + d.oA2, c) +
-                                   kmaj(r0 + b, k, 128)) =
-            make_float4(rtf32(g[0]), rtf32(g[1]), rtf32(g[2]), rtf32(g[3]));
-      } else {
-        const int v = u - na2, o = v / nb4, bq = 4 * (v - o * nb4);
-        float f[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) f[e] = bq + e < nr ? rtf32(gl[(bq + e) * sH + o]) : 0.f;
-        float* gt = cluster.map_shared_rank(sm + d.oGT, c);
-        if ((d.R & 3) == 0) {  // my rows are whole 4-row groups: one 16-byte store
-          *reinterpret_cast<float4*>(gt + kmaj(o, r0 + bq, d.Hp)) =
-              make_float4(f[0], f[1], f[2], f[3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (bq + e < nr) gt[kmaj(o, r0 + bq + e, d.Hp)] = f[e];
-        }
-      }
+    for (int t = tid; t < n; t += nt) {
+      const int c = t / (nr * q), u = t - c * (nr * q), b = u / q, k = 4 * (u - b * q);
+      *reinterpret_cast<float4*>(cluster.map_shared_rank(G, c) + (r0 + b) * sH + k) =
+          *reinterpret_cast<const float4*>(gl + b * sH + k);
     }
   }
-  asm volatile("fence.proxy.async;" ::: "memory");  // my pushes -> peers' MMAs
   HPHASE(5);
   cluster_arrive();
   cluster_wait();
   HPHASE(6);
-  // ---- 4 (issued now, drained below): on the tensor cores
-  //         dx[:, mine]     = gH W_H[:, mine]     (M = batch, N = my columns, K = hidden)
-  //         dW_H[:, mine]^T = x[:, mine]^T gH     (M = my columns, N = hidden, K = batch) ----
-  if (warp == 0 && ptx::elect_one()) {
-    ptx::fence_proxy_async_smem();  // the pushed gH tiles -> the async proxy
-    const uint32_t idx = ptx::idesc_tf32(128, d.Np), idw = ptx::idesc_tf32(128, d.Hp);
-    for (int ks = 0; ks < (d.Hp >> 3); ++ks)
-      ptx::mma_tf32(tX, kdesc(s_base + 4u * d.oA2, 128, ks), kdesc(s_base + 4u * d.oB2, d.Np, ks),
-                    idx, ks > 0 ? 1u : 0u);
-    for (int ks = 0; ks < (d.Bk >> 3); ++ks)
-      ptx::mma_tf32(tW, kdesc(s_base + 4u * d.oXT, 128, ks), kdesc(s_base + 4u * d.oGT, d.Hp, ks),
-                    idw, ks > 0 ? 1u : 0u);
-    ptx::mma_commit(&mma_bar[1]);
-  }
-  __syncwarp();
   // my rows' layer outputs and gradients (stored after the exchange: the
   // cluster barrier's release would otherwise wait for them)
 #pragma unroll 1
@@ -491,7 +445,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     a.gO[(size_t)r0 * out + e] = g5[e];
   }
 
-  // ---- 3: my slice of dW_O | db_O, (rank 0) the loss and db_H, summed in rank order ----
+  // ---- 3: my slice of dW_O | db_O and (rank 0) the loss, summed in rank order ----
   {
     const int np = out * lh, e0 = rank * d.per5;
     const int e1 = e0 + d.per5 < np ? e0 + d.per5 : np;
@@ -515,52 +469,82 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
 #pragma unroll 1
     for (int o = tid; o < h; o += nt) {
       float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < kC; ++c) acc += pdb[c * d.Hp + o];
+#pragma unroll 1
+      for (int b = 0; b < B; ++b) acc += G[b * sH + o];
       a.dbH[o] = acc;
     }
   HPHASE(7);
 
-  // ---- 4 (drain): 4 lane quadrants x 4 column groups; dx *= act_prev'(x) ----
-  ptx::mbar_wait(&mma_bar[1], 0);
-  ptx::tc_fence_after();
+  // ---- 4: on the tensor cores, one tile pool:
+  //         dW_H[:, mine] = gH^T x[:, mine]   (m16 hidden units x 2 n8 columns, K = batch)
+  //         dx[:, mine] = gH W_H[:, mine]      (m16 batch rows x 4 n8 columns, K = hidden)
+  //         dx *= act_prev'(x) ----
   {
-    const int qd = warp & 3, cgp = warp >> 2, step = (nwarps >> 2) * 16;
-    const int row = qd * 32 + lane;  // dx: batch row b; dW^T: my column
-    const uint32_t lrow = (uint32_t)(qd * 32) << 16;
-    if (a.dx)
-      for (int c0 = cgp * 16; c0 < d.Np; c0 += step) {
-        uint32_t r[16];
-        ptx::tmem_ld16(tX + lrow + (uint32_t)c0, r);
-        ptx::tmem_wait_ld();
-        if (row < B) {
-          const float* xs = a.x + (size_t)row * in + k0;
-          float* p = a.dx + (size_t)row * in + k0;
+    const int nN = d.Kp >> 3;
+    const int ga = (nN + 1) >> 1, na = (d.Hp >> 4) * ga;
+    const int gb = (nN + 3) >> 2, nb = a.dx ? (d.Bp >> 4) * gb : 0;
+    const int g = lane >> 2, t = lane & 3;
+    for (int tile = warp; tile < na + nb; tile += nwarps) {
+      if (tile < na) {
+        const int im = tile / ga, ig = tile - im * ga;
+        const int m0 = im * 16, n0 = ig * 16;
+        const int nv = nN - ig * 2 < 2 ? nN - ig * 2 : 2;
+        float c[2][4] = {};
+        warp_mma<2>(c, G, 1, sH, xr, 1, sK, m0, n0, nv, d.Bp >> 3, lane);
+        // column pairs (2t, 2t+1) are adjacent: one 8-byte store when both
+        // are in range and the address is 8-byte aligned
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int col = c0 + j;
-            if (col >= nc) break;
-            float v = __uint_as_float(r[j]);
-            if (a.act_prev == VCNN_ACT_RELU) v *= __ldg(xs + col) > 0.f ? 1.f : 0.f;
-            else if (a.act_prev != VCNN_ACT_IDENTITY) v *= actg(a.act_prev, __ldg(xs + col));
-            p[col] = v;
+        for (int hf = 0; hf < 2; ++hf) {
+          const int o = m0 + g + 8 * hf;
+          if (o >= h) continue;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = n0 + j * 8 + 2 * t;
+            if (j >= nv || col >= nc) continue;
+            float* p = a.dWH + (size_t)o * in + k0 + col;
+            if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+              *reinterpret_cast<float2*>(p) = make_float2(c[j][2 * hf], c[j][2 * hf + 1]);
+            } else {
+              p[0] = c[j][2 * hf];
+              if (col + 1 < nc) p[1] = c[j][2 * hf + 1];
+            }
+          }
+        }
+      } else {
+        const int u = tile - na, im = u / gb, ig = u - im * gb;
+        const int m0 = im * 16, n0 = ig * 32;
+        const int nv = nN - ig * 4 < 4 ? nN - ig * 4 : 4;
+        float c[4][4] = {};
+        warp_mma<4, true>(c, G, sH, 1, wr, 1, sK, m0, n0, nv, d.Hp >> 3, lane);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int b = m0 + g + 8 * hf;
+          if (b >= B) continue;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int col = n0 + j * 8 + 2 * t;
+            if (j >= nv || col >= nc) continue;
+            float v0 = c[j][2 * hf], v1 = c[j][2 * hf + 1];
+            if (a.act_prev == VCNN_ACT_RELU) {  // the common case inline
+              v0 *= xr[b * sK + col] > 0.f ? 1.f : 0.f;
+              v1 *= xr[b * sK + col + 1] > 0.f ? 1.f : 0.f;
+            } else if (a.act_prev != VCNN_ACT_IDENTITY) {
+              v0 *= actg(a.act_prev, xr[b * sK + col]);
+              if (col + 1 < nc) v1 *= actg(a.act_prev, xr[b * sK + col + 1]);
+            }
+            float* p = a.dx + (size_t)b * in + k0 + col;
+            if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
+              *reinterpret_cast<float2*>(p) = make_float2(v0, v1);
+            } else {
+              p[0] = v0;
+              if (col + 1 < nc) p[1] = v1;
+            }
           }
         }
       }
-    for (int c0 = cgp * 16; c0 < d.Hp; c0 += step) {
-      uint32_t r[16];
-      ptx::tmem_ld16(tW + lrow + (uint32_t)c0, r);
-      ptx::tmem_wait_ld();
-      if (row < nc)
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (c0 + j < h) a.dWH[(size_t)(c0 + j) * in + k0 + row] = __uint_as_float(r[j]);
     }
   }
   HPHASE(8);
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 0) ptx::tmem_dealloc(tmem, 256);
   HPHASE(9);
 }
 
@@ -611,12 +595,10 @@ static bool cluster_ok(size_t smem) {
 }
 
 bool mlp_head_fusable(int B, int in, int h, int out) {
-  // M = 128 batch rows / input columns per CTA; the dx accumulator sits at
-  // TMEM column 64 (Np <= 128) and dW_H^T after it (Hp <= 64): 256 columns
   if (B < 1 || B > 128 || h < 1 || h > 64 || out < 1 || out > 64 || in < kC || in > 128 * kC)
     return false;
   const size_t smem = mlp_head_smem(B, in, h, out);
-  return smem + 1024 <= 227 * 1024 && cluster_ok(smem);
+  return smem <= 200 * 1024 && cluster_ok(smem);
 }
 
 int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* WH,
