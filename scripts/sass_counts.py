@@ -34,6 +34,9 @@ def short(name):
 
 
 print("%-110s " % "kernel" + " ".join("%8s" % k for k in keys))
+seen = set()
 for fn, c in counts.items():
-    if any(c[k] for k in keys[:6]):
-        print("%-110s " % short(fn) + " ".join("%8d" % c[k] for k in keys))
+    row = "%-110s " % short(fn) + " ".join("%8d" % c[k] for k in keys)
+    if any(c[k] for k in keys[:6]) and row not in seen:  # (each cubin lists a kernel once)
+        seen.add(row)
+        print(row)
