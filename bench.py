@@ -645,6 +645,7 @@ def main():
         print(json.dumps(line))
     net.close()
     if world > 1:
+        barrier()  # rank 0's single-replica passes are done on every rank's clock
         dist.destroy_process_group()
 
 
