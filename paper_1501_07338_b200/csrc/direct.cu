@@ -35,6 +35,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "image_sum.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
@@ -741,10 +742,10 @@ __device__ __forceinline__ void update_pack(int64_t i, float gi, float* __restri
 // sgd_step (network.hpp:242-273): v = mom*v + scale*g; w -= lr*v; and the
 // updated conv weights are written straight into the direct kernels' packs
 // (fwd: row n, channel c, s = ky*kw+kx; dgrad: row c, channel n, flipped s)
-__global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restrict__ v,
-                                const float* __restrict__ g, float lr, float mom, float scale,
-                                const PackTable t, const float* __restrict__ loss,
-                                int* __restrict__ guard) {
+__global__ void __launch_bounds__(32 * kRedSlices) sgd_pack_kernel(
+    int64_t n, float* __restrict__ w, float* __restrict__ v, float* __restrict__ g, float lr,
+    float mom, float scale, const PackTable t, const float* __restrict__ loss,
+    int* __restrict__ guard, const ImageSumFold fold, int64_t fold_off) {
   PDL_ENTRY();
   // Trainer::fit's non-finite stop (training.hpp:77-80): while the guard is
   // armed, a non-finite batch loss skips this update and every later one, so
@@ -755,9 +756,23 @@ __global__ void sgd_pack_kernel(int64_t n, float* __restrict__ w, float* __restr
       return;
     }
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    update_pack(i, scale * g[i], w, v, lr, mom, t);
+  // the folded layer: blocks [0, nfold) sum its per-image partials exactly as
+  // wgrad_reduce_kernel does (same bits), store the gradient, update
+  const int nfold = fold.part ? (int)cdiv(fold.per, 32) : 0;
+  if ((int)blockIdx.x < nfold) {
+    __shared__ float red[kRedSlices][33];
+    const int64_t j = blockIdx.x * 32ll + (threadIdx.x & 31);
+    const float s = image_sum(fold.nimg, fold.per, fold.stride, j, fold.part, red);
+    if ((threadIdx.x >> 5) == 0 && j < fold.per) {
+      g[fold_off + j] = s;
+      update_pack(fold_off + j, scale * s, w, v, lr, mom, t);
+    }
+    return;
+  }
+  const int64_t f0 = nfold ? fold_off : n, f1 = nfold ? fold_off + fold.per : n;
+  for (int64_t i = (blockIdx.x - nfold) * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)(gridDim.x - nfold) * blockDim.x)
+    if (i < f0 || i >= f1) update_pack(i, scale * g[i], w, v, lr, mom, t);
 }
 
 // ---- data parallelism: one-shot peer reduce + SGD + packs -----------------
@@ -861,15 +876,22 @@ int pack_table(const std::vector<PackSpec>& layers, PackTable& t) {
 }
 }  // namespace
 
-int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss,
-             int* guard) {
+             int* guard, const ImageSumFold* fold, int64_t fold_off) {
   PackTable t;
   if (int s = pack_table(layers, t)) return s;
-  int64_t blocks = cdiv(n, 256);
-  if (blocks > 4 * sm_count()) blocks = 4 * sm_count();
+  constexpr int kT = 32 * kRedSlices;
+  int64_t blocks = cdiv(n, kT);
+  if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
   if (blocks < 1) blocks = 1;
-  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard));
+  ImageSumFold f{};
+  if (fold && fold->part) {
+    if (fold_off < 0 || fold_off + fold->per > n) return fail(VCNN_ESHAPE, "sgd_pack: fold range");
+    f = *fold;
+    blocks += cdiv(f.per, 32);
+  }
+  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(kT), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard, f, fold_off));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

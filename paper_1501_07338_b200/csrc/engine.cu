@@ -154,6 +154,11 @@ struct vcnn_net {
   int kernels_per_step = 0;
   bool guard = false;  // Trainer non-finite stop armed (err[2..3] on the device)
   DpLink* dp = nullptr;  // attached data-parallel group (vcnn_dp_*), or none
+  // train steps: layer 0's small-Kd weight gradient stays as per-image
+  // partials which the update sums itself (one launch less on the critical
+  // path); forward_backward alone reduces as usual
+  bool defer_fold = false;
+  direct::ImageSumFold fold{};
   // breakdown timer
   bool breakdown = false;
   struct MarkRec {
@@ -450,7 +455,8 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
           TRY(k1::conv_wgrad(d, in, l.gpre, gW, gB, wsw, sw));
         else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_small_ok(d, gs) &&
                  wsw.bytes >= direct::wgrad_small_workspace(d))
-          TRY(direct::conv_wgrad_small(d, in, gs, gW, gB, wsw, sw));
+          TRY(direct::conv_wgrad_small(d, in, gs, gW, gB, wsw, sw,
+                                       i == 0 && n->defer_fold ? &n->fold : nullptr));
         else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_ok(d, gs) &&
                  wsw.bytes >= direct::wgrad_workspace(d))
           TRY(direct::conv_wgrad(d, in, gs, gW, gB, wsw, sw));
@@ -541,7 +547,9 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   DpLink* dp = n->dp;
   if (!dp || dp->world == 1) {
     TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
-                         n->stream, n->loss, n->err + 2));
+                         n->stream, n->loss, n->err + 2, n->fold.part ? &n->fold : nullptr,
+                         n->L[0].w_off));
+    n->fold = direct::ImageSumFold{};
   } else if (dp->mode == VCNN_DP_P2P) {
     // one kernel: rank-ordered sum of every replica's gradient (peers over
     // NVLink) + SGD + packs
@@ -598,7 +606,11 @@ int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   } pdl_scope(n->breakdown);
   const int tail = tail_fused(n, batch);
   TRY(run_forward(n, batch, tail));
-  TRY(run_backward(n, batch, tail));
+  n->defer_fold = !n->dp || n->dp->world == 1;
+  n->fold = direct::ImageSumFold{};
+  const int sb = run_backward(n, batch, tail);
+  n->defer_fold = false;
+  if (sb) return sb;
   TRY(run_sgd(n, lr, mom, 1.0f));
   n->kernels_per_step = (int)(g_launches.load() - before);
   return VCNN_OK;

@@ -241,11 +241,20 @@ struct PackSpec {
   float* pd;
   float* ps = nullptr;  // small-Kd forward image (small_fwd_pack_floats)
 };
+// a weight gradient left as per-image partials [nimg][stride] (dW then db
+// in NetGrads order, `per` values), summed by the update (sgd_pack)
+struct ImageSumFold {
+  const float* part = nullptr;
+  int nimg = 0;
+  int64_t per = 0, stride = 0;
+};
 // guard (nullable): int[2] {armed, tripped}; while armed, a non-finite *loss
 // trips it and the update (and every later one) is skipped
-int sgd_pack(int64_t n, float* w, float* v, const float* g, float lr, float mom, float scale,
+// fold (nullable, fold->part set): params [fold_off, fold_off + per) take
+// their gradient from the per-image partials (written to g as well)
+int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss = nullptr,
-             int* guard = nullptr);
+             int* guard = nullptr, const ImageSumFold* fold = nullptr, int64_t fold_off = 0);
 int dp_blocks(int64_t n);
 int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
                 const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st);
@@ -261,7 +270,7 @@ int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, 
 bool wgrad_small_ok(const ConvDesc& d, const GradSrc& gs);
 size_t wgrad_small_workspace(const ConvDesc& d);
 int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
-                     const Workspace& ws, cudaStream_t st);
+                     const Workspace& ws, cudaStream_t st, ImageSumFold* defer = nullptr);
 }  // namespace direct
 
 // ---- single-output-map convolutions (k1.cu, K = 1, exact fp32, any precision) ----

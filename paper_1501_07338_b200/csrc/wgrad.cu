@@ -21,6 +21,7 @@
 // to the workspace and a fixed-order reduce over images writes dW / db
 // (deterministic).  The routed pool backward (GradSrc.pool) scatters dP to
 // the argmax positions while G is staged.
+#include "image_sum.cuh"
 #include "kernels.cuh"
 #include "tc_ptx.cuh"
 
@@ -355,35 +356,14 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
 // slice s of the block sums images [s*per_s, (s+1)*per_s) for 32 consecutive
 // outputs (loads coalesced, all in flight), then lane-wise over slices in
 // order.  Deterministic; latency is one round of loads, not nimg.
-constexpr int kRedSlices = 16;
 __global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
     int nimg, int64_t per, int64_t stride, int64_t nw, const float* __restrict__ part,
     float* __restrict__ dw, float* __restrict__ db) {
   PDL_ENTRY();
   __shared__ float red[kRedSlices][33];
-  const int lane = threadIdx.x & 31, sl = threadIdx.x >> 5;
-  const int64_t i = blockIdx.x * 32ll + lane;
-  const int per_s = (nimg + kRedSlices - 1) / kRedSlices;
-  const int b0 = sl * per_s, b1 = b0 + per_s < nimg ? b0 + per_s : nimg;
-  float acc = 0.f;
-  if (i < per) {
-    const float* p = part + i;
-    int bb = b0;
-    for (; bb + 8 <= b1; bb += 8) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (int64_t)(bb + u) * stride);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += v[u];
-    }
-    for (; bb < b1; ++bb) acc += __ldg(p + (int64_t)bb * stride);
-  }
-  red[sl][lane] = acc;
-  __syncthreads();
-  if (sl == 0 && i < per) {
-    float t = 0.f;
-#pragma unroll
-    for (int s2 = 0; s2 < kRedSlices; ++s2) t += red[s2][lane];
+  const int64_t i = blockIdx.x * 32ll + (threadIdx.x & 31);
+  const float t = image_sum(nimg, per, stride, i, part, red);
+  if ((threadIdx.x >> 5) == 0 && i < per) {
     if (i < nw) dw[i] = t;
     else if (db) db[i - nw] = t;
   }
@@ -674,7 +654,7 @@ size_t wgrad_small_workspace(const ConvDesc& d) {
 }
 
 int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, float* db,
-                     const Workspace& ws, cudaStream_t st) {
+                     const Workspace& ws, cudaStream_t st, ImageSumFold* defer) {
   SArgs a{};
   if (!splan(d, gs, a.g)) return fail(VCNN_ESHAPE, "small wgrad: geometry not supported");
   const size_t need = sizeof(float) * (size_t)(a.g.pstride * d.B);
@@ -703,6 +683,10 @@ int conv_wgrad_small(const ConvDesc& d, const float* x, const GradSrc& gs, float
         : a.g.nt <= 8 ? go(wgrad_small_kernel<2, 8>, c28) : go(wgrad_small_kernel<2, 12>, c212);
   if (s) return s;
   const int64_t per = a.g.part, nw = per - d.K;
+  if (defer) {  // the caller's update sums the per-image partials itself
+    *defer = ImageSumFold{ws.ptr, d.B, per, a.g.pstride};
+    return VCNN_OK;
+  }
   VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)cdiv(per, 32)),
                            dim3(32 * kRedSlices), 0, st, d.B, per, a.g.pstride, nw,
                            (const float*)ws.ptr, dw, db));
