@@ -434,6 +434,20 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   const bool routed = g.mode == 1 && a.gs.pool;
   const int wsz = routed ? a.gs.POH * a.gs.POW * g.Cin : 0;
   const float* pack = a.pack + nb * pk_per;
+  // the shifts that can touch a valid output of this tile: a 1-D dgrad tile
+  // skips the kernel taps whose view of the zero-padded gradient is empty
+  // for every valid position (they would add exact zeros) -- 121 -> 92 taps
+  // per tile on deconv-121's 1x121 layer; their pack chunks are not loaded
+  int s_lo = 0, s_hi = g.kh * g.kw - 1;
+  if (g.seg && g.mode == 1) {
+    const int wid = (x0 + g.segw < g.Wout ? x0 + g.segw : g.Wout) - x0;
+    const int lo = g.pad_x - x0 - (wid - 1), hi = g.pad_x - x0 + g.Win - 1;
+    s_lo = lo > 0 ? lo : 0;
+    s_hi = hi < g.kw - 1 ? hi : g.kw - 1;
+    if (s_lo > s_hi) s_lo = s_hi = 0;  // (no tap: one zero MMA keeps the accumulator defined)
+  }
+  const int c_lo = s_lo / g.SC, nloc = s_hi / g.SC - c_lo + 1;
+  const int nring = nloc < g.nbuf ? nloc : g.nbuf;
   if (tid == 0) {
     ptx::mbar_init(&load_bar, 1);
     ptx::mbar_init(&done_bar, 1);
@@ -442,12 +456,13 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       ptx::mbar_init(&wempty[i], 1);
     }
     ptx::fence_mbar_init();
-    // pack chunks 0 (and 1) into the ring
-    for (int c = 0; c < g.nbuf; ++c) {
+    // the tile's first pack chunks into the ring
+    for (int lc = 0; lc < nring; ++lc) {
+      const int c = c_lo + lc;
       const uint32_t bytes = chunk_bytes(g, c);
-      ptx::mbar_arrive_expect_tx(&wfull[c], bytes);
-      ptx::bulk_g2s(s_b + (uint32_t)(c * g.wchunk), pack + (int64_t)c * (g.wchunk / 4), bytes,
-                    &wfull[c]);
+      ptx::mbar_arrive_expect_tx(&wfull[lc], bytes);
+      ptx::bulk_g2s(s_b + (uint32_t)(lc * g.wchunk), pack + (int64_t)c * (g.wchunk / 4), bytes,
+                    &wfull[lc]);
     }
     if (g.off_yp >= 0 && a.be.yprev) {
       const uint32_t yb = 4u * (uint32_t)(g.Cout * g.Hout * g.Wout);
@@ -574,14 +589,16 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     const uint64_t a0 = ptx::interleave_desc(s_a, half, 128u);
     const uint64_t a_cg = (uint64_t)(2u * half >> 4), b_blk = (uint64_t)(g.BN * 32 >> 4);
     uint32_t acc = 0;
-    int ky = 0, kx = 0;  // shift s = ky * kw + kx, advanced incrementally
-    for (int c = 0; c < g.nchunk; ++c) {
-      const int buf = g.nbuf == 2 ? (c & 1) : 0;
-      ptx::mbar_wait(&wfull[buf], (uint32_t)(g.nbuf == 2 ? (c >> 1) : c) & 1u);
+    int ky = s_lo / g.kw, kx = s_lo - ky * g.kw;  // shift s = ky * kw + kx, incremental
+    for (int lc = 0; lc < nloc; ++lc) {
+      const int c = c_lo + lc, buf = lc % g.nbuf;
+      ptx::mbar_wait(&wfull[buf], (uint32_t)(lc / g.nbuf) & 1u);
       ptx::tc_fence_after();
-      uint64_t bd = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u);
-      const int s1 = (c + 1) * g.SC < g.kh * g.kw ? (c + 1) * g.SC : g.kh * g.kw;
-      for (int sft = c * g.SC; sft < s1; ++sft) {
+      const int s0 = c * g.SC > s_lo ? c * g.SC : s_lo;
+      const int s1 = (c + 1) * g.SC - 1 < s_hi ? (c + 1) * g.SC - 1 : s_hi;
+      uint64_t bd = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u) +
+                    (uint64_t)(s0 - c * g.SC) * g.CG * b_blk;
+      for (int sft = s0; sft <= s1; ++sft) {
         uint64_t ad = a0 + (uint64_t)(ky * g.Wg + kx);
         for (int cg = 0; cg < g.CG; ++cg) {
           ptx::mma_tf32(tmem, ad, bd, idesc, acc);
@@ -598,10 +615,10 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     }
     ptx::mma_commit(&done_bar);
   } else if (warp == 1 && ptx::elect_one()) {
-    // refill the ring: chunk c once chunk c - nbuf's MMAs have read its slot
-    for (int c = g.nbuf; c < g.nchunk; ++c) {
-      const int buf = g.nbuf == 2 ? (c & 1) : 0;
-      ptx::mbar_wait(&wempty[buf], (uint32_t)((c - g.nbuf) / g.nbuf) & 1u);
+    // refill the ring: chunk lc once chunk lc - nbuf's MMAs have read its slot
+    for (int lc = g.nbuf; lc < nloc; ++lc) {
+      const int c = c_lo + lc, buf = lc % g.nbuf;
+      ptx::mbar_wait(&wempty[buf], (uint32_t)((lc - g.nbuf) / g.nbuf) & 1u);
       const uint32_t bytes = chunk_bytes(g, c);
       ptx::mbar_arrive_expect_tx(&wfull[buf], bytes);
       ptx::bulk_g2s(s_b + (uint32_t)(buf * g.wchunk), pack + (int64_t)c * (g.wchunk / 4), bytes,
