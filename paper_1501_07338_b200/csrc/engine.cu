@@ -460,6 +460,9 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
         else if (n->precision == VCNN_PREC_TF32 && direct::wgrad_ok(d, gs) &&
                  wsw.bytes >= direct::wgrad_workspace(d))
           TRY(direct::conv_wgrad(d, in, gs, gW, gB, wsw, sw));
+        else if (!fpool && n->precision == VCNN_PREC_TF32 && direct::wgrad1d_ok(d) &&
+                 wsw.bytes >= direct::wgrad1d_workspace(d))
+          TRY(direct::conv_wgrad1d(d, in, l.gpre, gW, gB, wsw, sw));
         else if (fpool)
           TRY(tc::slab_conv_wgrad(d, in, gs, gW, gB, wsw, sw));
         else
@@ -910,6 +913,8 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
         if (dws > need) need = dws;
         const size_t dk1 = k1::wgrad_workspace(conv_of(l, B));
         if (dk1 > need) need = dk1;
+        const size_t dw1 = direct::wgrad1d_workspace(conv_of(l, B));
+        if (dw1 > need) need = dw1;
       }
       else if (l.spec.kind == VCNN_LAYER_FULL)
         need = full_workspace(B, (int)l.in_per, l.spec.units, VCNN_PREC_TF32);

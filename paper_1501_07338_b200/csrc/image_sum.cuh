@@ -42,4 +42,11 @@ __device__ __forceinline__ float image_sum(int nimg, int64_t per, int64_t stride
   return t;
 }
 
+namespace direct {
+// out[i] = image_sum over nimg partials (dW then db), wgrad.cu
+__global__ void wgrad_reduce_kernel(int nimg, int64_t per, int64_t stride, int64_t nw,
+                                    const float* __restrict__ part, float* __restrict__ dw,
+                                    float* __restrict__ db);
+}  // namespace direct
+
 }  // namespace vcnn_b200

@@ -258,6 +258,13 @@ int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float
 int dp_blocks(int64_t n);
 int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
                 const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st);
+// weight gradient of a 1-D (kh == 1) conv with a long kernel (kw 16..128) on
+// tcgen05 (wgrad1d.cu): M = taps, N = maps, K = a row's positions, the row
+// staged as 4-element granules; row-group partials + fixed-order reduce
+bool wgrad1d_ok(const ConvDesc& d);
+size_t wgrad1d_workspace(const ConvDesc& d);
+int conv_wgrad1d(const ConvDesc& d, const float* x, const float* gpre, float* dw, float* db,
+                 const Workspace& ws, cudaStream_t st);
 // weight gradient as shifted-view GEMMs (wgrad.cu): dW [K][C][kh][kw] and db
 // [K] (nullable) from x and the (possibly pool-routed) gradient; per-image
 // partials in ws, fixed-order reduce

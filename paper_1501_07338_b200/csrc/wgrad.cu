@@ -352,22 +352,6 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
   if (warp == 0) ptx::tmem_dealloc(tmem, g.tmem_cols);
 }
 
-// out[i] = sum over images of part[b][i] (dW then db) in a fixed order:
-// slice s of the block sums images [s*per_s, (s+1)*per_s) for 32 consecutive
-// outputs (loads coalesced, all in flight), then lane-wise over slices in
-// order.  Deterministic; latency is one round of loads, not nimg.
-__global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
-    int nimg, int64_t per, int64_t stride, int64_t nw, const float* __restrict__ part,
-    float* __restrict__ dw, float* __restrict__ db) {
-  PDL_ENTRY();
-  __shared__ float red[kRedSlices][33];
-  const int64_t i = blockIdx.x * 32ll + (threadIdx.x & 31);
-  const float t = image_sum(nimg, per, stride, i, part, red);
-  if ((threadIdx.x >> 5) == 0 && i < per) {
-    if (i < nw) dw[i] = t;
-    else if (db) db[i - nw] = t;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Small-Kd weight gradient (first layers: C*kh*kw + 1 <= 96, e.g. CIFAR-3
@@ -602,6 +586,21 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
 }
 
 }  // namespace
+
+// out[i] = sum over images of part[b][i] (dW then db) in a fixed order
+// (image_sum.cuh).  External linkage: wgrad1d.cu launches it too.
+__global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
+    int nimg, int64_t per, int64_t stride, int64_t nw, const float* __restrict__ part,
+    float* __restrict__ dw, float* __restrict__ db) {
+  PDL_ENTRY();
+  __shared__ float red[kRedSlices][33];
+  const int64_t i = blockIdx.x * 32ll + (threadIdx.x & 31);
+  const float t = image_sum(nimg, per, stride, i, part, red);
+  if ((threadIdx.x >> 5) == 0 && i < per) {
+    if (i < nw) dw[i] = t;
+    else if (db) db[i - nw] = t;
+  }
+}
 
 bool wgrad_ok(const ConvDesc& d, const GradSrc& gs) {
   WGeo g;
