@@ -1026,7 +1026,7 @@ __device__ __forceinline__ void mma_tf32_m16n8k8(float (&c)[4], uint32_t a0, uin
 // CTA (b, s) computes M tiles [s*kTilesPerCta, ...) of image b; warp w the
 // pair 2w, 2w+1 of them (two independent accumulator sets per K step)
 template <int KS, int ACT>
-__global__ void __launch_bounds__(FT) conv_small_fwd_kernel(const FSArgs a) {
+__global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
   pdl_launch_dependents();
   const FGeo& g = a.g;
   extern __shared__ __align__(128) uint8_t smem_raw[];
