@@ -165,7 +165,7 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     if (SC > g.kh * g.kw) SC = g.kh * g.kw;
     const int nchunk = (int)cdiv(g.kh * g.kw, SC);
     const int wchunk = SC * shift_bytes;
-    const int nbuf = nchunk >= 2 ? 2 : 1;
+    const int nbuf = nchunk >= 2 ? 2 : 1;  // (a 3-deep ring: dgrad drops to 1 CTA/SM, 19.5 -> 33 us)
     const int b_bytes = nbuf * wchunk;
     // the epilogue tile [bn][128] reuses raw + window + A (all dead by then)
     const int ep_bytes = bn * EPS * 4;
@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   if (tid == 0) {
     ptx::mbar_init(&load_bar, 1);
     ptx::mbar_init(&done_bar, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < g.nbuf; ++i) {
       ptx::mbar_init(&wfull[i], 1);
       ptx::mbar_init(&wempty[i], 1);
     }

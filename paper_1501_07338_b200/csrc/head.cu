@@ -194,6 +194,9 @@ __device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, 
   }
 }
 
+// TB/TIN/TH/TOUT: compile-time dims for the common shape (CIFAR-3's tail:
+// every index division and loop bound folds), 0 = read from the arguments
+template <int TB, int TIN, int TH, int TOUT>
 __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   HPHASE(0);
   // every CTA of the cluster has started before anyone writes into its smem
@@ -202,9 +205,10 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   HPHASE(1);
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
-  const Dims d = dims_of(a.B, a.in, a.h, a.out);
-  const int B = a.B, in = a.in, h = a.h, out = a.out;
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int B = TB ? TB : a.B, in = TIN ? TIN : a.in, h = TH ? TH : a.h,
+            out = TOUT ? TOUT : a.out;
+  const Dims d = dims_of(B, in, h, out);
+  const int tid = threadIdx.x, nt = kThreadsM, lane = tid & 31, warp = tid >> 5;
   const int nwarps = nt >> 5;
   extern __shared__ __align__(16) float sm[];
   float* xr = sm + d.oxr;
@@ -311,25 +315,26 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   }
   __syncthreads();
   HPHASE(10);
+  // y = act(h W_O^T + b): 4 lanes per output (strided k, independent loads),
+  // fixed xor tree; warp-uniform loop so every lane reaches the shuffles
 #pragma unroll 1
-  for (int e = tid; e < nr * out; e += nt) {
-    const int b = e / out, o = e - b * out;
+  for (int base = warp * 32; base < nr * out * 4; base += nt) {
+    const int e = (base + lane) >> 2, part = lane & 3;
+    const bool ok = e < nr * out;
+    const int b = ok ? e / out : 0, o = ok ? e - b * out : 0;
     const float* hr = hs + b * lh;
     const float* wo = W5 + o * lh;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    int k = 0;
-#pragma unroll 1
-    for (; k + 3 < h; k += 4) {
-      a0 += hr[k] * wo[k];
-      a1 += hr[k + 1] * wo[k + 1];
-      a2 += hr[k + 2] * wo[k + 2];
-      a3 += hr[k + 3] * wo[k + 3];
+    float acc = 0.f;
+    if (ok)
+#pragma unroll 4
+      for (int k = part; k < h; k += 4) acc += hr[k] * wo[k];
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (ok && part == 0) {
+      const float v = actf(a.actO, acc + sbO[o]);
+      g5[e] = v;
+      y5[e] = v;
     }
-#pragma unroll 1
-    for (; k < h; ++k) a0 += hr[k] * wo[k];
-    const float v = actf(a.actO, ((a0 + a1) + (a2 + a3)) + sbO[o]);
-    g5[e] = v;
-    y5[e] = v;
   }
   __syncthreads();
   HPHASE(11);
@@ -382,11 +387,11 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     if (lane == 0) rowloss[warp] += mine;
   }
   __syncthreads();
-  if (tid == 0) {
-    float v = 0.f;
-#pragma unroll 1
-    for (int w = 0; w < nwarps; ++w) v += rowloss[w];
-    *cluster.map_shared_rank(lossp + rank, 0) = v;
+  if (warp == 0) {  // the per-warp partial losses, fixed xor tree (16 warps)
+    float v = lane < nwarps ? rowloss[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) *cluster.map_shared_rank(lossp + rank, 0) = v;
   }
   HPHASE(12);
   // dW_O | db_O partials over my rows, pushed to the slice owner's slot [rank]
@@ -394,12 +399,10 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   for (int t = tid; t < out * lh; t += nt) {
     const int o = t / lh, i = t - o * lh;
     float acc = 0.f;
-    if (i < h)
-#pragma unroll 1
-      for (int b = 0; b < nr; ++b) acc += g5[b * out + o] * hs[b * lh + i];
-    else
-#pragma unroll 1
-      for (int b = 0; b < nr; ++b) acc += g5[b * out + o];
+    const float* hc = i < h ? hs + i : nullptr;
+#pragma unroll
+    for (int b = 0; b < 8; ++b)  // nr <= R <= 8 (B <= 128 over 16 CTAs)
+      if (b < nr) acc += g5[b * out + o] * (hc ? hc[b * lh] : 1.f);
     const int c = t / d.per5;
     *cluster.map_shared_rank(p5 + rank * d.per5 + (t - c * d.per5), c) = acc;
   }
@@ -409,7 +412,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     const int b = t / d.Hp, i = t - b * d.Hp;
     float acc = 0.f;
     if (b < nr && i < h) {
-#pragma unroll 1
+#pragma unroll 4
       for (int o = 0; o < out; ++o) acc += g5[b * out + o] * W5[o * lh + i];
       if (a.actH != VCNN_ACT_IDENTITY) acc *= actg(a.actH, hs[b * lh + i]);
     }
@@ -465,14 +468,20 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     for (int c = 0; c < kC; ++c) v += lossp[c];
     *a.loss = a.loss_kind == VCNN_LOSS_SOFTMAX_CE ? v / (float)B : v / (float)(B * out);
   }
-  if (rank == 0)
-#pragma unroll 1
-    for (int o = tid; o < h; o += nt) {
-      float acc = 0.f;
-#pragma unroll 1
-      for (int b = 0; b < B; ++b) acc += G[b * sH + o];
-      a.dbH[o] = acc;
-    }
+  if (rank == 0) {
+    // db_H = column sums of gH: 8 lanes per unit, each over a contiguous
+    // run of rows (independent loads), then a fixed xor tree (h <= 64 = nt/8)
+    const int o = tid >> 3, part = tid & 7, per = (B + 7) >> 3;
+    const int b0 = part * per, b1 = b0 + per < B ? b0 + per : B;
+    float acc = 0.f;
+    if (o < h)
+#pragma unroll 4
+      for (int b = b0; b < b1; ++b) acc += G[b * sH + o];
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (o < h && part == 0) a.dbH[o] = acc;
+  }
   HPHASE(7);
 
   // ---- 4: on the tensor cores, one tile pool:
@@ -563,15 +572,25 @@ size_t mlp_head_smem(int B, int in, int h, int out) {
   return sizeof(float) * (size_t)dims_of(B, in, h, out).total;
 }
 
-// cluster of kC CTAs with this kernel's shared memory schedulable? (cached)
-static bool cluster_ok(size_t smem) {
-  static size_t ok_upto = 0, bad_from = ~(size_t)0;
-  if (smem <= ok_upto) return true;
-  if (smem >= bad_from) return false;
-  bool ok = cudaFuncSetAttribute(mlp_head_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                 1) == cudaSuccess &&
-            cudaFuncSetAttribute(mlp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) == cudaSuccess;
+using HeadFn = void (*)(MlpArgs);
+// the specialised shape (CIFAR-3: B 128, 5*5*32 -> 64 -> 10) or the generic kernel
+static HeadFn head_fn(int B, int in, int h, int out) {
+  if (B == 128 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<128, 800, 64, 10>;
+  return mlp_head_kernel<0, 0, 0, 0>;
+}
+
+// cluster of kC CTAs with this kernel's shared memory schedulable? (cached per kernel)
+static bool cluster_ok(HeadFn fn, size_t smem) {
+  struct Cache { HeadFn fn; size_t ok_upto, bad_from; };
+  static Cache cache[2] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0}};
+  Cache* c = cache[0].fn == fn || cache[0].fn == nullptr ? &cache[0] : &cache[1];
+  c->fn = fn;
+  if (smem <= c->ok_upto) return true;
+  if (smem >= c->bad_from) return false;
+  bool ok = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                cudaSuccess &&
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                cudaSuccess;
   if (ok) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kC);
@@ -585,12 +604,11 @@ static bool cluster_ok(size_t smem) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    ok = cudaOccupancyMaxActiveClusters(&nclusters, mlp_head_kernel, &cfg) == cudaSuccess &&
-         nclusters > 0;
+    ok = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) == cudaSuccess && nclusters > 0;
   }
   cudaGetLastError();
-  if (ok) ok_upto = smem;
-  else bad_from = smem;
+  if (ok) c->ok_upto = smem;
+  else c->bad_from = smem;
   return ok;
 }
 
@@ -598,7 +616,7 @@ bool mlp_head_fusable(int B, int in, int h, int out) {
   if (B < 1 || B > 128 || h < 1 || h > 64 || out < 1 || out > 64 || in < kC || in > 128 * kC)
     return false;
   const size_t smem = mlp_head_smem(B, in, h, out);
-  return smem <= 200 * 1024 && cluster_ok(smem);
+  return smem <= 200 * 1024 && cluster_ok(head_fn(B, in, h, out), smem);
 }
 
 int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* WH,
@@ -607,7 +625,8 @@ int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* 
                     float* loss, int* err, float* gH, float* gO, float* dWH, float* dbH,
                     float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st) {
   const size_t smem = mlp_head_smem(B, in, h, out);
-  if (!cluster_ok(smem)) return fail(VCNN_ECUDA, "mlp head: cluster not schedulable");
+  const HeadFn fn = head_fn(B, in, h, out);
+  if (!cluster_ok(fn, smem)) return fail(VCNN_ECUDA, "mlp head: cluster not schedulable");
   const bool vec = in % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) |
                                     reinterpret_cast<uintptr_t>(WH)) & 15) == 0;
   MlpArgs a{B, in, h, out, x, WH, bH, actH, WO, bO, actO, yH, yO, loss_kind, cls, values,
@@ -626,7 +645,7 @@ int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* 
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  VCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, mlp_head_kernel, a));
+  VCNN_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

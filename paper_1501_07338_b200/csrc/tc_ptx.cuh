@@ -92,6 +92,29 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// the same MMA issued from a CONVERGED warp: elect.sync picks the issuing
+// lane inside the asm, so the loop around it stays warp-uniform and its
+// descriptors live on the uniform datapath (no per-MMA R2UR round trips).
+// Measured (scripts/micro/mma_issue.cu, M=128 K=8 N=32): 41 cycles per MMA vs
+// 56 from a one-thread branch -- the MMA itself is then bound by its shared
+// memory operand reads (A 4 KB + B N*32 B at 128 B/clk)
+__device__ __forceinline__ void mma_tf32_warp(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// commit from a converged warp (one elected lane)
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar)));
+}
 // arrive on an mbarrier once all previously issued tcgen05 ops complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
