@@ -44,7 +44,7 @@ namespace direct {
 
 namespace {
 
-constexpr int NT = 128;
+constexpr int NT = 256;  // 8 warps: warp w drains TMEM lane quadrant w % 4, column half w / 4
 constexpr int BM = 128;
 constexpr int EPS = BM + 1;  // epilogue tile row stride (floats): conflict-free per-map reads
 constexpr size_t kSmemOptin = 227 * 1024;
@@ -70,19 +70,105 @@ struct Geo {
   int SC, nchunk;          // shifts (ky,kx) per chunk, chunks
   int seg, nseg, segw;     // 1-D row segments (kh == 1, rows wider than a tile): segments
                            // per output row, outputs per segment
+  int ts, T, ngx, NM;      // tap-stacked tile (Cout <= 32): the MMA's M rows are T taps x 32
+                           // maps of one kernel row (ngx groups per row), N = NM positions
+  int eps, off_ep;         // epilogue staging: row stride (floats), offset (bytes)
 };
+
+// kernel "shifts" the MMA loop walks: taps, or tap groups in the stacked mode
+__host__ __device__ inline int nshift(const Geo& g) { return g.ts ? g.kh * g.ngx : g.kh * g.kw; }
+
+// the tap-stacked mode can be switched off (VCNN_TAPSTACK=0) for A/B runs
+inline bool tapstack_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("VCNN_TAPSTACK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // pack layout per N block: [s = ky*kw+kx][cg][BN/8][2][8][4] (K-major
 // no-swizzle core matrices: LBO = 128 B between the two 4-channel halves,
 // SBO = 256 B between 8-row groups)
 __host__ __device__ inline int64_t pack_floats_per_block(const Geo& g) {
-  return (int64_t)g.kh * g.kw * g.CG * g.BN * 8;
+  return (int64_t)nshift(g) * g.CG * g.BN * 8;
 }
 
 // bytes of pack chunk c (the last chunk may hold fewer shifts)
 __host__ __device__ inline uint32_t chunk_bytes(const Geo& g, int c) {
-  const int s1 = (c + 1) * g.SC < g.kh * g.kw ? (c + 1) * g.SC : g.kh * g.kw;
+  const int s1 = (c + 1) * g.SC < nshift(g) ? (c + 1) * g.SC : nshift(g);
   return (uint32_t)((s1 - c * g.SC) * g.CG * g.BN * 32);
+}
+
+// tap-stacked plan (see plan()): g.Cin/Hin/.../Wg already set
+bool plan_ts(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int tma) {
+  if (tma) return false;  // (the stacked tile builds its own slab)
+  constexpr int kMaxN = 256;
+  g.ts = 1;
+  g.T = 4;
+  g.ngx = (int)cdiv(g.kw, g.T);
+  int R = (kMaxN - (g.T - 1)) / g.Wg;  // positions R*Wg + T-1 <= 256 (one MMA N)
+  if (R > g.Hout) R = g.Hout;
+  // at least two row tiles per image with a 2-deep weight ring, so two CTAs
+  // share an SM and one's MMAs overlap the other's staging / epilogue
+  // (CIFAR-3 conv2 fwd b128: 12.6 us vs 13.2 us for one whole-image tile
+  // with a 3-deep ring and 14.5 us unstacked)
+  if (g.Hout >= 4) {
+    int half = (g.Hout + 1) / 2;
+    if (pool && mode == 0) half = (int)cdiv(half, pool) * pool;  // whole pool windows
+    if (R > half) R = half;
+  }
+  const int nt = (int)cdiv(g.Hout, R);
+  if (pool && mode == 0) {
+    R = (R / pool) * pool;
+    if (R < 1) return false;
+    R = pool * (int)cdiv(cdiv(g.Hout, pool), cdiv(g.Hout, R));
+  } else {
+    R = (int)cdiv(g.Hout, nt);
+  }
+  g.R = R;
+  g.tpi = (int)cdiv(g.Hout, R);
+  g.CG = (int)cdiv(g.Cin, 8);
+  g.NM = (int)cdiv(R * g.Wg + g.T - 1, 16) * 16;
+  if (g.NM > kMaxN) return false;
+  const int maxsh = (g.kh - 1) * g.Wg + (g.ngx - 1) * g.T;
+  g.NP = (int)cdiv(maxsh + g.NM, 8) * 8;
+  if ((g.Cin * g.Hin * g.Win) % 4 != 0) return false;
+  if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
+  g.raw_n = g.Cin * g.Hin * g.Win;
+  if (mode == 1) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
+  const int a_bytes = g.CG * 2 * g.NP * 16 + 4 * g.NP;
+  const int raw_bytes = 4 * g.raw_n;
+  const int win_bytes = 2 * 4 * g.win_n;
+  if (raw_bytes > 96 * 1024) return false;
+  g.BN = BM;  // pack rows: T taps x 32 maps
+  g.nblk = 1;
+  g.SC = g.ngx;  // one kernel row of tap groups per chunk
+  g.nchunk = g.kh;
+  g.wchunk = g.ngx * g.CG * g.BN * 32;
+  g.eps = g.NM + 1;  // odd: conflict-free per-lane rows
+  const int ep_bytes = 4 * 32 * g.eps * 4;
+  const int yp_floats = mode == 1 ? g.Cout * g.Hout * g.Wout : 0;
+  const int yp_bytes = (yp_floats % 4 == 0 && 4 * yp_floats <= 48 * 1024) ? 4 * yp_floats : 0;
+  for (int nbuf = g.nchunk >= 2 ? 2 : g.nchunk; nbuf >= 1; --nbuf) {
+    const int b_bytes = nbuf * g.wchunk;
+    const int body = b_bytes + raw_bytes + win_bytes + a_bytes;
+    int total = (body > ep_bytes ? body : ep_bytes) + 1024;
+    const bool stage_yp = yp_bytes && (size_t)(total + yp_bytes) + 512 <= kSmemOptin;
+    const int off_yp = total - 1024;
+    if (stage_yp) total += yp_bytes;
+    if ((size_t)total + 512 > kSmemOptin) continue;
+    g.nbuf = nbuf;
+    g.off_b = 0;
+    g.off_raw = b_bytes;
+    g.off_win = g.off_raw + raw_bytes;
+    g.off_a = g.off_win + win_bytes;
+    g.off_ep = 0;  // over the ring, raw, windows and slab (all dead by then)
+    g.off_yp = stage_yp ? off_yp : -1;
+    g.smem = total;
+    return (int64_t)g.B * g.tpi < (1 << 24);
+  }
+  return false;
 }
 
 bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int tma = 0) {
@@ -111,6 +197,17 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
   // a forward view with < 4 input channels pads the MMA K (8 channels) by 2x
   // or more; those layers go to the small-Kd kernel or the generic implicit GEMM
   if (mode == 0 && g.Cin < 4) return false;
+  // tap-stacked tiles (a function of the conv alone, so every variant of a
+  // layer -- pooled, routed, packed -- agrees on the pack layout): when the
+  // output has <= 32 maps an M=128 MMA over positions x maps reads 4 KB of A
+  // for 32 columns of N; instead the M rows are 4 taps x 32 maps (weights)
+  // and N = up to 256 positions (the slab), ~4x less operand traffic per MAC
+  // (scripts/micro/mma_issue.cu: an M=128 K=8 tf32 MMA costs ~32 + N/4
+  // cycles -- its shared-memory operand reads)
+  if (tapstack_enabled() && mode == 0 && !g.seg && g.Cout <= 32 && g.kw >= 3 && g.Wg <= 63 &&
+      d.kd() >= 32)
+    return plan_ts(d, mode, pool, POH, POW, g, tma);
+  g.eps = EPS;
   int R = g.seg ? 1 : BM / g.Wg;
   if (R > g.Hout) R = g.Hout;
   if (g.seg) {
@@ -185,6 +282,7 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
       g.off_raw = b_bytes;
       g.off_win = g.off_raw + raw_bytes;
       g.off_a = g.off_win + win_bytes;  // (tma: == off_raw, the epilogue tile reuses the slab)
+      g.off_ep = g.off_raw;
       g.off_yp = stage_yp ? b_bytes + tail : -1;
       g.smem = total;
       return (int64_t)g.B * g.tpi < (1 << 24);
@@ -212,8 +310,12 @@ __global__ void pack_kernel(Geo g, int mode, const float* __restrict__ w, float*
     const int row = nb * g.BN + rg * 8 + r8;  // GEMM N index
     const int ch = cg * 8 + kh2 * 4 + k4;     // GEMM K index (input channel of the view)
     float v = 0.f;
-    if (row < g.Cout && ch < g.Cin) {
-      const int ky = s / g.kw, kx = s - (s / g.kw) * g.kw;
+    // tap-stacked: pack row = j * 32 + map, shift = ky * ngx + gx, tap kx = gx * T + j
+    const int prow = g.ts ? (row & 31) : row;
+    const int ky = g.ts ? s / g.ngx : s / g.kw;
+    const int kx = g.ts ? (s - ky * g.ngx) * g.T + (row >> 5) : s - ky * g.kw;
+    if (prow < g.Cout && ch < g.Cin && kx < g.kw) {
+      const int row = prow;
       const int n = mode == 0 ? row : ch, c = mode == 0 ? ch : row;
       const int wy = mode == 0 ? ky : g.kh - 1 - ky, wx = mode == 0 ? kx : g.kw - 1 - kx;
       v = ptx::to_tf32(w[(((int64_t)n * Cch + c) * g.kh + wy) * g.kw + wx]);
@@ -254,11 +356,22 @@ struct alignas(64) Args {
   BwdEpi be;
 };
 
+// one accumulator value at staging address e: plain, or (tap-stacked) the sum
+// of the four row blocks, block j shifted by j columns -- fixed order
+template <bool TS>
+__device__ __forceinline__ float epv(uint32_t e, int eps) {
+  if (!TS) return ptx::lds_f32(e);
+  const uint32_t bs = 4u * (uint32_t)(32 * eps + 1);  // next block, next column
+  const float v0 = ptx::lds_f32(e), v1 = ptx::lds_f32(e + bs), v2 = ptx::lds_f32(e + 2 * bs),
+              v3 = ptx::lds_f32(e + 3 * bs);
+  return ((v0 + v1) + v2) + v3;
+}
+
 // Epilogues read the accumulator tile ep[n][128] (position m = r*Wg + x) from
 // shared memory.  Work is spread warp = output row, lane = column, loop =
 // map, so no thread divides by a runtime extent; stores along a row are
 // coalesced.
-template <int ACT>
+template <int ACT, bool TS>
 __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, int x0) {
   const Geo& g = a.g;
   const FwdEpi& e = a.fe;
@@ -274,8 +387,9 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
       for (int x = x0 + lane; x < x1; x += 32) {
         float* yp = e.y + plane0 * ohw + (int64_t)(r0 + r) * g.Wout + x;
         const uint32_t ep = eb + 4u * (r * g.Wg + x - x0);
+#pragma unroll 4
         for (int n = 0; n < nmaps; ++n)
-          yp[n * ohw] = actf<ACT>(ptx::lds_f32(ep + 4u * (n * EPS)) + __ldg(e.bias + n0 + n));
+          yp[n * ohw] = actf<ACT>(epv<TS>(ep + 4u * (n * g.eps), g.eps) + __ldg(e.bias + n0 + n));
       }
   }
   if (e.pool) {
@@ -287,7 +401,7 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
     const int nwin = nwr * e.POW;
     for (int n = lane; n < nmaps; n += 32) {
       const float bn_ = __ldg(e.bias + n0 + n);
-      const uint32_t en = eb + 4u * (n * EPS);
+      const uint32_t en = eb + 4u * (n * g.eps);
       int wr = 0, wc = warp;
       while (wc >= e.POW) {
         wc -= e.POW;
@@ -297,11 +411,11 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
         {
           const int ry = wr * p, cx = wc * p;
           const int64_t o0 = plane0 * pplane + (int64_t)(r0 / p + wr) * e.POW + wc;
-          float best = actf<ACT>(ptx::lds_f32(en + 4u * (ry * g.Wg + cx)) + bn_);
+          float best = actf<ACT>(epv<TS>(en + 4u * (ry * g.Wg + cx), g.eps) + bn_);
           int by = 0, bx = 0;
           for (int u = 0; u < p; ++u)
             for (int v = 0; v < p; ++v) {
-              const float val = actf<ACT>(ptx::lds_f32(en + 4u * ((ry + u) * g.Wg + cx + v)) + bn_);
+              const float val = actf<ACT>(epv<TS>(en + 4u * ((ry + u) * g.Wg + cx + v), g.eps) + bn_);
               if (val > best) {
                 best = val;
                 by = u;
@@ -325,7 +439,7 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
 // dgrad epilogue: lane = output position of the tile (coalesced along x),
 // warp = channel slice; the yprev loads of 16 (position, channel) pairs are
 // in flight together (read-only path).
-template <int ACT>
+template <int ACT, bool TS>
 __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, int x0) {
   const Geo& g = a.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -339,17 +453,17 @@ __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
   const float* yp = a.be.yprev;
   // yprev staged in shared memory (whole image) when the plan had room
   const bool ys = yp && g.off_yp >= 0;
-  const uint32_t s_yp = eb - (uint32_t)g.off_raw + (uint32_t)(g.off_yp < 0 ? 0 : g.off_yp);
+  const uint32_t s_yp = eb - (uint32_t)g.off_ep + (uint32_t)(g.off_yp < 0 ? 0 : g.off_yp);
   for (int p = lane; p < npix; p += 32) {
     const int r = p / wid, x = x0 + (p - r * wid);
     const int64_t o = plane0 * hw + (int64_t)(r0 + r) * g.Wout + x;
     const uint32_t ep = eb + 4u * (r * g.Wg + x - x0);
     const int lo = (r0 + r) * g.Wout + x;  // offset inside one channel plane
-    for (int c0 = warp; c0 < nch; c0 += 4 * 16) {
+    for (int c0 = warp; c0 < nch; c0 += (NT / 32) * 16) {
       float yv[16];
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const int c = c0 + 4 * u;
+        const int c = c0 + (NT / 32) * u;
         yv[u] = (yp && c < nch)
                     ? (ys ? ptx::lds_f32(s_yp + 4u * (uint32_t)((n0 + c) * (int)hw + lo))
                           : __ldg(yp + o + c * hw))
@@ -357,9 +471,9 @@ __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
       }
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
-        const int c = c0 + 4 * u;
+        const int c = c0 + (NT / 32) * u;
         if (c >= nch) break;
-        float v = ptx::lds_f32(ep + 4u * (c * EPS));
+        float v = epv<TS>(ep + 4u * (c * g.eps), g.eps);
         if (yp) {
           if (ACT == VCNN_ACT_RELU) v *= yv[u] > 0.f ? 1.f : 0.f;
           else if (ACT == VCNN_ACT_SIGMOID) v *= yv[u] * (1.f - yv[u]);
@@ -411,7 +525,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  __shared__ uint64_t load_bar, done_bar, wfull[2], wempty[2];
+  __shared__ uint64_t load_bar, done_bar, wfull[3], wempty[3];  // ring depth <= 3
   __shared__ uint32_t tmem_base_sh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int tile = blockIdx.x, nb = blockIdx.y;
@@ -438,7 +552,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   // skips the kernel taps whose view of the zero-padded gradient is empty
   // for every valid position (they would add exact zeros) -- 121 -> 92 taps
   // per tile on deconv-121's 1x121 layer; their pack chunks are not loaded
-  int s_lo = 0, s_hi = g.kh * g.kw - 1;
+  int s_lo = 0, s_hi = nshift(g) - 1;
   if (g.seg && g.mode == 1) {
     const int wid = (x0 + g.segw < g.Wout ? x0 + g.segw : g.Wout) - x0;
     const int lo = g.pad_x - x0 - (wid - 1), hi = g.pad_x - x0 + g.Win - 1;
@@ -581,7 +695,35 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   DPHASE(3);
   // ---- one elected lane of warp 0 issues every MMA (converged warp: the
   // tcgen05 issue stays on the uniform datapath) ----
-  if (warp == 0 && ptx::elect_one()) {
+  if (g.ts && warp == 0 && ptx::elect_one()) {
+    // stacked: A = the pack block of (kernel row ky, tap group gx, channel
+    // group) -- 128 rows = 4 taps x 32 maps; B = the slab viewed at the
+    // group's first tap (ky * Wg + gx * T), N = NM positions.  Row block j of
+    // the accumulator at column n holds tap gx*T+j's products for output
+    // position n - j (summed in the epilogue)
+    const uint32_t idesc = ptx::idesc_tf32(BM, g.NM);
+    const uint32_t half = (uint32_t)g.NP * 16u;
+    const uint64_t b0 = ptx::interleave_desc(s_a, half, 128u);
+    const uint64_t b_cg = (uint64_t)(2u * half >> 4), a_blk = (uint64_t)(BM * 32 >> 4);
+    uint32_t acc = 0;
+    for (int lc = 0; lc < nloc; ++lc) {
+      const int ky = c_lo + lc, buf = lc % g.nbuf;
+      ptx::mbar_wait(&wfull[buf], (uint32_t)(lc / g.nbuf) & 1u);
+      ptx::tc_fence_after();
+      uint64_t ad = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u);
+      for (int gx = 0; gx < g.ngx; ++gx) {
+        uint64_t bd = b0 + (uint64_t)(ky * g.Wg + gx * g.T);
+        for (int cg = 0; cg < g.CG; ++cg) {
+          ptx::mma_tf32(tmem, ad, bd, idesc, acc);
+          acc = 1;
+          ad += a_blk;
+          bd += b_cg;
+        }
+      }
+      ptx::mma_commit(&wempty[buf]);
+    }
+    ptx::mma_commit(&done_bar);
+  } else if (!g.ts && warp == 0 && ptx::elect_one()) {
     const uint32_t idesc = ptx::idesc_tf32(BM, g.BN);  // both operands K-major
     const uint32_t half = (uint32_t)g.NP * 16u;          // LBO: the two 4-channel halves
     // descriptors advance by plain additions on the start-address field
@@ -632,10 +774,35 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   DPHASE(4);
 
   // ---- epilogue: TMEM -> smem [n][128] (over raw / window / slab) -> stores ----
-  {
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    const int row = warp * 32 + lane;
-    for (int c = 0; c < g.BN; c += 16) {
+  const uint32_t s_ep = sbase + (uint32_t)g.off_ep;
+  if (g.ts) {
+    // warp j holds row block j (tap offset j): stage all four; the epilogue
+    // reads out[m][p] = ((S0[m][p] + S1[m][p+1]) + S2[m][p+2]) + S3[m][p+3]
+    const int quad = warp & 3;
+    const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
+    const uint32_t srow = s_ep + 4u * (uint32_t)((quad * 32 + lane) * g.eps);
+    // the two warps of a lane quadrant take alternate 16-column slices; four
+    // loads in flight per wait (the load latency bounds this loop)
+    for (int c = 16 * (warp >> 2); c < g.NM; c += 128) {
+      uint32_t r[4][16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + 32 * q < g.NM) ptx::tmem_ld16(trow + (uint32_t)(c + 32 * q), r[q]);
+      ptx::tmem_wait_ld();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + 32 * q < g.NM)
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj)
+            ptx::sts_f32(srow + 4u * (c + 32 * q + jj), __uint_as_float(r[q][jj]));
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    DPHASE(7);
+  } else {
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int row = (warp & 3) * 32 + lane;
+    for (int c = 16 * (warp >> 2); c < g.BN; c += 32) {
       uint32_t r[16];
       ptx::tmem_ld16(trow + (uint32_t)c, r);
       ptx::tmem_wait_ld();
@@ -651,11 +818,15 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     for (int i = tid; i < 256; i += NT) g_dump[3][i] = ptx::lds_f32(s_raw + 4u * i);
 #endif
   if (g.mode == 0)
-    with_act(a.fe.act,
-             [&](auto A) { fwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0, x0); });
+    with_act(a.fe.act, [&](auto A) {
+      if (g.ts) fwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
+      else fwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
+    });
   else
-    with_act(a.be.act_prev,
-             [&](auto A) { bwd_epilogue<decltype(A)::value>(a, s_raw, b, r0, n0, x0); });
+    with_act(a.be.act_prev, [&](auto A) {
+      if (g.ts) bwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
+      else bwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
+    });
   DPHASE(5);
   __syncthreads();
   if (warp == 0) ptx::tmem_dealloc(tmem, TMEM_COLS);
@@ -676,7 +847,8 @@ int launch(const Args& a, cudaStream_t st) {
     VCNN_LAUNCHED();
     return VCNN_OK;
   };
-  static size_t cfg32 = 0, cfg64 = 0, cfg128 = 0;
+  static size_t cfg32 = 0, cfg64 = 0, cfg128 = 0, cfg256 = 0;
+  if (g.ts) return go(direct_conv_kernel<256>, cfg256);
   if (g.BN <= 32) return go(direct_conv_kernel<32>, cfg32);
   if (g.BN <= 64) return go(direct_conv_kernel<64>, cfg64);
   return go(direct_conv_kernel<128>, cfg128);
@@ -727,8 +899,13 @@ struct PackTable {
 
 // offset of (row = GEMM N index, ch = GEMM K index, s = ky*kw+kx) in a pack
 __device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int s) {
+  if (g.ts) {  // stacked: row (j = kx % T) * 32 + row, shift ky * ngx + kx / T
+    const int ky = s / g.kw, kx = s - ky * g.kw;
+    row += (kx % g.T) * 32;
+    s = ky * g.ngx + kx / g.T;
+  }
   const int nb = row / g.BN, r = row - nb * g.BN, cg = ch >> 3, kk = ch & 7;
-  return ((((int64_t)nb * g.kh * g.kw + s) * g.CG + cg) * (g.BN / 8) + (r >> 3)) * 64 +
+  return ((((int64_t)nb * nshift(g) + s) * g.CG + cg) * (g.BN / 8) + (r >> 3)) * 64 +
          (kk >> 2) * 32 + (r & 7) * 4 + (kk & 3);
 }
 

@@ -32,7 +32,8 @@ def dphases(tag, fn, reps=3):
         t = [buf[b * 8 + i] for i in range(8)]
         names = ["init", "load-wait", "build", "mma", "epilogue", "dealloc"]
         print("   cta", b, " ".join(f"{n}={t[i + 1] - t[i]}" for i, n in enumerate(names)),
-              "total", t[6] - t[0])
+              "total", t[6] - t[0],
+              f"(stacked: tmem->smem {t[7] - t[4]}, sum+epilogue {t[5] - t[7]})" if t[7] > t[4] else "")
 NAMES = ["setup", "stage", "kloop(prod)", "mma-issue-end", "done-wait", "epilogue", "dealloc"]
 
 
