@@ -939,7 +939,8 @@ __device__ __forceinline__ void update_pack(int64_t i, float gi, float* __restri
 __global__ void __launch_bounds__(32 * kRedSlices) sgd_pack_kernel(
     int64_t n, float* __restrict__ w, float* __restrict__ v, float* __restrict__ g, float lr,
     float mom, float scale, const PackTable t, const float* __restrict__ loss,
-    int* __restrict__ guard, const ImageSumFold fold, int64_t fold_off) {
+    int* __restrict__ guard, const ImageSumFold fold, int64_t fold_off, const ImageSumFold fold2,
+    int64_t fold2_off) {
   PDL_ENTRY();
   // Trainer::fit's non-finite stop (training.hpp:77-80): while the guard is
   // armed, a non-finite batch loss skips this update and every later one, so
@@ -950,8 +951,11 @@ __global__ void __launch_bounds__(32 * kRedSlices) sgd_pack_kernel(
       return;
     }
   }
-  // the folded layer: blocks [0, nfold) sum its per-image partials exactly as
-  // wgrad_reduce_kernel does (same bits), store the gradient, update
+  // the first folded range (many partials): blocks [0, nfold) sum them
+  // exactly as wgrad_reduce_kernel does (same bits), store the gradient,
+  // update.  The second (at most kRedSlices partials, e.g. the tail's batch
+  // slices) is summed inline by the update loop: with one partial per slice
+  // image_sum is the plain in-order sum, so the bits are the same
   const int nfold = fold.part ? (int)cdiv(fold.per, 32) : 0;
   if ((int)blockIdx.x < nfold) {
     __shared__ float red[kRedSlices][33];
@@ -964,9 +968,21 @@ __global__ void __launch_bounds__(32 * kRedSlices) sgd_pack_kernel(
     return;
   }
   const int64_t f0 = nfold ? fold_off : n, f1 = nfold ? fold_off + fold.per : n;
+  const int64_t h0 = fold2.part ? fold2_off : n, h1 = fold2.part ? fold2_off + fold2.per : n;
   for (int64_t i = (blockIdx.x - nfold) * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)(gridDim.x - nfold) * blockDim.x)
-    if (i < f0 || i >= f1) update_pack(i, scale * g[i], w, v, lr, mom, t);
+       i += (int64_t)(gridDim.x - nfold) * blockDim.x) {
+    if (i >= f0 && i < f1) continue;
+    float gi;
+    if (i >= h0 && i < h1) {
+      const float* p = fold2.part + (i - h0);
+      gi = 0.f;
+      for (int k = 0; k < fold2.nimg; ++k) gi += __ldg(p + k * fold2.stride);
+      g[i] = gi;
+    } else {
+      gi = g[i];
+    }
+    update_pack(i, scale * gi, w, v, lr, mom, t);
+  }
 }
 
 // ---- data parallelism: one-shot peer reduce + SGD + packs -----------------
@@ -1072,20 +1088,27 @@ int pack_table(const std::vector<PackSpec>& layers, PackTable& t) {
 
 int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss,
-             int* guard, const ImageSumFold* fold, int64_t fold_off) {
+             int* guard, const ImageSumFold* fold, int64_t fold_off, const ImageSumFold* fold2,
+             int64_t fold2_off) {
   PackTable t;
   if (int s = pack_table(layers, t)) return s;
   constexpr int kT = 32 * kRedSlices;
   int64_t blocks = cdiv(n, kT);
   if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
   if (blocks < 1) blocks = 1;
-  ImageSumFold f{};
+  ImageSumFold f{}, f2{};
   if (fold && fold->part) {
     if (fold_off < 0 || fold_off + fold->per > n) return fail(VCNN_ESHAPE, "sgd_pack: fold range");
     f = *fold;
     blocks += cdiv(f.per, 32);
   }
-  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(kT), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard, f, fold_off));
+  if (fold2 && fold2->part) {
+    if (fold2_off < 0 || fold2_off + fold2->per > n || fold2->nimg > kRedSlices ||
+        (f.part && fold2_off < fold_off + f.per && fold_off < fold2_off + fold2->per))
+      return fail(VCNN_ESHAPE, "sgd_pack: fold range");
+    f2 = *fold2;
+  }
+  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(kT), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard, f, fold_off, f2, fold2_off));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

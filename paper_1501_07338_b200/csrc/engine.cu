@@ -159,6 +159,13 @@ struct vcnn_net {
   // path); forward_backward alone reduces as usual
   bool defer_fold = false;
   direct::ImageSumFold fold{};
+  // the two-layer tail in batch slices (mlp_head_slices): per-slice dW / db
+  // partials [2][per] (folded into the update like layer 0's, or summed by a
+  // reduce launch), loss partials + ticket (tail_aux[0..3], [4])
+  float* tail_part = nullptr;
+  float* tail_aux = nullptr;
+  direct::ImageSumFold fold2{};
+  int64_t fold2_off = 0;
   // breakdown timer
   bool breakdown = false;
   struct MarkRec {
@@ -386,13 +393,24 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
     const LayerRt* prev = nl > 2 ? &n->L[nl - 3] : nullptr;
     int act_prev = prev ? prev->spec.act : VCNN_ACT_IDENTITY;
     if (nl > 3 && fused_pool_of(n, (size_t)(nl - 4), B)) act_prev = n->L[nl - 4].spec.act;
-    TRY(launch_mlp_head(B, (int)hl.in_per, hl.spec.units, last.spec.units,
-                        prev ? prev->out : n->x, n->params + hl.w_off, n->params + hl.b_off,
-                        hl.spec.act, n->params + last.w_off, n->params + last.b_off,
-                        last.spec.act, hl.out, last.out, n->spec.loss, n->cls, n->values,
-                        n->loss, n->err, hl.gpre, last.gpre, n->grads + hl.w_off,
-                        n->grads + hl.b_off, n->grads + last.w_off, n->grads + last.b_off,
-                        prev ? prev->gpre : nullptr, act_prev, st));
+    const int hin = (int)hl.in_per, hh = hl.spec.units, ho = last.spec.units;
+    const int ncl = n->tail_part ? mlp_head_slices(B, hin, hh, ho) : 1;
+    TRY(launch_mlp_head(B, hin, hh, ho, prev ? prev->out : n->x, n->params + hl.w_off,
+                        n->params + hl.b_off, hl.spec.act, n->params + last.w_off,
+                        n->params + last.b_off, last.spec.act, hl.out, last.out, n->spec.loss,
+                        n->cls, n->values, n->loss, n->err, hl.gpre, last.gpre,
+                        n->grads + hl.w_off, n->grads + hl.b_off, n->grads + last.w_off,
+                        n->grads + last.b_off, prev ? prev->gpre : nullptr, act_prev, st, ncl,
+                        n->tail_part, n->tail_aux, reinterpret_cast<unsigned*>(n->tail_aux + 4)));
+    if (ncl > 1) {  // the slices' dW / db: summed in slice order by the update, or here
+      const int64_t per = (int64_t)hh * hin + hh + (int64_t)ho * hh + ho;
+      if (n->defer_fold) {
+        n->fold2 = direct::ImageSumFold{n->tail_part, ncl, per, per};
+        n->fold2_off = hl.w_off;
+      } else {
+        TRY(direct::sum_partials(ncl, per, per, n->tail_part, n->grads + hl.w_off, st));
+      }
+    }
   } else if (tail == 1) {  // last full layer fwd + loss + its backward, one kernel
     Mark m(n, OTHER_F, nl - 1, OP_LOSS);
     const LayerRt* prev = nl > 1 ? &n->L[nl - 2] : nullptr;
@@ -411,7 +429,8 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
   }
   // weight gradients on the side stream (not in breakdown mode, whose
   // per-op events live on the main stream)
-  const bool par = n->side && !n->breakdown;
+  static const bool no_side = getenv("VCNN_NO_SIDE") != nullptr;  // A/B experiments
+  const bool par = n->side && !n->breakdown && !no_side;
   const cudaStream_t sw = par ? n->side : st;
   const Workspace& wsw = par ? n->ws2 : n->ws;
   for (int i = nl - 1 - (tail ? tail : 0); i >= 0; --i) {
@@ -551,8 +570,9 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   if (!dp || dp->world == 1) {
     TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
                          n->stream, n->loss, n->err + 2, n->fold.part ? &n->fold : nullptr,
-                         n->L[0].w_off));
+                         n->L[0].w_off, n->fold2.part ? &n->fold2 : nullptr, n->fold2_off));
     n->fold = direct::ImageSumFold{};
+    n->fold2 = direct::ImageSumFold{};
   } else if (dp->mode == VCNN_DP_P2P) {
     // one kernel: rank-ordered sum of every replica's gradient (peers over
     // NVLink) + SGD + packs
@@ -611,6 +631,7 @@ int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   TRY(run_forward(n, batch, tail));
   n->defer_fold = !n->dp || n->dp->world == 1;
   n->fold = direct::ImageSumFold{};
+  n->fold2 = direct::ImageSumFold{};
   const int sb = run_backward(n, batch, tail);
   n->defer_fold = false;
   if (sb) return sb;
@@ -937,6 +958,19 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
     s = dalloc((void**)&p.nhwc, sizeof(float) * (size_t)(p.out_per * max_batch));
     if (!s && direct::make_nhwc_map(dc, p.nhwc, c.tmap) == VCNN_OK) c.has_tmap = true;
   }
+  {  // the two-layer tail's batch-slice partials (mlp_head_slices <= 2)
+    const size_t nl = n->L.size();
+    if (nl >= 2 && n->L[nl - 1].spec.kind == VCNN_LAYER_FULL &&
+        (n->L[nl - 2].spec.kind == VCNN_LAYER_FULL || conv_is_dense(n->L[nl - 2]))) {
+      const LayerRt& hl = n->L[nl - 2];
+      const LayerRt& ll = n->L[nl - 1];
+      const size_t per = (size_t)(hl.w_len + hl.b_len + ll.w_len + ll.b_len);
+      s = s ? s : dalloc((void**)&n->tail_part, sizeof(float) * 2 * per);
+      s = s ? s : dalloc((void**)&n->tail_aux, sizeof(float) * 8);
+      if (!s && cudaMemset(n->tail_aux, 0, sizeof(float) * 8) != cudaSuccess)
+        s = fail(VCNN_ECUDA, "net_create: tail buffers");
+    }
+  }
   if (wsb) {
     s = s ? s : dalloc((void**)&n->ws.ptr, wsb);
     n->ws.bytes = wsb;
@@ -1002,6 +1036,8 @@ int vcnn_net_destroy(vcnn_net* n) {
   cudaFree(n->err);
   cudaFree(n->ws.ptr);
   cudaFree(n->ws2.ptr);
+  cudaFree(n->tail_part);
+  cudaFree(n->tail_aux);
   for (cudaEvent_t e : n->fork_ev)
     if (e) cudaEventDestroy(e);
   if (n->join_ev) cudaEventDestroy(n->join_ev);

@@ -86,6 +86,12 @@ struct MlpArgs {
   float* dWH; float* dbH; float* dWO; float* dbO;
   float* dx; int act_prev;    // dx * act_prev'(x); null for the first layer
   int vec;                    // x / W_H rows 16B aligned: float4 staging
+  // batch slices: cluster c owns rows [c*B, (c+1)*B) of the Bg-row batch; with
+  // more than one cluster the dW/db of each slice go to part + c*per (param
+  // order W_H | b_H | W_O | b_O; the caller sums the slices in order) and the
+  // loss partials are summed by the last cluster to finish (ticket)
+  int Bg, ncl;
+  float* part; float* lpart; unsigned* ticket;
 };
 
 #ifdef VCNN_PHASE_TIMING
@@ -207,6 +213,23 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   const int rank = (int)cluster.block_rank();
   const int B = TB ? TB : a.B, in = TIN ? TIN : a.in, h = TH ? TH : a.h,
             out = TOUT ? TOUT : a.out;
+  // this cluster's batch slice (rows rb .. rb + B of the Bg-row batch)
+  const int cid = (int)(blockIdx.x / kC), Bg = a.Bg;
+  const size_t rb = (size_t)cid * B;
+  const float* x_ = a.x + rb * in;
+  const int* cls_ = a.cls ? a.cls + rb : nullptr;
+  const float* vals_ = a.values ? a.values + rb * out : nullptr;
+  float* yH_ = a.yH + rb * h;
+  float* gH_ = a.gH + rb * h;
+  float* yO_ = a.yO + rb * out;
+  float* gO_ = a.gO + rb * out;
+  float* dx_ = a.dx ? a.dx + rb * in : nullptr;
+  const size_t per = (size_t)h * in + h + (size_t)out * h + out;
+  float* sl = a.ncl > 1 ? a.part + cid * per : nullptr;
+  float* dWH_ = sl ? sl : a.dWH;
+  float* dbH_ = sl ? sl + (size_t)h * in : a.dbH;
+  float* dWO_ = sl ? sl + (size_t)h * in + h : a.dWO;
+  float* dbO_ = sl ? sl + (size_t)h * in + h + (size_t)out * h : a.dbO;
   const Dims d = dims_of(B, in, h, out);
   const int tid = threadIdx.x, nt = kThreadsM, lane = tid & 31, warp = tid >> 5;
   const int nwarps = nt >> 5;
@@ -245,7 +268,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     i -= h;
     if (i < out) return __ldg(a.bO + i);
     i -= out;
-    return ce ? __int_as_float(__ldg(a.cls + r0 + i)) : __ldg(a.values + (size_t)r0 * out + i);
+    return ce ? __int_as_float(__ldg(cls_ + r0 + i)) : __ldg(vals_ + (size_t)r0 * out + i);
   };
   auto small_dst = [&](int i) -> float* {
     if (i < nw5) return W5 + (i / h) * lh + (i - (i / h) * h);
@@ -259,7 +282,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   // instruction footprint is fetched cold -- code size is latency here)
   const float sv0 = tid < nsmall ? small_src(tid) : 0.f;
   const float sv1 = tid + nt < nsmall ? small_src(tid + nt) : 0.f;
-  stage_cols(xr, sK, a.x, in, B, d.Bp, k0, nc, d.Kp, a.vec, tid, nt);
+  stage_cols(xr, sK, x_, in, B, d.Bp, k0, nc, d.Kp, a.vec, tid, nt);
   stage_cols(wr, sK, a.WH, in, h, d.Hp, k0, nc, d.Kp, a.vec, tid, nt, true);  // MMA-only: tf32
   if (tid < nsmall) *small_dst(tid) = sv0;
   if (tid + nt < nsmall) *small_dst(tid + nt) = sv1;
@@ -342,7 +365,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   // the classes (shuffle-tree max / sum); MSE: one thread per element.  The
   // partial loss: per-warp values summed by thread 0 in warp order.
   if (ce) {
-    const float inv_b = 1.0f / (float)B;
+    const float inv_b = 1.0f / (float)Bg;
 #pragma unroll 1
     for (int b = warp; b < nr; b += nwarps) {
       float* l = g5 + b * out;
@@ -372,7 +395,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
       }
     }
   } else {
-    const float scale = 2.0f / (float)(B * out);
+    const float scale = 2.0f / (float)(Bg * out);
     float mine = 0.f;
 #pragma unroll 1
     for (int t = tid; t < nr * out; t += nt) {
@@ -439,13 +462,13 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
 #pragma unroll 1
   for (int e = tid; e < nr * h; e += nt) {
     const int b = e / h, o = e - b * h;
-    a.yH[(size_t)r0 * h + e] = hs[b * lh + o];
-    a.gH[(size_t)r0 * h + e] = gl[b * sH + o];
+    yH_[(size_t)r0 * h + e] = hs[b * lh + o];
+    gH_[(size_t)r0 * h + e] = gl[b * sH + o];
   }
 #pragma unroll 1
   for (int e = tid; e < nr * out; e += nt) {
-    a.yO[(size_t)r0 * out + e] = y5[e];
-    a.gO[(size_t)r0 * out + e] = g5[e];
+    yO_[(size_t)r0 * out + e] = y5[e];
+    gO_[(size_t)r0 * out + e] = g5[e];
   }
 
   // ---- 3: my slice of dW_O | db_O and (rank 0) the loss, summed in rank order ----
@@ -458,15 +481,28 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
 #pragma unroll
       for (int c = 0; c < kC; ++c) acc += p5[c * d.per5 + (e - e0)];
       const int o = e / lh, i = e - o * lh;
-      if (i < h) a.dWO[(size_t)o * h + i] = acc;
-      else a.dbO[o] = acc;
+      if (i < h) dWO_[(size_t)o * h + i] = acc;
+      else dbO_[o] = acc;
     }
   }
   if (rank == 0 && tid == 0 && a.loss) {
     float v = 0.f;
 #pragma unroll 1
     for (int c = 0; c < kC; ++c) v += lossp[c];
-    *a.loss = a.loss_kind == VCNN_LOSS_SOFTMAX_CE ? v / (float)B : v / (float)(B * out);
+    const float norm = a.loss_kind == VCNN_LOSS_SOFTMAX_CE ? (float)Bg : (float)(Bg * out);
+    if (a.ncl == 1) {
+      *a.loss = v / norm;
+    } else {  // the last slice to finish sums the partials in slice order
+      a.lpart[cid] = v;
+      __threadfence();
+      if (atomicAdd(a.ticket, 1u) == (unsigned)a.ncl - 1) {
+        __threadfence();
+        float t = 0.f;
+        for (int c = 0; c < a.ncl; ++c) t += *(volatile float*)(a.lpart + c);
+        *a.loss = t / norm;
+        *a.ticket = 0u;
+      }
+    }
   }
   if (rank == 0) {
     // db_H = column sums of gH: 8 lanes per unit, each over a contiguous
@@ -480,7 +516,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     acc += __shfl_xor_sync(0xffffffffu, acc, 4);
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    if (o < h && part == 0) a.dbH[o] = acc;
+    if (o < h && part == 0) dbH_[o] = acc;
   }
   HPHASE(7);
 
@@ -491,7 +527,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   {
     const int nN = d.Kp >> 3;
     const int ga = (nN + 1) >> 1, na = (d.Hp >> 4) * ga;
-    const int gb = (nN + 3) >> 2, nb = a.dx ? (d.Bp >> 4) * gb : 0;
+    const int gb = (nN + 3) >> 2, nb = dx_ ? (d.Bp >> 4) * gb : 0;
     const int g = lane >> 2, t = lane & 3;
     for (int tile = warp; tile < na + nb; tile += nwarps) {
       if (tile < na) {
@@ -510,7 +546,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
           for (int j = 0; j < 2; ++j) {
             const int col = n0 + j * 8 + 2 * t;
             if (j >= nv || col >= nc) continue;
-            float* p = a.dWH + (size_t)o * in + k0 + col;
+            float* p = dWH_ + (size_t)o * in + k0 + col;
             if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
               *reinterpret_cast<float2*>(p) = make_float2(c[j][2 * hf], c[j][2 * hf + 1]);
             } else {
@@ -541,7 +577,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
               v0 *= actg(a.act_prev, xr[b * sK + col]);
               if (col + 1 < nc) v1 *= actg(a.act_prev, xr[b * sK + col + 1]);
             }
-            float* p = a.dx + (size_t)b * in + k0 + col;
+            float* p = dx_ + (size_t)b * in + k0 + col;
             if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
               *reinterpret_cast<float2*>(p) = make_float2(v0, v1);
             } else {
@@ -576,14 +612,21 @@ using HeadFn = void (*)(MlpArgs);
 // the specialised shape (CIFAR-3: B 128, 5*5*32 -> 64 -> 10) or the generic kernel
 static HeadFn head_fn(int B, int in, int h, int out) {
   if (B == 128 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<128, 800, 64, 10>;
+  if (B == 64 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<64, 800, 64, 10>;
   return mlp_head_kernel<0, 0, 0, 0>;
 }
 
 // cluster of kC CTAs with this kernel's shared memory schedulable? (cached per kernel)
 static bool cluster_ok(HeadFn fn, size_t smem) {
   struct Cache { HeadFn fn; size_t ok_upto, bad_from; };
-  static Cache cache[2] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0}};
-  Cache* c = cache[0].fn == fn || cache[0].fn == nullptr ? &cache[0] : &cache[1];
+  static Cache cache[3] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
+                           {nullptr, 0, ~(size_t)0}};
+  Cache* c = &cache[2];
+  for (Cache& e : cache)
+    if (e.fn == fn || e.fn == nullptr) {
+      c = &e;
+      break;
+    }
   c->fn = fn;
   if (smem <= c->ok_upto) return true;
   if (smem >= c->bad_from) return false;
@@ -619,20 +662,38 @@ bool mlp_head_fusable(int B, int in, int h, int out) {
   return smem <= 200 * 1024 && cluster_ok(head_fn(B, in, h, out), smem);
 }
 
+int mlp_head_slices(int B, int in, int h, int out) {
+  // two batch slices (two clusters, 32 SMs) when the batch splits evenly and
+  // each half still fills the 16 CTAs: every per-row phase halves
+  static const bool one = getenv("VCNN_TAIL_SLICES") && atoi(getenv("VCNN_TAIL_SLICES")) == 1;
+  if (!one && B >= 64 && B % 2 == 0 && mlp_head_fusable(B / 2, in, h, out)) return 2;
+  return 1;
+}
+
+size_t mlp_head_part_floats(int B, int in, int h, int out) {
+  const int ncl = mlp_head_slices(B, in, h, out);
+  return ncl > 1 ? (size_t)ncl * ((size_t)h * in + h + (size_t)out * h + out) : 0;
+}
+
 int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* WH,
                     const float* bH, int actH, const float* WO, const float* bO, int actO,
                     float* yH, float* yO, int loss_kind, const int* cls, const float* values,
                     float* loss, int* err, float* gH, float* gO, float* dWH, float* dbH,
-                    float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st) {
-  const size_t smem = mlp_head_smem(B, in, h, out);
-  const HeadFn fn = head_fn(B, in, h, out);
+                    float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st,
+                    int ncl, float* part, float* lpart, unsigned* ticket) {
+  if (ncl < 1 || B % ncl || (ncl > 1 && (!part || !lpart || !ticket)))
+    return fail(VCNN_ECONFIG, "mlp head: bad batch slicing");
+  const int Bc = B / ncl;
+  const size_t smem = mlp_head_smem(Bc, in, h, out);
+  const HeadFn fn = head_fn(Bc, in, h, out);
   if (!cluster_ok(fn, smem)) return fail(VCNN_ECUDA, "mlp head: cluster not schedulable");
   const bool vec = in % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) |
                                     reinterpret_cast<uintptr_t>(WH)) & 15) == 0;
-  MlpArgs a{B, in, h, out, x, WH, bH, actH, WO, bO, actO, yH, yO, loss_kind, cls, values,
-            loss, err, gH, gO, dWH, dbH, dWO, dbO, dx, act_prev, vec ? 1 : 0};
+  MlpArgs a{Bc, in, h, out, x, WH, bH, actH, WO, bO, actO, yH, yO, loss_kind, cls, values,
+            loss, err, gH, gO, dWH, dbH, dWO, dbO, dx, act_prev, vec ? 1 : 0,
+            B, ncl, part, lpart, ticket};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kC);
+  cfg.gridDim = dim3(kC * ncl);
   cfg.blockDim = dim3(kThreadsM);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;

@@ -82,13 +82,21 @@ int launch_head(int B, int in, int out, const float* x, const float* W, const fl
                 float* loss, float* gpre, float* dW, float* db, float* dx, int act_prev, int* err,
                 cudaStream_t st);
 // the two-layer tail fused (head.cu): small full layer H + last full layer O
-// fwd, loss fwd/bwd, both layers' dW / db and dX; one 16-CTA cluster
+// fwd, loss fwd/bwd, both layers' dW / db and dX; one 16-CTA cluster per
+// batch slice (mlp_head_slices): with ncl > 1 slices the layers' dW / db are
+// written per slice to part ([ncl][per], param order W_H | b_H | W_O | b_O,
+// mlp_head_part_floats) for the caller to sum in slice order; lpart [ncl]
+// and the zero-initialised ticket carry the loss partials
 bool mlp_head_fusable(int B, int in, int h, int out);
+int mlp_head_slices(int B, int in, int h, int out);
+size_t mlp_head_part_floats(int B, int in, int h, int out);
 int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* WH,
                     const float* bH, int actH, const float* WO, const float* bO, int actO,
                     float* yH, float* yO, int loss_kind, const int* cls, const float* values,
                     float* loss, int* err, float* gH, float* gO, float* dWH, float* dbH,
-                    float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st);
+                    float* dWO, float* dbO, float* dx, int act_prev, cudaStream_t st,
+                    int ncl = 1, float* part = nullptr, float* lpart = nullptr,
+                    unsigned* ticket = nullptr);
 int launch_accumulate(const float* values, const int64_t* source, const int64_t* target,
                       int64_t pairs, int64_t target_len, int reducer, float* out, int64_t* arg,
                       cudaStream_t st);
@@ -252,9 +260,13 @@ struct ImageSumFold {
 // trips it and the update (and every later one) is skipped
 // fold (nullable, fold->part set): params [fold_off, fold_off + per) take
 // their gradient from the per-image partials (written to g as well)
+// out[i] = the fixed-order sum over nimg partials part[k * stride + i], i < per
+int sum_partials(int nimg, int64_t per, int64_t stride, const float* part, float* out,
+                 cudaStream_t st);
 int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss = nullptr,
-             int* guard = nullptr, const ImageSumFold* fold = nullptr, int64_t fold_off = 0);
+             int* guard = nullptr, const ImageSumFold* fold = nullptr, int64_t fold_off = 0,
+             const ImageSumFold* fold2 = nullptr, int64_t fold2_off = 0);
 int dp_blocks(int64_t n);
 int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
                 const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st);

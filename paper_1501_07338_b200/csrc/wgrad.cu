@@ -640,6 +640,15 @@ int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, 
   return VCNN_OK;
 }
 
+int sum_partials(int nimg, int64_t per, int64_t stride, const float* part, float* out,
+                 cudaStream_t st) {
+  VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)cdiv(per, 32)),
+                           dim3(32 * kRedSlices), 0, st, nimg, per, stride, per, part, out,
+                           (float*)nullptr));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
 bool wgrad_small_ok(const ConvDesc& d, const GradSrc& gs) {
   SGeo g;
   return splan(d, gs, g);
