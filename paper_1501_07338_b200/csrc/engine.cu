@@ -160,8 +160,8 @@ struct vcnn_net {
   bool defer_fold = false;
   direct::ImageSumFold fold{};
   // the two-layer tail in batch slices (mlp_head_slices): per-slice dW / db
-  // partials [2][per] (folded into the update like layer 0's, or summed by a
-  // reduce launch), loss partials + ticket (tail_aux[0..3], [4])
+  // partials [kMaxSlices][per] (folded into the update like layer 0's, or
+  // summed by a reduce launch), loss partials + ticket (tail_aux[0..3], [4])
   float* tail_part = nullptr;
   float* tail_aux = nullptr;
   direct::ImageSumFold fold2{};
@@ -965,7 +965,7 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
       const LayerRt& hl = n->L[nl - 2];
       const LayerRt& ll = n->L[nl - 1];
       const size_t per = (size_t)(hl.w_len + hl.b_len + ll.w_len + ll.b_len);
-      s = s ? s : dalloc((void**)&n->tail_part, sizeof(float) * 2 * per);
+      s = s ? s : dalloc((void**)&n->tail_part, sizeof(float) * kMaxSlices * per);
       s = s ? s : dalloc((void**)&n->tail_aux, sizeof(float) * 8);
       if (!s && cudaMemset(n->tail_aux, 0, sizeof(float) * 8) != cudaSuccess)
         s = fail(VCNN_ECUDA, "net_create: tail buffers");

@@ -613,15 +613,18 @@ using HeadFn = void (*)(MlpArgs);
 static HeadFn head_fn(int B, int in, int h, int out) {
   if (B == 128 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<128, 800, 64, 10>;
   if (B == 64 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<64, 800, 64, 10>;
+  if (B == 32 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<32, 800, 64, 10>;
+  if (B == 16 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<16, 800, 64, 10>;
   return mlp_head_kernel<0, 0, 0, 0>;
 }
 
 // cluster of kC CTAs with this kernel's shared memory schedulable? (cached per kernel)
 static bool cluster_ok(HeadFn fn, size_t smem) {
   struct Cache { HeadFn fn; size_t ok_upto, bad_from; };
-  static Cache cache[3] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
-                           {nullptr, 0, ~(size_t)0}};
-  Cache* c = &cache[2];
+  static Cache cache[6] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
+                           {nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
+                           {nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0}};
+  Cache* c = &cache[5];
   for (Cache& e : cache)
     if (e.fn == fn || e.fn == nullptr) {
       c = &e;
@@ -663,10 +666,13 @@ bool mlp_head_fusable(int B, int in, int h, int out) {
 }
 
 int mlp_head_slices(int B, int in, int h, int out) {
-  // two batch slices (two clusters, 32 SMs) when the batch splits evenly and
-  // each half still fills the 16 CTAs: every per-row phase halves
-  static const bool one = getenv("VCNN_TAIL_SLICES") && atoi(getenv("VCNN_TAIL_SLICES")) == 1;
-  if (!one && B >= 64 && B % 2 == 0 && mlp_head_fusable(B / 2, in, h, out)) return 2;
+  // batch slices (one 16-CTA cluster each) while every slice keeps >= 16
+  // rows: each per-row phase shrinks with the slice.  CIFAR-3 b128 (graph
+  // replay): 1 slice 19.7 us / 1.22M img/s, 2: 15.5 us / 1.24M, 4: 13.6 us /
+  // 1.27M, 8 (16 rows, 128 SMs): 13.4 us / 1.30M
+  static const int want = getenv("VCNN_TAIL_SLICES") ? atoi(getenv("VCNN_TAIL_SLICES")) : 8;
+  for (int ncl = want < kMaxSlices ? want : kMaxSlices; ncl > 1; ncl /= 2)
+    if (B >= 16 * ncl && B % ncl == 0 && mlp_head_fusable(B / ncl, in, h, out)) return ncl;
   return 1;
 }
 

@@ -87,6 +87,7 @@ int launch_head(int B, int in, int out, const float* x, const float* W, const fl
 // written per slice to part ([ncl][per], param order W_H | b_H | W_O | b_O,
 // mlp_head_part_floats) for the caller to sum in slice order; lpart [ncl]
 // and the zero-initialised ticket carry the loss partials
+constexpr int kMaxSlices = 8;
 bool mlp_head_fusable(int B, int in, int h, int out);
 int mlp_head_slices(int B, int in, int h, int out);
 size_t mlp_head_part_floats(int B, int in, int h, int out);
