@@ -161,7 +161,8 @@ struct vcnn_net {
   direct::ImageSumFold fold{};
   // the two-layer tail in batch slices (mlp_head_slices): per-slice dW / db
   // partials [kMaxSlices][per] (folded into the update like layer 0's, or
-  // summed by a reduce launch), loss partials + ticket (tail_aux[0..3], [4])
+  // summed by a reduce launch), loss partials + ticket (tail_aux[0..kMaxSlices),
+  // [kMaxSlices])
   float* tail_part = nullptr;
   float* tail_aux = nullptr;
   direct::ImageSumFold fold2{};
@@ -401,7 +402,7 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
                         n->cls, n->values, n->loss, n->err, hl.gpre, last.gpre,
                         n->grads + hl.w_off, n->grads + hl.b_off, n->grads + last.w_off,
                         n->grads + last.b_off, prev ? prev->gpre : nullptr, act_prev, st, ncl,
-                        n->tail_part, n->tail_aux, reinterpret_cast<unsigned*>(n->tail_aux + 4)));
+                        n->tail_part, n->tail_aux, reinterpret_cast<unsigned*>(n->tail_aux + kMaxSlices)));
     if (ncl > 1) {  // the slices' dW / db: summed in slice order by the update, or here
       const int64_t per = (int64_t)hh * hin + hh + (int64_t)ho * hh + ho;
       if (n->defer_fold) {
@@ -966,8 +967,8 @@ int vcnn_net_create(const vcnn_net_spec* spec, int max_batch, int precision, vcn
       const LayerRt& ll = n->L[nl - 1];
       const size_t per = (size_t)(hl.w_len + hl.b_len + ll.w_len + ll.b_len);
       s = s ? s : dalloc((void**)&n->tail_part, sizeof(float) * kMaxSlices * per);
-      s = s ? s : dalloc((void**)&n->tail_aux, sizeof(float) * 8);
-      if (!s && cudaMemset(n->tail_aux, 0, sizeof(float) * 8) != cudaSuccess)
+      s = s ? s : dalloc((void**)&n->tail_aux, sizeof(float) * (kMaxSlices + 4));
+      if (!s && cudaMemset(n->tail_aux, 0, sizeof(float) * (kMaxSlices + 4)) != cudaSuccess)
         s = fail(VCNN_ECUDA, "net_create: tail buffers");
     }
   }

@@ -1,7 +1,7 @@
 """One pass over every kernel family for compute-sanitizer (memcheck /
 racecheck / synccheck): CIFAR-3 fused + trace + 3xTF32 + fp32 steps, the
 forward-only chain, denoise-style (K=1 kernels), deconv-121 (1-D segment
-direct conv), the small-Kd TMA-slab path (b256), a 2-replica DP group step
+direct conv), the tap-stacked forward + batch-sliced tail (b128 / b256), a 2-replica DP group step
 (barrier-free: the sanitizer serialises kernels) and the op-level ABI."""
 import sys
 
@@ -37,7 +37,8 @@ step(S.cifar3(), 16)
 step(S.cifar3(), 16, trace=True)
 step(S.cifar3(), 8, S.Precision.tf32x3)
 step(S.cifar3(), 8, S.Precision.fp32)
-step(S.cifar3(), 256, n=1)  # TMA slab path
+step(S.cifar3(), 256, n=1)  # large batch (tap-stacked forward, 8-slice tail)
+step(S.cifar3(), 128, n=1)  # the benchmark batch (8-slice tail, folded update)
 step(S.lenet_caffe(), 16)
 step(S.NetworkSpec((40, 40, 1), [S.ConvSpec(16, 16, 16, 1, A.relu), S.ConvSpec(16, 1, 1, 1, A.relu),
                                  S.ConvSpec(1, 8, 8, 1, A.identity)], S.LossKind.mse, 7), 2)

@@ -380,6 +380,31 @@ def test_full_size_step_vs_oracle(name, B):
     net.close()
 
 
+@pytest.mark.parametrize("B", [32, 64, 96, 128, 100])
+def test_tail_batch_slices_vs_oracle(B):
+    """The fused two-layer tail runs in 1 / 2 / 4 / 8 batch slices (one
+    cluster each) by batch size: the loss (summed over slices by the last
+    one) and every layer's output / dW / db / handed-down gradient match the
+    oracle; the update (slice partials folded into sgd_pack) equals the
+    unfused reference of the same step within TF32 tolerance."""
+    spec = S.cifar3()
+    x, cls, _ = O.synth_bench_data(spec, B, 8)
+    net = Network(spec, B, Precision.tf32)
+    net.set_trace(True)
+    _load(net, spec, x, cls, None)
+    net.forward_backward(B)
+    r = O.net_run_batch(spec, net.get_params().astype(np.float64), f32(x), cls=cls)
+    assert abs(net.loss() - r["loss"]) <= 1e-3 * r["loss"], (net.loss(), r["loss"])
+    teacher_forced(net, spec, x, B, TOL[Precision.tf32])
+    g_fb = net.get_grads()
+    p0 = net.get_params()
+    net.train_step(B, 0.01, 0.9)  # folded update: grads rewritten by sgd_pack
+    assert np.array_equal(net.get_grads(), g_fb)
+    want = (p0.astype(np.float64) - np.float64(np.float32(0.01)) * g_fb).astype(np.float32)
+    assert_close(net.get_params(), want, 1e-6, "folded update")
+    net.close()
+
+
 def test_big_batch_and_presets_run():
     """Every BASELINE config builds and steps at its benchmark size; losses are
     finite and training lowers the loss on a fixed batch."""
