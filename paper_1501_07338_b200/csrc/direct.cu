@@ -1223,11 +1223,24 @@ __device__ __forceinline__ void mma_tf32_m16n8k8(float (&c)[4], uint32_t a0, uin
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+#ifdef VCNN_PHASE_TIMING
+__device__ unsigned long long g_fphase[4][8];
+#define FPHASE(i)                                                              \
+  do {                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 4) g_fphase[blockIdx.x][i] = clock64(); \
+  } while (0)
+#else
+#define FPHASE(i) \
+  do {            \
+  } while (0)
+#endif
+
 // CTA (b, s) computes M tiles [s*kTilesPerCta, ...) of image b; warp w the
 // pair 2w, 2w+1 of them (two independent accumulator sets per K step)
 template <int KS, int ACT>
 __global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
   pdl_launch_dependents();
+  FPHASE(0);
   const FGeo& g = a.g;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((128u - (ptx::smem_u32(smem_raw) & 127u)) & 127u);
@@ -1251,6 +1264,7 @@ __global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
     for (int h = 0; h < 2; ++h) coff[ks][h] = g.jo[ks * 8 + t + 4 * h];
   __syncthreads();
   pdl_wait();
+  FPHASE(1);
   constexpr int wcols = KS * 8;
   const int wrows = g.nnt * 8;
   if (tid == 0) {
@@ -1278,8 +1292,10 @@ __global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
     }
   }
   ptx::mbar_wait(&load_bar, 0);
+  FPHASE(2);
   for (int i = tid; i < g.C * hw; i += FT) sx[i] = ptx::to_tf32(sx[i]);
   __syncthreads();
+  FPHASE(3);
 
   const int mbase = sidx * kTilesPerCta;
   float acc[kTilesPerWarp][4][4];
@@ -1337,6 +1353,7 @@ __global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
       }
     }
   }
+  FPHASE(4);
   // epilogue: c = {(gq, 2t), (gq, 2t+1), (gq+8, 2t), (gq+8, 2t+1)}
   float bb[4][2];
 #pragma unroll
@@ -1397,6 +1414,7 @@ __global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
   }
   if (g.pool) {  // the CTA's windows [w0, w0+nw) of every map: row segments
     __syncthreads();
+    FPHASE(5);
     constexpr int CW = kTilesPerCta * 4;
     const int w0 = mbase * 4;
     const int nw = PP - w0 < CW ? PP - w0 : CW;
@@ -1413,6 +1431,7 @@ __global__ void __launch_bounds__(FT, 4) conv_small_fwd_kernel(const FSArgs a) {
         a.pyn[((int64_t)b * PP + w0 + r) * g.K + n] = ptx::to_tf32(so[n * kSoStride + r]);
       }
   }
+  FPHASE(6);
 }
 
 template <int ACT>
@@ -1577,6 +1596,12 @@ int conv_dgrad(const ConvDesc& d, const GradSrc& gs, const float* pk, float* dx,
 }  // namespace vcnn_b200
 
 #ifdef VCNN_PHASE_TIMING
+extern "C" int vcnn_debug_fphases(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_fphase, sizeof(unsigned long long) * 32) ==
+                 cudaSuccess
+             ? 0
+             : 4;
+}
 extern "C" int vcnn_debug_dphases(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, vcnn_b200::direct::g_dphase, sizeof(unsigned long long) * 64) ==
                  cudaSuccess

@@ -61,3 +61,16 @@ try:
               "total", t[6] - t[0])
 except AttributeError:
     pass
+
+# the small-Kd forward of conv1 (direct.cu conv_small_fwd_kernel)
+try:
+    L.vcnn_debug_fphases.argtypes = [C.c_void_p]
+    fb = (C.c_ulonglong * 32)()
+    L.vcnn_debug_fphases(fb)
+    fn = ["setup+pdl", "load-wait", "round", "mma", "epilogue", "pool-store"]
+    for r in range(4):
+        t = [fb[r * 8 + i] for i in range(8)]
+        print(f"small_fwd cta {r} " + " ".join(f"{n}={t[i + 1] - t[i]}" for i, n in enumerate(fn)),
+              "total", t[6] - t[0])
+except AttributeError:
+    pass
