@@ -72,11 +72,15 @@ struct Geo {
                            // per output row, outputs per segment
   int ts, T, ngx, NM;      // tap-stacked tile (Cout <= 32): the MMA's M rows are T taps x 32
                            // maps of one kernel row (ngx groups per row), N = NM positions
+  int ns;                  // N-stacked 1-D segments: the MMA's N = T taps x Cout maps
   int eps, off_ep;         // epilogue staging: row stride (floats), offset (bytes)
+  int bsx;                 // stacked: bytes between the staged tap blocks (incl. the +1 shift)
 };
 
 // kernel "shifts" the MMA loop walks: taps, or tap groups in the stacked mode
-__host__ __device__ inline int nshift(const Geo& g) { return g.ts ? g.kh * g.ngx : g.kh * g.kw; }
+__host__ __device__ inline int nshift(const Geo& g) {
+  return g.ts || g.ns ? g.kh * g.ngx : g.kh * g.kw;
+}
 
 // the tap-stacked mode can be switched off (VCNN_TAPSTACK=0) for A/B runs
 inline bool tapstack_enabled() {
@@ -147,6 +151,7 @@ bool plan_ts(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, in
   g.nchunk = g.kh;
   g.wchunk = g.ngx * g.CG * g.BN * 32;
   g.eps = g.NM + 1;  // odd: conflict-free per-lane rows
+  g.bsx = 4 * (32 * g.eps + 1);
   const int ep_bytes = 4 * 32 * g.eps * 4;
   const int yp_floats = mode == 1 ? g.Cout * g.Hout * g.Wout : 0;
   const int yp_bytes = (yp_floats % 4 == 0 && 4 * yp_floats <= 48 * 1024) ? 4 * yp_floats : 0;
@@ -165,6 +170,60 @@ bool plan_ts(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, in
     g.off_a = g.off_win + win_bytes;
     g.off_ep = 0;  // over the ring, raw, windows and slab (all dead by then)
     g.off_yp = stage_yp ? off_yp : -1;
+    g.smem = total;
+    return (int64_t)g.B * g.tpi < (1 << 24);
+  }
+  return false;
+}
+
+// N-stacked 1-D row segments (deconv-121's 1x121 layer): the MMA's N rows
+// are T consecutive taps x Cout maps (the pack, T*Cout <= 256), M = the 128
+// positions of a row segment (the slab, viewed at the group's first tap).
+// Accumulator column block j at row p holds tap gi*T+j's products for output
+// p - j, so a segment yields 128 - (T-1) outputs and the epilogue reads
+// out[n][o] = sum_j S[j*Cout + n][o + j] in j order.  Per MMA: 4 KB of slab +
+// T*Cout*32 B of weights for T*Cout*128*8 MACs, vs T MMAs of N = Cout each
+// issued one at a time (the single-thread issue loop, ~50 cycles per MMA,
+// bounds the unstacked 1-D kernel)
+bool plan_ns(const ConvDesc& d, int mode, Geo& g) {
+  int T = 256 / g.Cout;
+  if (T > 8) T = 8;
+  if (T > g.kw) T = g.kw;
+  if (T < 2) return false;
+  g.ns = 1;
+  g.T = T;
+  g.ngx = (int)cdiv(g.kw, T);
+  const int NB = (int)cdiv(T * g.Cout, 16) * 16;
+  g.R = 1;
+  g.nseg = (int)cdiv(g.Wout, BM - (T - 1));
+  g.segw = (int)cdiv(g.Wout, g.nseg);
+  g.tpi = g.Hout * g.nseg;
+  g.CG = (int)cdiv(g.Cin, 8);
+  g.NP = (int)cdiv((g.ngx - 1) * T + BM, 8) * 8;
+  g.raw_n = g.Cin * g.Hin * g.Win;
+  const int a_bytes = g.CG * 2 * g.NP * 16;
+  g.BN = NB;
+  g.nblk = 1;
+  g.eps = EPS;
+  g.bsx = 4 * (g.Cout * EPS + 1);
+  const int shift_bytes = g.CG * NB * 32;  // one tap group
+  g.SC = (int)std::max<int64_t>(1, (40 * 1024) / shift_bytes);
+  if (g.SC > g.ngx) g.SC = g.ngx;
+  g.nchunk = (int)cdiv(g.ngx, g.SC);
+  g.wchunk = g.SC * shift_bytes;
+  const int ep_bytes = NB * EPS * 4;
+  for (int nbuf = g.nchunk >= 3 ? 3 : g.nchunk; nbuf >= 1; --nbuf) {
+    const int b_bytes = nbuf * g.wchunk;
+    const int body = b_bytes + a_bytes;
+    const int total = (body > ep_bytes ? body : ep_bytes) + 1024;
+    if ((size_t)total + 512 > kSmemOptin) continue;
+    g.nbuf = nbuf;
+    g.off_b = 0;
+    g.off_raw = b_bytes;
+    g.off_win = b_bytes;
+    g.off_a = b_bytes;
+    g.off_ep = 0;  // over the ring and the slab (dead by then)
+    g.off_yp = -1;
     g.smem = total;
     return (int64_t)g.B * g.tpi < (1 << 24);
   }
@@ -192,6 +251,12 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     // positions; the slab is the row segment plus the kw-1 halo, staged
     // straight from global memory
     if (d.kh != 1 || pool || tma || g.Wg > 4096) return false;
+    g.seg = 1;
+    if (tapstack_enabled() && g.Cout <= 128 && g.kw >= 8 && (mode == 1 || g.Cin >= 4) &&
+        plan_ns(d, mode, g))
+      return true;
+    g = Geo{g.mode, g.B, g.Cin, g.Hin, g.Win, g.Cout, g.kh, g.kw, g.Wg, g.Hout, g.Wout,
+            g.pad_y, g.pad_x};
     g.seg = 1;
   }
   // a forward view with < 4 input channels pads the MMA K (8 channels) by 2x
@@ -310,11 +375,13 @@ __global__ void pack_kernel(Geo g, int mode, const float* __restrict__ w, float*
     const int row = nb * g.BN + rg * 8 + r8;  // GEMM N index
     const int ch = cg * 8 + kh2 * 4 + k4;     // GEMM K index (input channel of the view)
     float v = 0.f;
-    // tap-stacked: pack row = j * 32 + map, shift = ky * ngx + gx, tap kx = gx * T + j
-    const int prow = g.ts ? (row & 31) : row;
-    const int ky = g.ts ? s / g.ngx : s / g.kw;
-    const int kx = g.ts ? (s - ky * g.ngx) * g.T + (row >> 5) : s - ky * g.kw;
-    if (prow < g.Cout && ch < g.Cin && kx < g.kw) {
+    // tap-stacked: pack row = j * 32 + map (ts) or j * Cout + map (ns),
+    // shift = ky * ngx + gx, tap kx = gx * T + j
+    const int jb = g.ts ? (row >> 5) : g.ns ? row / g.Cout : 0;
+    const int prow = g.ts ? (row & 31) : g.ns ? row - jb * g.Cout : row;
+    const int ky = g.ts || g.ns ? s / g.ngx : s / g.kw;
+    const int kx = g.ts || g.ns ? (s - ky * g.ngx) * g.T + jb : s - ky * g.kw;
+    if (prow < g.Cout && ch < g.Cin && kx < g.kw && jb < (g.ns ? g.T : 4)) {
       const int row = prow;
       const int n = mode == 0 ? row : ch, c = mode == 0 ? ch : row;
       const int wy = mode == 0 ? ky : g.kh - 1 - ky, wx = mode == 0 ? kx : g.kw - 1 - kx;
@@ -356,15 +423,23 @@ struct alignas(64) Args {
   BwdEpi be;
 };
 
-// one accumulator value at staging address e: plain, or (tap-stacked) the sum
-// of the four row blocks, block j shifted by j columns -- fixed order
+// one accumulator value at staging address e: plain, or (tap-stacked, ts /
+// ns) the sum of the T tap blocks, block j one column further -- fixed order
 template <bool TS>
-__device__ __forceinline__ float epv(uint32_t e, int eps) {
-  if (!TS) return ptx::lds_f32(e);
-  const uint32_t bs = 4u * (uint32_t)(32 * eps + 1);  // next block, next column
-  const float v0 = ptx::lds_f32(e), v1 = ptx::lds_f32(e + bs), v2 = ptx::lds_f32(e + 2 * bs),
-              v3 = ptx::lds_f32(e + 3 * bs);
-  return ((v0 + v1) + v2) + v3;
+__device__ __forceinline__ float epv(uint32_t e, const Geo& g) {
+  if constexpr (!TS) {
+    return ptx::lds_f32(e);
+  } else {
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      v[j] = j < g.T ? ptx::lds_f32(e + (uint32_t)j * (uint32_t)g.bsx) : 0.f;
+    float s = v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j)
+      if (j < g.T) s += v[j];
+    return s;
+  }
 }
 
 // Epilogues read the accumulator tile ep[n][128] (position m = r*Wg + x) from
@@ -389,7 +464,7 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
         const uint32_t ep = eb + 4u * (r * g.Wg + x - x0);
 #pragma unroll 4
         for (int n = 0; n < nmaps; ++n)
-          yp[n * ohw] = actf<ACT>(epv<TS>(ep + 4u * (n * g.eps), g.eps) + __ldg(e.bias + n0 + n));
+          yp[n * ohw] = actf<ACT>(epv<TS>(ep + 4u * (n * g.eps), g) + __ldg(e.bias + n0 + n));
       }
   }
   if (e.pool) {
@@ -411,11 +486,11 @@ __device__ void fwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
         {
           const int ry = wr * p, cx = wc * p;
           const int64_t o0 = plane0 * pplane + (int64_t)(r0 / p + wr) * e.POW + wc;
-          float best = actf<ACT>(epv<TS>(en + 4u * (ry * g.Wg + cx), g.eps) + bn_);
+          float best = actf<ACT>(epv<TS>(en + 4u * (ry * g.Wg + cx), g) + bn_);
           int by = 0, bx = 0;
           for (int u = 0; u < p; ++u)
             for (int v = 0; v < p; ++v) {
-              const float val = actf<ACT>(epv<TS>(en + 4u * ((ry + u) * g.Wg + cx + v), g.eps) + bn_);
+              const float val = actf<ACT>(epv<TS>(en + 4u * ((ry + u) * g.Wg + cx + v), g) + bn_);
               if (val > best) {
                 best = val;
                 by = u;
@@ -473,7 +548,7 @@ __device__ void bwd_epilogue(const Args& a, uint32_t eb, int b, int r0, int n0, 
       for (int u = 0; u < 16; ++u) {
         const int c = c0 + (NT / 32) * u;
         if (c >= nch) break;
-        float v = epv<TS>(ep + 4u * (c * g.eps), g.eps);
+        float v = epv<TS>(ep + 4u * (c * g.eps), g);
         if (yp) {
           if (ACT == VCNN_ACT_RELU) v *= yv[u] > 0.f ? 1.f : 0.f;
           else if (ACT == VCNN_ACT_SIGMOID) v *= yv[u] * (1.f - yv[u]);
@@ -559,6 +634,10 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     s_lo = lo > 0 ? lo : 0;
     s_hi = hi < g.kw - 1 ? hi : g.kw - 1;
     if (s_lo > s_hi) s_lo = s_hi = 0;  // (no tap: one zero MMA keeps the accumulator defined)
+    if (g.ns) {  // tap range -> tap-group range
+      s_lo /= g.T;
+      s_hi /= g.T;
+    }
   }
   const int c_lo = s_lo / g.SC, nloc = s_hi / g.SC - c_lo + 1;
   const int nring = nloc < g.nbuf ? nloc : g.nbuf;
@@ -723,7 +802,35 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       ptx::mma_commit(&wempty[buf]);
     }
     ptx::mma_commit(&done_bar);
-  } else if (!g.ts && warp == 0 && ptx::elect_one()) {
+  } else if (g.ns && warp == 0 && ptx::elect_one()) {
+    // N-stacked segments: A = the slab at the group's first tap gi*T, B = the
+    // pack block of group gi (T taps x Cout maps), one MMA per channel group
+    const uint32_t idesc = ptx::idesc_tf32(BM, g.BN);
+    const uint32_t half = (uint32_t)g.NP * 16u;
+    const uint64_t a0 = ptx::interleave_desc(s_a, half, 128u);
+    const uint64_t a_cg = (uint64_t)(2u * half >> 4), b_blk = (uint64_t)(g.BN * 32 >> 4);
+    uint32_t acc = 0;
+    for (int lc = 0; lc < nloc; ++lc) {
+      const int c = c_lo + lc, buf = lc % g.nbuf;
+      ptx::mbar_wait(&wfull[buf], (uint32_t)(lc / g.nbuf) & 1u);
+      ptx::tc_fence_after();
+      const int g0 = c * g.SC > s_lo ? c * g.SC : s_lo;
+      const int g1 = (c + 1) * g.SC - 1 < s_hi ? (c + 1) * g.SC - 1 : s_hi;
+      uint64_t bd = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u) +
+                    (uint64_t)(g0 - c * g.SC) * g.CG * b_blk;
+      for (int gi = g0; gi <= g1; ++gi) {
+        uint64_t ad = a0 + (uint64_t)(gi * g.T);
+        for (int cg = 0; cg < g.CG; ++cg) {
+          ptx::mma_tf32(tmem, ad, bd, idesc, acc);
+          acc = 1;
+          ad += a_cg;
+          bd += b_blk;
+        }
+      }
+      ptx::mma_commit(&wempty[buf]);
+    }
+    ptx::mma_commit(&done_bar);
+  } else if (!g.ts && !g.ns && warp == 0 && ptx::elect_one()) {
     const uint32_t idesc = ptx::idesc_tf32(BM, g.BN);  // both operands K-major
     const uint32_t half = (uint32_t)g.NP * 16u;          // LBO: the two 4-channel halves
     // descriptors advance by plain additions on the start-address field
@@ -808,7 +915,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       ptx::tmem_wait_ld();
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj)
-        ptx::sts_f32(s_raw + 4u * ((c + jj) * EPS + row), __uint_as_float(r[jj]));
+        ptx::sts_f32(s_ep + 4u * ((c + jj) * EPS + row), __uint_as_float(r[jj]));
     }
   }
   ptx::tc_fence_before();
@@ -819,12 +926,12 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
 #endif
   if (g.mode == 0)
     with_act(a.fe.act, [&](auto A) {
-      if (g.ts) fwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
+      if (g.ts || g.ns) fwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
       else fwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
     });
   else
     with_act(a.be.act_prev, [&](auto A) {
-      if (g.ts) bwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
+      if (g.ts || g.ns) bwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
       else bwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
     });
   DPHASE(5);
@@ -851,7 +958,8 @@ int launch(const Args& a, cudaStream_t st) {
   if (g.ts) return go(direct_conv_kernel<256>, cfg256);
   if (g.BN <= 32) return go(direct_conv_kernel<32>, cfg32);
   if (g.BN <= 64) return go(direct_conv_kernel<64>, cfg64);
-  return go(direct_conv_kernel<128>, cfg128);
+  if (g.BN <= 128) return go(direct_conv_kernel<128>, cfg128);
+  return go(direct_conv_kernel<256>, cfg256);
 }
 
 }  // namespace
@@ -899,9 +1007,9 @@ struct PackTable {
 
 // offset of (row = GEMM N index, ch = GEMM K index, s = ky*kw+kx) in a pack
 __device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int s) {
-  if (g.ts) {  // stacked: row (j = kx % T) * 32 + row, shift ky * ngx + kx / T
+  if (g.ts || g.ns) {  // stacked: row (j = kx % T) * (32 | Cout) + row, shift ky * ngx + kx / T
     const int ky = s / g.kw, kx = s - ky * g.kw;
-    row += (kx % g.T) * 32;
+    row += (kx % g.T) * (g.ts ? 32 : g.Cout);
     s = ky * g.ngx + kx / g.T;
   }
   const int nb = row / g.BN, r = row - nb * g.BN, cg = ch >> 3, kk = ch & 7;
