@@ -409,7 +409,7 @@ bool splan(const ConvDesc& d, const GradSrc& gs, SGeo& g) {
   g.off_g = 0;
   const int gbytes = 4 * g.mt * 16 * g.Qs;
   const int ntb = g.nt <= 4 ? 4 : g.nt <= 8 ? 8 : 12;  // the kernel's NT bucket
-  const int red_bytes = 4 * SKG * g.mt * 16 * ntb * 8;  // reuses G
+  const int red_bytes = 4 * SKG * g.mt * 16 * (ntb * 8 + 4);  // reuses G
   g.off_x = ((gbytes > red_bytes ? gbytes : red_bytes) + 127) & ~127;
   g.off_q = (g.off_x + 4 * g.xfl + 127) & ~127;
   g.off_win = (g.off_q + 4 * g.Q8 + 127) & ~127;
@@ -558,7 +558,10 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
   }
   __syncthreads();  // G is dead: the K groups' partial tiles go over it
   SPHASE(5);
-  const int tw = MT * 16 * NT * 8;  // floats per K-group tile [m][n]
+  // floats per K-group tile [m][n]; row stride NT*8 + 4 (a multiple of 32
+  // plus 4): the 8 accumulator rows of a fragment store hit distinct banks
+  constexpr int RS = NT * 8 + 4;
+  const int tw = MT * 16 * RS;
   float* red = sg + kg * tw;
 #pragma unroll
   for (int mi = 0; mi < MT; ++mi)
@@ -567,10 +570,10 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
       const int jt = nh * NTW + jl;
       if (jt >= NT) continue;
       const int m = mi * 16 + gq, n = jt * 8 + 2 * t;
-      red[m * NT * 8 + n] = acc[mi][jl][0];
-      red[m * NT * 8 + n + 1] = acc[mi][jl][1];
-      red[(m + 8) * NT * 8 + n] = acc[mi][jl][2];
-      red[(m + 8) * NT * 8 + n + 1] = acc[mi][jl][3];
+      red[m * RS + n] = acc[mi][jl][0];
+      red[m * RS + n + 1] = acc[mi][jl][1];
+      red[(m + 8) * RS + n] = acc[mi][jl][2];
+      red[(m + 8) * RS + n + 1] = acc[mi][jl][3];
     }
   __syncthreads();
   float* part = a.part + (int64_t)b * g.pstride;
@@ -579,7 +582,7 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
     const int m = i / cols, j = i - m * cols;
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < SKG; ++w) s += sg[w * tw + m * NT * 8 + j];
+    for (int w = 0; w < SKG; ++w) s += sg[w * tw + m * RS + j];
     part[j < g.Kd ? m * g.Kd + j : g.K * g.Kd + m] = s;
   }
   SPHASE(6);
