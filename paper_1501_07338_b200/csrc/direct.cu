@@ -1259,10 +1259,11 @@ namespace {
 constexpr int FT = 256;   // 8 warps
 constexpr int kTilesPerWarp = 2;
 constexpr int kTilesPerCta = (FT / 32) * kTilesPerWarp;
-// row stride (floats) of the CTA's pooled [map][window] stage: one pad word so
-// both the [map][window] (NCHW) and the [window][map] (NHWC) reads are
-// conflict-free
-constexpr int kSoStride = kTilesPerCta * 4 + 1;
+// row stride (floats) of the CTA's pooled [map][window] stage, = 4 (mod 32):
+// the epilogue's fragment stores (lanes: 8 maps x 4 windows) hit 32 distinct
+// banks (stride 65 made them 3-4-way conflicted), the [map][window] (NCHW)
+// reads stay conflict-free (the NHWC reads of the TMA path are 4-way)
+constexpr int kSoStride = kTilesPerCta * 4 + 4;
 struct FGeo {
   int B, C, H, W, K, kh, kw, OH, OW;
   int Kd, nks, nnt;   // columns, K steps (8), N tiles (8 maps)
