@@ -42,10 +42,11 @@ struct Dims {
 __host__ __device__ inline int up4(int v) { return (v + 3) & ~3; }
 __host__ __device__ inline int up8(int v) { return (v + 7) & ~7; }
 __host__ __device__ inline int up16(int v) { return (v + 15) & ~15; }
-// a row stride of v floats (v % 4 == 0) whose 16-byte units are odd: float4
-// accesses of 8 consecutive rows, and mma fragment loads (8 rows x 4 columns)
-// hit distinct banks
-__host__ __device__ inline int odd16(int v) { return (v >> 2) & 1 ? v : v + 4; }
+// a row stride of v floats (v % 4 == 0) rounded up to 8 (mod 32): the mma
+// fragment loads hit 32 distinct banks both row-major (bank g*s + t) and
+// transposed (bank g + t*s) -- the dW GEMM reads x and gH transposed; an odd
+// number of 16-byte units (the previous rule) left those 2-way conflicted
+__host__ __device__ inline int pad8of32(int v) { return v + ((8 - v % 32) + 32) % 32; }
 
 __host__ __device__ inline Dims dims_of(int B, int in, int h, int out) {
   Dims d;
@@ -53,8 +54,8 @@ __host__ __device__ inline Dims dims_of(int B, int in, int h, int out) {
   d.R = (B + kC - 1) / kC;
   d.Kc = up4((in + kC - 1) / kC);
   d.Bp = up16(B); d.Hp = up16(h); d.Kp = up8(d.Kc);
-  d.sK = odd16(d.Kp);
-  d.sH = odd16(d.Hp);
+  d.sK = pad8of32(d.Kp);
+  d.sH = pad8of32(d.Hp);
   d.per5 = (out * (h + 1) + kC - 1) / kC;
   int o = 0;
   d.oxr = o; o += d.Bp * d.sK;        // x[:, mine]   [Bp][sK]
