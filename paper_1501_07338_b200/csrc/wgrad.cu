@@ -409,7 +409,7 @@ bool splan(const ConvDesc& d, const GradSrc& gs, SGeo& g) {
   g.off_g = 0;
   const int gbytes = 4 * g.mt * 16 * g.Qs;
   const int ntb = g.nt <= 4 ? 4 : g.nt <= 8 ? 8 : 12;  // the kernel's NT bucket
-  const int red_bytes = 4 * SKG * g.mt * 16 * (ntb * 8 + 4);  // reuses G
+  const int red_bytes = 4 * SKG * g.mt * 16 * (ntb * 8 + 8);  // reuses G
   g.off_x = ((gbytes > red_bytes ? gbytes : red_bytes) + 127) & ~127;
   g.off_q = (g.off_x + 4 * g.xfl + 127) & ~127;
   g.off_win = (g.off_q + 4 * g.Q8 + 127) & ~127;
@@ -558,9 +558,10 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
   }
   __syncthreads();  // G is dead: the K groups' partial tiles go over it
   SPHASE(5);
-  // floats per K-group tile [m][n]; row stride NT*8 + 4 (a multiple of 32
-  // plus 4): the 8 accumulator rows of a fragment store hit distinct banks
-  constexpr int RS = NT * 8 + 4;
+  // floats per K-group tile [m][n]; row stride NT*8 + 8 (= 8 mod 32) and
+  // 8-byte stores of each fragment column pair: a warp's 32 pairs land in 32
+  // distinct 8-byte slots (two wavefronts, no replays)
+  constexpr int RS = NT * 8 + 8;
   const int tw = MT * 16 * RS;
   float* red = sg + kg * tw;
 #pragma unroll
@@ -570,10 +571,9 @@ __global__ void __launch_bounds__(ST, 1) wgrad_small_kernel(const SArgs a) {
       const int jt = nh * NTW + jl;
       if (jt >= NT) continue;
       const int m = mi * 16 + gq, n = jt * 8 + 2 * t;
-      red[m * RS + n] = acc[mi][jl][0];
-      red[m * RS + n + 1] = acc[mi][jl][1];
-      red[(m + 8) * RS + n] = acc[mi][jl][2];
-      red[(m + 8) * RS + n + 1] = acc[mi][jl][3];
+      *reinterpret_cast<float2*>(red + m * RS + n) = make_float2(acc[mi][jl][0], acc[mi][jl][1]);
+      *reinterpret_cast<float2*>(red + (m + 8) * RS + n) =
+          make_float2(acc[mi][jl][2], acc[mi][jl][3]);
     }
   __syncthreads();
   float* part = a.part + (int64_t)b * g.pstride;
