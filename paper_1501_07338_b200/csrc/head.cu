@@ -99,7 +99,7 @@ struct MlpArgs {
 __device__ unsigned long long g_hphase[kC][16];
 #define HPHASE(i)                                                   \
   do {                                                              \
-    if (threadIdx.x == 0) g_hphase[blockIdx.x % kC][i] = clock64(); \
+    if (threadIdx.x == 0 && blockIdx.x < kC) g_hphase[blockIdx.x][i] = clock64(); \
   } while (0)
 #else
 #define HPHASE(i) \
