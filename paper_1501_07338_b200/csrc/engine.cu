@@ -140,11 +140,14 @@ struct vcnn_net {
   // slots filled by a copy stream while the previous step computes
   struct Pipe {
     cudaStream_t cp = nullptr;
+    cudaStream_t rd = nullptr;  // loss read-back (its own stream: it waits for each step)
     cudaEvent_t start = nullptr, copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    cudaEvent_t stored = nullptr;  // a step's loss is in the device ring
     float* xs[2] = {nullptr, nullptr};
     int* cs[2] = {nullptr, nullptr};
     float* vs[2] = {nullptr, nullptr};
     float* hl = nullptr;  // pinned per-step losses (a pageable D2H would block the host)
+    float* dl = nullptr;  // device per-step losses (one store kernel per step, one D2H per call)
     int hl_cap = 0;
   } pipe;
   int g_batch = -1;
@@ -1052,8 +1055,11 @@ int vcnn_net_destroy(vcnn_net* n) {
     if (n->pipe.consumed[k]) cudaEventDestroy(n->pipe.consumed[k]);
   }
   if (n->pipe.start) cudaEventDestroy(n->pipe.start);
+  if (n->pipe.stored) cudaEventDestroy(n->pipe.stored);
   if (n->pipe.hl) cudaFreeHost(n->pipe.hl);
+  cudaFree(n->pipe.dl);
   if (n->pipe.cp) cudaStreamDestroy(n->pipe.cp);
+  if (n->pipe.rd) cudaStreamDestroy(n->pipe.rd);
   for (cudaEvent_t e : n->event_pool) cudaEventDestroy(e);
   delete n;
   return VCNN_OK;
@@ -1252,7 +1258,9 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
   auto& P = n->pipe;
   if (!P.cp) {
     VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.cp, cudaStreamNonBlocking));
+    VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.rd, cudaStreamNonBlocking));
     VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming));
+    VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.stored, cudaEventDisableTiming));
     for (int k = 0; k < 2; ++k) {
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.copied[k], cudaEventDisableTiming));
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.consumed[k], cudaEventDisableTiming));
@@ -1263,10 +1271,13 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
   }
   if (P.hl_cap < nsteps) {
     if (P.hl) cudaFreeHost(P.hl);
+    if (P.dl) cudaFree(P.dl);
     P.hl = nullptr;
+    P.dl = nullptr;
     P.hl_cap = 0;
     VCNN_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P.hl), sizeof(float) * nsteps,
                                 cudaHostAllocDefault));
+    VCNN_CUDA_TRY(cudaMalloc(&P.dl, sizeof(float) * nsteps));
     P.hl_cap = nsteps;
   }
   const size_t xb = sizeof(float) * n->in_per * batch;
@@ -1295,10 +1306,17 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
                                   cudaMemcpyDeviceToDevice, n->stream));
     VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
     TRY(train_step(n, batch, lr, mom));
-    VCNN_CUDA_TRY(cudaMemcpyAsync(P.hl + i, n->loss, sizeof(float), cudaMemcpyDeviceToHost,
-                                  n->stream));
+    // the step's loss: a store kernel into its own device slot (no copy-engine
+    // op between two graph launches on the compute stream), read back to the
+    // host by the copy stream once the step is done
+    TRY(launch_store_scalar(n->loss, P.dl + i, n->stream));
+    VCNN_CUDA_TRY(cudaEventRecord(P.stored, n->stream));
+    VCNN_CUDA_TRY(cudaStreamWaitEvent(P.rd, P.stored, 0));
+    VCNN_CUDA_TRY(cudaMemcpyAsync(P.hl + i, P.dl + i, sizeof(float), cudaMemcpyDeviceToHost,
+                                  P.rd));
   }
   VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  VCNN_CUDA_TRY(cudaStreamSynchronize(P.rd));
   if (losses) std::memcpy(losses, P.hl, sizeof(float) * nsteps);
   return VCNN_OK;
 }
