@@ -1174,15 +1174,13 @@ int vcnn_net_set_batch_device(vcnn_net* n, int batch, const float* x, const int*
                               const float* values) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
   TRY(check_batch(n, batch));
-  VCNN_CUDA_TRY(cudaMemcpyAsync(n->x, x, sizeof(float) * n->in_per * batch,
-                                cudaMemcpyDeviceToDevice, n->stream));
-  if (cls)
-    VCNN_CUDA_TRY(cudaMemcpyAsync(n->cls, cls, sizeof(int) * batch, cudaMemcpyDeviceToDevice,
-                                  n->stream));
-  if (values)
+  // one staging kernel for the images and the targets
+  if (cls && values)
     VCNN_CUDA_TRY(cudaMemcpyAsync(n->values, values, sizeof(float) * n->out_units * batch,
                                   cudaMemcpyDeviceToDevice, n->stream));
-  return VCNN_OK;
+  return launch_stage_batch(x, n->x, n->in_per * batch, cls ? (const void*)cls : values,
+                            cls ? (void*)n->cls : (void*)n->values,
+                            cls ? batch : n->out_units * batch, n->stream);
 }
 
 int vcnn_net_forward_backward(vcnn_net* n, int batch) {
@@ -1300,10 +1298,9 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
     VCNN_CUDA_TRY(cudaEventRecord(P.copied[k], P.cp));
     // compute stream: slot k -> the input slots, the step, the loss to host
     VCNN_CUDA_TRY(cudaStreamWaitEvent(n->stream, P.copied[k], 0));
-    VCNN_CUDA_TRY(cudaMemcpyAsync(n->x, P.xs[k], xb, cudaMemcpyDeviceToDevice, n->stream));
-    VCNN_CUDA_TRY(cudaMemcpyAsync(ce ? (void*)n->cls : (void*)n->values,
-                                  ce ? (void*)P.cs[k] : (void*)P.vs[k], tb,
-                                  cudaMemcpyDeviceToDevice, n->stream));
+    TRY(launch_stage_batch(P.xs[k], n->x, n->in_per * batch,
+                           ce ? (const void*)P.cs[k] : (const void*)P.vs[k],
+                           ce ? (void*)n->cls : (void*)n->values, (int64_t)(tb / 4), n->stream));
     VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
     TRY(train_step(n, batch, lr, mom));
     // the step's loss: a store kernel into its own device slot (no copy-engine

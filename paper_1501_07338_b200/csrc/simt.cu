@@ -1035,6 +1035,39 @@ __global__ void store_scalar_kernel(const float* __restrict__ src, float* __rest
   if (threadIdx.x == 0) *dst = *src;
 }
 
+// stage a device batch into the net's input slots: the images (float4 when
+// 16-byte aligned) and the targets (32-bit words) in ONE launch -- a kernel
+// between two graph launches pipelines; two copy-engine memcpys did not
+__global__ void stage_batch_kernel(const float* __restrict__ xs, float* __restrict__ xd, int64_t nx,
+                                   const uint32_t* __restrict__ ts, uint32_t* __restrict__ td,
+                                   int64_t nt, int vec) {
+  PDL_ENTRY();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    const float4* s4 = reinterpret_cast<const float4*>(xs);
+    float4* d4 = reinterpret_cast<float4*>(xd);
+    for (int64_t i = i0; i < nx / 4; i += stride) d4[i] = __ldg(s4 + i);
+    for (int64_t i = nx / 4 * 4 + i0; i < nx; i += stride) xd[i] = __ldg(xs + i);
+  } else {
+    for (int64_t i = i0; i < nx; i += stride) xd[i] = __ldg(xs + i);
+  }
+  for (int64_t i = i0; i < nt; i += stride) td[i] = __ldg(ts + i);
+}
+
+int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, void* td,
+                       int64_t nt_words, cudaStream_t st) {
+  const int vec = ((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(xd)) & 15) == 0;
+  int64_t blocks = cdiv(vec ? nx / 4 + 1 : nx, 256);
+  if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
+  if (blocks < 1) blocks = 1;
+  VCNN_CUDA_TRY(launch_pdl(stage_batch_kernel, dim3((unsigned)blocks), dim3(256), 0, st, xs, xd,
+                           nx, static_cast<const uint32_t*>(ts), static_cast<uint32_t*>(td),
+                           ts ? nt_words : (int64_t)0, vec));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
 int launch_store_scalar(const float* src, float* dst, cudaStream_t st) {
   VCNN_CUDA_TRY(launch_pdl(store_scalar_kernel, dim3(1), dim3(32), 0, st, src, dst));
   VCNN_LAUNCHED();
