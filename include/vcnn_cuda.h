@@ -281,6 +281,13 @@ int vcnn_net_input_buffers(vcnn_net* net, float** x, int** cls, float** values);
 /* stage a batch already in device memory (copied, stream-ordered) */
 int vcnn_net_set_batch_device(vcnn_net* net, int batch, const float* x, const int* cls,
                               const float* values);
+/* a ring of nbatch device batches (x [nbatch][x_stride floats], targets
+ * [nbatch][t_stride 32-bit words]: class ids or target values): every
+ * following train step first stages the ring's next batch (a kernel captured
+ * in the step's graph; a device cursor walks the ring) -- for dataset epochs
+ * and benchmarks whose batches are already resident.  nbatch = 0 detaches. */
+int vcnn_net_set_batch_ring(vcnn_net* net, int nbatch, int batch, const float* x,
+                            int64_t x_stride, const void* targets, int64_t t_stride);
 /* Executor::run_batch with targets (variants.hpp:353-376): forward, fused
  * loss, backward; grads land in the device grads buffer, loss in a device
  * scalar.  Stream-ordered, no host sync. */

@@ -130,6 +130,7 @@ struct vcnn_net {
     float lr, mom;
     const DpLink* dp;
     int dpv;
+    const void* ring;  // the batch ring the graph stages from (null: none)
     cudaGraphExec_t exec;
     int kernels;
   };
@@ -154,6 +155,7 @@ struct vcnn_net {
   float g_lr = 0, g_mom = 0;
   const DpLink* g_dp = nullptr;
   int g_dpv = 0;
+  const void* g_ring = nullptr;
   int kernels_per_step = 0;
   bool guard = false;  // Trainer non-finite stop armed (err[2..3] on the device)
   DpLink* dp = nullptr;  // attached data-parallel group (vcnn_dp_*), or none
@@ -168,6 +170,14 @@ struct vcnn_net {
   // [kMaxSlices])
   float* tail_part = nullptr;
   float* tail_aux = nullptr;
+  // device batch ring (vcnn_net_set_batch_ring): staged by the step itself
+  struct Ring {
+    const float* x = nullptr;
+    const void* t = nullptr;
+    int nbatch = 0, batch = 0;
+    int64_t xs = 0, ts = 0;
+    int* cursor = nullptr;  // [slot, blocks done]
+  } ring;
   direct::ImageSumFold fold2{};
   int64_t fold2_off = 0;
   // breakdown timer
@@ -632,6 +642,13 @@ int eager_step(vcnn_net* n, int batch, float lr, float mom) {
     ~PdlScope() { pdl_enabled() = saved; }
   } pdl_scope(n->breakdown);
   const int tail = tail_fused(n, batch);
+  if (n->ring.nbatch) {  // the ring's next batch into the input slots
+    const bool ce = n->spec.loss == VCNN_LOSS_SOFTMAX_CE;
+    TRY(launch_ring_stage(n->ring.x, n->x, n->in_per * batch, n->ring.xs, n->ring.t,
+                          ce ? (void*)n->cls : (void*)n->values,
+                          ce ? batch : n->out_units * batch, n->ring.ts, n->ring.nbatch,
+                          n->ring.cursor, n->stream));
+  }
   TRY(run_forward(n, batch, tail));
   n->defer_fold = !n->dp || n->dp->world == 1;
   n->fold = direct::ImageSumFold{};
@@ -649,12 +666,13 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
   TRY(check_cfg(lr, mom));
   if (!n->use_graph || n->breakdown) return eager_step(n, batch, lr, mom);
   const int dpv = n->dp ? n->dp->version : 0;
+  const void* ring = n->ring.nbatch ? (const void*)n->ring.x : nullptr;
   if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom ||
-      n->g_dp != n->dp || n->g_dpv != dpv) {
+      n->g_dp != n->dp || n->g_dpv != dpv || n->g_ring != ring) {
     n->gexec = nullptr;
     for (auto& e : n->graphs)
       if (e.batch == batch && e.lr == lr && e.mom == mom && e.dp == n->dp &&
-          e.dpv == (n->dp ? n->dp->version : 0)) {
+          e.dpv == (n->dp ? n->dp->version : 0) && e.ring == ring) {
         n->gexec = e.exec;
         n->kernels_per_step = e.kernels;
       }
@@ -665,6 +683,7 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     n->g_mom = mom;
     n->g_dp = n->dp;
     n->g_dpv = dpv;
+    n->g_ring = ring;
   } else {
     if (n->graphs.size() >= 4) drop_graph(n);
     if (!n->cap_stream)
@@ -688,12 +707,13 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
     n->graphs.push_back(
-        vcnn_net::GraphEntry{batch, lr, mom, n->dp, dpv, n->gexec, n->kernels_per_step});
+        vcnn_net::GraphEntry{batch, lr, mom, n->dp, dpv, ring, n->gexec, n->kernels_per_step});
     n->g_batch = batch;
     n->g_lr = lr;
     n->g_mom = mom;
     n->g_dp = n->dp;
     n->g_dpv = dpv;
+    n->g_ring = ring;
   }
   VCNN_CUDA_TRY(cudaGraphLaunch(n->gexec, n->stream));
   g_launches.fetch_add(n->kernels_per_step);
@@ -1042,6 +1062,7 @@ int vcnn_net_destroy(vcnn_net* n) {
   cudaFree(n->ws2.ptr);
   cudaFree(n->tail_part);
   cudaFree(n->tail_aux);
+  cudaFree(n->ring.cursor);
   for (cudaEvent_t e : n->fork_ev)
     if (e) cudaEventDestroy(e);
   if (n->join_ev) cudaEventDestroy(n->join_ev);
@@ -1183,6 +1204,31 @@ int vcnn_net_set_batch_device(vcnn_net* n, int batch, const float* x, const int*
                             cls ? batch : n->out_units * batch, n->stream);
 }
 
+int vcnn_net_set_batch_ring(vcnn_net* n, int nbatch, int batch, const float* x,
+                            int64_t x_stride, const void* targets, int64_t t_stride) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (nbatch <= 0) {
+    n->ring.x = nullptr;
+    n->ring.t = nullptr;
+    n->ring.nbatch = 0;
+    return VCNN_OK;
+  }
+  TRY(check_batch(n, batch));
+  const bool ce = n->spec.loss == VCNN_LOSS_SOFTMAX_CE;
+  if (!x || !targets || x_stride < n->in_per * batch ||
+      t_stride < (ce ? batch : n->out_units * batch))
+    return fail(VCNN_ESHAPE, "batch ring: buffers / strides");
+  if (!n->ring.cursor) VCNN_CUDA_TRY(cudaMalloc(&n->ring.cursor, 2 * sizeof(int)));
+  VCNN_CUDA_TRY(cudaMemsetAsync(n->ring.cursor, 0, 2 * sizeof(int), n->stream));
+  n->ring.x = x;
+  n->ring.t = targets;
+  n->ring.nbatch = nbatch;
+  n->ring.batch = batch;
+  n->ring.xs = x_stride;
+  n->ring.ts = t_stride;
+  return VCNN_OK;
+}
+
 int vcnn_net_forward_backward(vcnn_net* n, int batch) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
   TRY(check_batch(n, batch));
@@ -1253,6 +1299,12 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
           return fail(VCNN_EBOUNDS, "loss: class index " + std::to_string(c) +
                                         " out of range [0," + std::to_string(n->out_units) + ")");
       }
+  struct RingOff {  // this loop stages its own batches: the ring stays detached
+    vcnn_net* n;
+    int saved;
+    explicit RingOff(vcnn_net* m) : n(m), saved(m->ring.nbatch) { m->ring.nbatch = 0; }
+    ~RingOff() { n->ring.nbatch = saved; }
+  } ring_off(n);
   auto& P = n->pipe;
   if (!P.cp) {
     VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.cp, cudaStreamNonBlocking));
@@ -1328,6 +1380,12 @@ int vcnn_net_train_epoch(vcnn_net* n, const float* images, const int* cls, const
   TRY(check_cfg(lr, mom));
   const bool ce = n->spec.loss == VCNN_LOSS_SOFTMAX_CE;
   if (ce ? !cls : !values) return fail(VCNN_ESHAPE, "train_epoch: targets required");
+  struct RingOff {  // the epoch loop gathers its own batches
+    vcnn_net* n;
+    int saved;
+    explicit RingOff(vcnn_net* m) : n(m), saved(m->ring.nbatch) { m->ring.nbatch = 0; }
+    ~RingOff() { n->ring.nbatch = saved; }
+  } ring_off(n);
   // arm the non-finite guard (err[2] armed, err[3] tripped) for this epoch
   TRY(write_guard(n, 1));
   int bi = 0;

@@ -76,6 +76,9 @@ int launch_gather_rows(int n, int64_t per, const float* src, const int* order, i
 int launch_store_scalar(const float* src, float* dst, cudaStream_t st);
 int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, void* td,
                        int64_t nt_words, cudaStream_t st);
+int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, const void* ts,
+                      void* td, int64_t nt, int64_t tstride, int nbatch, int* cursor,
+                      cudaStream_t st);
 // the network head fused: last full layer fwd + loss fwd/bwd + its
 // dW / db / dX (dX * act_prev'(x)); one cluster, fp32
 bool head_fusable(int B, int in, int out);

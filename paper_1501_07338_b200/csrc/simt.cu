@@ -1068,6 +1068,51 @@ int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, v
   return VCNN_OK;
 }
 
+// the ring variant: the batch index comes from a device cursor, advanced by
+// the last block to finish (a graph replays the same launch every step)
+__global__ void ring_stage_kernel(const float* __restrict__ xs, float* __restrict__ xd, int64_t nx,
+                                  int64_t xstride, const uint32_t* __restrict__ ts,
+                                  uint32_t* __restrict__ td, int64_t nt, int64_t tstride,
+                                  int nbatch, int* cursor) {
+  PDL_ENTRY();
+  __shared__ int slot;
+  if (threadIdx.x == 0) slot = *((volatile int*)cursor);
+  __syncthreads();
+  const float* xsrc = xs + (int64_t)slot * xstride;
+  const uint32_t* tsrc = ts + (int64_t)slot * tstride;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const float4* s4 = reinterpret_cast<const float4*>(xsrc);
+  float4* d4 = reinterpret_cast<float4*>(xd);
+  for (int64_t i = i0; i < nx / 4; i += stride) d4[i] = __ldg(s4 + i);
+  for (int64_t i = nx / 4 * 4 + i0; i < nx; i += stride) xd[i] = __ldg(xsrc + i);
+  for (int64_t i = i0; i < nt; i += stride) td[i] = __ldg(tsrc + i);
+  // every block has read the cursor; the last one advances it
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(cursor + 1, 1) == (int)gridDim.x - 1) {
+      cursor[1] = 0;
+      cursor[0] = slot + 1 == nbatch ? 0 : slot + 1;
+    }
+  }
+}
+
+int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, const void* ts,
+                      void* td, int64_t nt, int64_t tstride, int nbatch, int* cursor,
+                      cudaStream_t st) {
+  if (((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(xd)) & 15) ||
+      xstride % 4)
+    return fail(VCNN_ESHAPE, "batch ring: x must be 16-byte aligned, x_stride a multiple of 4");
+  int64_t blocks = cdiv(nx / 4 + 1, 256);
+  if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
+  VCNN_CUDA_TRY(launch_pdl(ring_stage_kernel, dim3((unsigned)blocks), dim3(256), 0, st, xs, xd,
+                           nx, xstride, static_cast<const uint32_t*>(ts),
+                           static_cast<uint32_t*>(td), nt, tstride, nbatch, cursor));
+  VCNN_LAUNCHED();
+  return VCNN_OK;
+}
+
 int launch_store_scalar(const float* src, float* dst, cudaStream_t st) {
   VCNN_CUDA_TRY(launch_pdl(store_scalar_kernel, dim3(1), dim3(32), 0, st, src, dst));
   VCNN_LAUNCHED();

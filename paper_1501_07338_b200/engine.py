@@ -195,6 +195,24 @@ class Network:
                                               None if v is None else C.c_void_p(v.data_ptr())))
         return B
 
+    def set_batch_ring(self, x_pool=None, t_pool=None):
+        """Device batch ring (vcnn_net_set_batch_ring): x_pool [nbatch, B, in]
+        and t_pool [nbatch, B] class ids (int32) or [nbatch, B, units] targets,
+        resident on the device; every following train step stages the ring's
+        next batch itself (inside its graph).  No arguments detach the ring."""
+        if x_pool is None:
+            self._ring = None
+            check(lib().vcnn_net_set_batch_ring(self._h, 0, 0, None, 0, None, 0))
+            return
+        x = x_pool.contiguous().float()
+        t = t_pool.contiguous()
+        t = t.to(torch.int32) if not t.is_floating_point() else t.float()
+        nb, B = x.shape[0], x.shape[1]
+        self._ring = (x, t)  # keep the buffers alive while attached
+        check(lib().vcnn_net_set_batch_ring(self._h, int(nb), int(B), C.c_void_p(x.data_ptr()),
+                                            int(x[0].numel()), C.c_void_p(t.data_ptr()),
+                                            int(t[0].numel())))
+
     # ---- execution (stream-ordered) ----
     def forward_backward(self, batch):
         check(lib().vcnn_net_forward_backward(self._h, int(batch)))
