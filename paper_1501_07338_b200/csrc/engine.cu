@@ -1068,10 +1068,10 @@ int vcnn_net_destroy(vcnn_net* n) {
   if (n->join_ev) cudaEventDestroy(n->join_ev);
   if (n->side) cudaStreamDestroy(n->side);
   if (n->cap_stream) cudaStreamDestroy(n->cap_stream);
+  cudaFree(n->pipe.xs[0]);  // (slot 1 lies inside slot 0's allocation)
+  cudaFree(n->pipe.cs[0]);
+  cudaFree(n->pipe.vs[0]);
   for (int k = 0; k < 2; ++k) {
-    cudaFree(n->pipe.xs[k]);
-    cudaFree(n->pipe.cs[k]);
-    cudaFree(n->pipe.vs[k]);
     if (n->pipe.copied[k]) cudaEventDestroy(n->pipe.copied[k]);
     if (n->pipe.consumed[k]) cudaEventDestroy(n->pipe.consumed[k]);
   }
@@ -1299,25 +1299,40 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
           return fail(VCNN_EBOUNDS, "loss: class index " + std::to_string(c) +
                                         " out of range [0," + std::to_string(n->out_units) + ")");
       }
-  struct RingOff {  // this loop stages its own batches: the ring stays detached
+  // the caller's batch ring is swapped for the two staging slots (restored on exit)
+  struct RingSwap {
     vcnn_net* n;
-    int saved;
-    explicit RingOff(vcnn_net* m) : n(m), saved(m->ring.nbatch) { m->ring.nbatch = 0; }
-    ~RingOff() { n->ring.nbatch = saved; }
-  } ring_off(n);
+    vcnn_net::Ring saved;
+    explicit RingSwap(vcnn_net* m) : n(m), saved(m->ring) {}
+    ~RingSwap() {
+      int* c = n->ring.cursor;
+      n->ring = saved;
+      n->ring.cursor = c;
+    }
+  } ring_swap(n);
   auto& P = n->pipe;
   if (!P.cp) {
     VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.cp, cudaStreamNonBlocking));
     VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.rd, cudaStreamNonBlocking));
     VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming));
     VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.stored, cudaEventDisableTiming));
+    // the two slots are contiguous: they form the staging ring
+    VCNN_CUDA_TRY(cudaMalloc(&P.xs[0], 2 * sizeof(float) * n->in_per * n->max_batch));
+    VCNN_CUDA_TRY(cudaMalloc(&P.cs[0], 2 * sizeof(int) * n->max_batch));
+    VCNN_CUDA_TRY(cudaMalloc(&P.vs[0], 2 * sizeof(float) * n->out_units * n->max_batch));
+    P.xs[1] = P.xs[0] + n->in_per * n->max_batch;
+    P.cs[1] = P.cs[0] + n->max_batch;
+    P.vs[1] = P.vs[0] + n->out_units * n->max_batch;
     for (int k = 0; k < 2; ++k) {
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.copied[k], cudaEventDisableTiming));
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.consumed[k], cudaEventDisableTiming));
-      VCNN_CUDA_TRY(cudaMalloc(&P.xs[k], sizeof(float) * n->in_per * n->max_batch));
-      VCNN_CUDA_TRY(cudaMalloc(&P.cs[k], sizeof(int) * n->max_batch));
-      VCNN_CUDA_TRY(cudaMalloc(&P.vs[k], sizeof(float) * n->out_units * n->max_batch));
     }
+  }
+  {
+    const float* x0 = P.xs[0];
+    const void* t0 = ce ? (const void*)P.cs[0] : (const void*)P.vs[0];
+    TRY(vcnn_net_set_batch_ring(n, 2, batch, x0, n->in_per * n->max_batch, t0,
+                                ce ? n->max_batch : n->out_units * n->max_batch));
   }
   if (P.hl_cap < nsteps) {
     if (P.hl) cudaFreeHost(P.hl);
@@ -1350,11 +1365,9 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
     VCNN_CUDA_TRY(cudaEventRecord(P.copied[k], P.cp));
     // compute stream: slot k -> the input slots, the step, the loss to host
     VCNN_CUDA_TRY(cudaStreamWaitEvent(n->stream, P.copied[k], 0));
-    TRY(launch_stage_batch(P.xs[k], n->x, n->in_per * batch,
-                           ce ? (const void*)P.cs[k] : (const void*)P.vs[k],
-                           ce ? (void*)n->cls : (void*)n->values, (int64_t)(tb / 4), n->stream));
-    VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
+    // the step's graph stages slot k (the ring's cursor walks 0, 1, 0, ...)
     TRY(train_step(n, batch, lr, mom));
+    VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
     // the step's loss: a store kernel into its own device slot (no copy-engine
     // op between two graph launches on the compute stream), read back to the
     // host by the copy stream once the step is done

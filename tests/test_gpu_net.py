@@ -522,6 +522,39 @@ def test_large_mse_loss_multi_cta(prec):
     assert_close(g0, r["grads"], TOL[prec], "grads")
 
 
+def test_batch_ring_equals_explicit_staging():
+    """vcnn_net_set_batch_ring: graph-replayed steps that stage the ring's
+    next batch themselves (device cursor, wrapping) train bit-identically to
+    explicit load_batch + step over the same batches; a host-stream call in
+    between keeps the ring (and its position) for the steps after it."""
+    spec, B, nb, steps = S.cifar3(), 32, 3, 7
+    x, cls, _ = O.synth_bench_data(spec, B * nb, 8)
+    xp = torch.from_numpy(x.reshape(nb, B, -1)).cuda()
+    cp = torch.from_numpy(cls.reshape(nb, B).astype(np.int32)).cuda()
+    a, b = Network(spec, B), Network(spec, B)
+    a.enable_graph(True)
+    b.enable_graph(True)
+    a.set_batch_ring(xp, cp)
+    for i in range(steps):
+        a.train_step(B, 0.01, 0.9)
+        b.load_batch(xp[i % nb], cls=cp[i % nb])
+        b.train_step(B, 0.01, 0.9)
+        assert a.loss() == b.loss(), i
+    assert np.array_equal(a.get_params(), b.get_params())
+    xs = torch.from_numpy(x.reshape(nb, B, -1)).pin_memory()
+    cs = torch.from_numpy(cls.reshape(nb, B).astype(np.int32)).pin_memory()
+    la = a.train_host_stream(xs, cls=cs, lr=0.01, momentum=0.9)
+    lb = b.train_host_stream(xs, cls=cs, lr=0.01, momentum=0.9)
+    assert np.array_equal(la, lb)
+    a.train_step(B, 0.01, 0.9)  # ring resumes at batch steps % nb
+    b.load_batch(xp[steps % nb], cls=cp[steps % nb])
+    b.train_step(B, 0.01, 0.9)
+    assert np.array_equal(a.get_params(), b.get_params())
+    a.set_batch_ring()
+    a.close()
+    b.close()
+
+
 def test_host_stream_equals_host_steps():
     """vcnn_net_train_host_stream (H2D of batch i+1 on a copy stream while
     step i computes) gives bit-identical losses and weights to the same
