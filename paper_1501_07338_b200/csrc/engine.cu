@@ -139,14 +139,15 @@ struct vcnn_net {
   cudaStream_t cap_stream = nullptr;  // capture needs a non-legacy stream
   // host-stream training (vcnn_net_train_host_stream): two device staging
   // slots filled by a copy stream while the previous step computes
+  static constexpr int kSlots = 3;  // host-stream staging slots (H2D gets two step times)
   struct Pipe {
     cudaStream_t cp = nullptr;
     cudaStream_t rd = nullptr;  // loss read-back (its own stream: it waits for each step)
-    cudaEvent_t start = nullptr, copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    cudaEvent_t start = nullptr, copied[kSlots] = {}, consumed[kSlots] = {};
     cudaEvent_t stored = nullptr;  // a step's loss is in the device ring
-    float* xs[2] = {nullptr, nullptr};
-    int* cs[2] = {nullptr, nullptr};
-    float* vs[2] = {nullptr, nullptr};
+    float* xs[kSlots] = {};
+    int* cs[kSlots] = {};
+    float* vs[kSlots] = {};
     float* hl = nullptr;  // pinned per-step losses (a pageable D2H would block the host)
     float* dl = nullptr;  // device per-step losses (one store kernel per step, one D2H per call)
     int hl_cap = 0;
@@ -1071,7 +1072,7 @@ int vcnn_net_destroy(vcnn_net* n) {
   cudaFree(n->pipe.xs[0]);  // (slot 1 lies inside slot 0's allocation)
   cudaFree(n->pipe.cs[0]);
   cudaFree(n->pipe.vs[0]);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < vcnn_net::kSlots; ++k) {
     if (n->pipe.copied[k]) cudaEventDestroy(n->pipe.copied[k]);
     if (n->pipe.consumed[k]) cudaEventDestroy(n->pipe.consumed[k]);
   }
@@ -1316,14 +1317,17 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
     VCNN_CUDA_TRY(cudaStreamCreateWithFlags(&P.rd, cudaStreamNonBlocking));
     VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.start, cudaEventDisableTiming));
     VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.stored, cudaEventDisableTiming));
-    // the two slots are contiguous: they form the staging ring
-    VCNN_CUDA_TRY(cudaMalloc(&P.xs[0], 2 * sizeof(float) * n->in_per * n->max_batch));
-    VCNN_CUDA_TRY(cudaMalloc(&P.cs[0], 2 * sizeof(int) * n->max_batch));
-    VCNN_CUDA_TRY(cudaMalloc(&P.vs[0], 2 * sizeof(float) * n->out_units * n->max_batch));
-    P.xs[1] = P.xs[0] + n->in_per * n->max_batch;
-    P.cs[1] = P.cs[0] + n->max_batch;
-    P.vs[1] = P.vs[0] + n->out_units * n->max_batch;
-    for (int k = 0; k < 2; ++k) {
+    // the slots are contiguous: they form the staging ring
+    constexpr int K = vcnn_net::kSlots;
+    VCNN_CUDA_TRY(cudaMalloc(&P.xs[0], K * sizeof(float) * n->in_per * n->max_batch));
+    VCNN_CUDA_TRY(cudaMalloc(&P.cs[0], K * sizeof(int) * n->max_batch));
+    VCNN_CUDA_TRY(cudaMalloc(&P.vs[0], K * sizeof(float) * n->out_units * n->max_batch));
+    for (int k = 1; k < K; ++k) {
+      P.xs[k] = P.xs[0] + k * n->in_per * n->max_batch;
+      P.cs[k] = P.cs[0] + k * n->max_batch;
+      P.vs[k] = P.vs[0] + k * n->out_units * n->max_batch;
+    }
+    for (int k = 0; k < K; ++k) {
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.copied[k], cudaEventDisableTiming));
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.consumed[k], cudaEventDisableTiming));
     }
@@ -1331,7 +1335,7 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
   {
     const float* x0 = P.xs[0];
     const void* t0 = ce ? (const void*)P.cs[0] : (const void*)P.vs[0];
-    TRY(vcnn_net_set_batch_ring(n, 2, batch, x0, n->in_per * n->max_batch, t0,
+    TRY(vcnn_net_set_batch_ring(n, vcnn_net::kSlots, batch, x0, n->in_per * n->max_batch, t0,
                                 ce ? n->max_batch : n->out_units * n->max_batch));
   }
   if (P.hl_cap < nsteps) {
@@ -1351,9 +1355,9 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
   VCNN_CUDA_TRY(cudaEventRecord(P.start, n->stream));
   VCNN_CUDA_TRY(cudaStreamWaitEvent(P.cp, P.start, 0));
   for (int i = 0; i < nsteps; ++i) {
-    const int k = i & 1;
-    // copy stream: batch i into slot k once step i-2 has taken it over
-    if (i >= 2) VCNN_CUDA_TRY(cudaStreamWaitEvent(P.cp, P.consumed[k], 0));
+    const int k = i % vcnn_net::kSlots;
+    // copy stream: batch i into slot k once step i-kSlots has finished with it
+    if (i >= vcnn_net::kSlots) VCNN_CUDA_TRY(cudaStreamWaitEvent(P.cp, P.consumed[k], 0));
     VCNN_CUDA_TRY(cudaMemcpyAsync(P.xs[k], x + (int64_t)i * x_stride, xb,
                                   cudaMemcpyHostToDevice, P.cp));
     if (ce)
@@ -1365,7 +1369,7 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
     VCNN_CUDA_TRY(cudaEventRecord(P.copied[k], P.cp));
     // compute stream: slot k -> the input slots, the step, the loss to host
     VCNN_CUDA_TRY(cudaStreamWaitEvent(n->stream, P.copied[k], 0));
-    // the step's graph stages slot k (the ring's cursor walks 0, 1, 0, ...)
+    // the step's graph stages slot k (the ring cursor walks 0, 1, 2, 0, ...)
     TRY(train_step(n, batch, lr, mom));
     VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
     // the step's loss: a store kernel into its own device slot (no copy-engine
