@@ -73,6 +73,7 @@ struct Geo {
   int ts, T, ngx, NM;      // tap-stacked tile (Cout <= 32): the MMA's M rows are T taps x 32
                            // maps of one kernel row (ngx groups per row), N = NM positions
   int ns;                  // N-stacked 1-D segments: the MMA's N = T taps x Cout maps
+  int gbuild;              // 2-D tile slab built straight from global (image too big to stage)
   int eps, off_ep;         // epilogue staging: row stride (floats), offset (bytes)
   int bsx;                 // stacked: bytes between the staged tap blocks (incl. the +1 shift)
 };
@@ -302,15 +303,23 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     if (g.rows > 256) return false;
     g.NP = g.rows * g.Wg;
   }
-  // the input image and the window arrays go in with single bulk copies
-  if (!g.seg && (g.Cin * g.Hin * g.Win) % 4 != 0) return false;
-  if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
   g.raw_n = g.Cin * g.Hin * g.Win;
+  // an image too big to stage whole (e.g. denoise-16's 64 x 49 x 49 maps):
+  // each tile builds its slab straight from global memory (not for a routed
+  // data gradient, which scatters into the staged image)
+  if (!g.tma && !g.seg && 4 * g.raw_n > 96 * 1024) {
+    if (mode == 1 && pool) return false;
+    g.gbuild = 1;
+  }
+  // the input image and the window arrays go in with single bulk copies
+  if (!g.seg && !g.gbuild && (g.Cin * g.Hin * g.Win) % 4 != 0) return false;
+  if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
   // dgrad always reserves window scratch for a >= 2x2 pool, so the routed
   // and unrouted plans (and the weight pack) share one BN
-  if (mode == 1 && !g.seg) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
-  const int a_bytes = g.CG * 2 * g.NP * 16 + (g.tma || g.seg ? 0 : 4 * g.NP);  // slab + table
-  const int raw_bytes = g.tma || g.seg ? 0 : 4 * g.raw_n;
+  if (mode == 1 && !g.seg && !g.gbuild) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
+  const bool staged = !(g.tma || g.seg || g.gbuild);
+  const int a_bytes = g.CG * 2 * g.NP * 16 + (staged ? 4 * g.NP : 0);  // slab + table
+  const int raw_bytes = staged ? 4 * g.raw_n : 0;
   const int win_bytes = 2 * 4 * g.win_n;
   if (raw_bytes > 96 * 1024) return false;
   // dgrad: stage the whole image's yprev (C x H x W) with one bulk copy so
@@ -667,8 +676,8 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       const uint32_t ab = 16u * (uint32_t)(2 * g.CG * g.NP);
       ptx::mbar_expect_tx(&load_bar, ab);
       tma_load_5d(s_a, &a.tmap, 0, -g.pad_x, r0 - g.pad_y, 0, b, &load_bar);
-    } else if (g.seg) {
-      // (the row segment is staged by all threads below)
+    } else if (g.seg || g.gbuild) {
+      // (the row segment / tile is built from global by all threads below)
     } else if (!routed) {
       const uint32_t rb = 4u * (uint32_t)(g.Cin * g.Hin * g.Win);
       ptx::mbar_expect_tx(&load_bar, rb);
@@ -719,6 +728,26 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       for (int u = 0; u < 4; ++u) {
         const int c = cq * 4 + u;
         v[u] = (ok && c < g.Cin) ? ptx::to_tf32(__ldg(src + c * plane + xx)) : 0.f;
+      }
+      ptx::sts_f32x4(s_a + 16u * (uint32_t)j, make_float4(v[0], v[1], v[2], v[3]));
+    }
+  } else if (g.gbuild) {
+    // slab position P = (row r0 + P / Wg - pad_y, column P % Wg - pad_x) of
+    // the image in global memory; thread -> (channel quad, P), 4 coalesced
+    // loads, one 16-byte store
+    const int64_t plane = (int64_t)g.Hin * g.Win;
+    const float* src = a.in + (int64_t)b * g.Cin * plane;
+    for (int j = tid; j < 2 * g.CG * g.NP; j += NT) {
+      const int cq = j / g.NP, P = j - cq * g.NP;
+      const int pr = P / g.Wg;
+      const int yy = r0 + pr - g.pad_y, xx = P - pr * g.Wg - g.pad_x;
+      const bool ok = yy >= 0 && yy < g.Hin && xx >= 0 && xx < g.Win;
+      const int64_t off = (int64_t)yy * g.Win + xx;
+      float v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = cq * 4 + u;
+        v[u] = (ok && c < g.Cin) ? ptx::to_tf32(__ldg(src + c * plane + off)) : 0.f;
       }
       ptx::sts_f32x4(s_a + 16u * (uint32_t)j, make_float4(v[0], v[1], v[2], v[3]));
     }

@@ -150,6 +150,7 @@ struct vcnn_net {
     float* vs[kSlots] = {};
     float* hl = nullptr;  // pinned per-step losses (a pageable D2H would block the host)
     float* dl = nullptr;  // device per-step losses (one store kernel per step, one D2H per call)
+    int* cur = nullptr;   // the staging ring's own cursor (the caller's ring keeps its place)
     int hl_cap = 0;
   } pipe;
   int g_batch = -1;
@@ -1080,6 +1081,7 @@ int vcnn_net_destroy(vcnn_net* n) {
   if (n->pipe.stored) cudaEventDestroy(n->pipe.stored);
   if (n->pipe.hl) cudaFreeHost(n->pipe.hl);
   cudaFree(n->pipe.dl);
+  cudaFree(n->pipe.cur);
   if (n->pipe.cp) cudaStreamDestroy(n->pipe.cp);
   if (n->pipe.rd) cudaStreamDestroy(n->pipe.rd);
   for (cudaEvent_t e : n->event_pool) cudaEventDestroy(e);
@@ -1300,16 +1302,13 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
           return fail(VCNN_EBOUNDS, "loss: class index " + std::to_string(c) +
                                         " out of range [0," + std::to_string(n->out_units) + ")");
       }
-  // the caller's batch ring is swapped for the two staging slots (restored on exit)
+  // the caller's batch ring (and its cursor) is swapped for the staging slots
+  // with their own cursor, restored on exit
   struct RingSwap {
     vcnn_net* n;
     vcnn_net::Ring saved;
     explicit RingSwap(vcnn_net* m) : n(m), saved(m->ring) {}
-    ~RingSwap() {
-      int* c = n->ring.cursor;
-      n->ring = saved;
-      n->ring.cursor = c;
-    }
+    ~RingSwap() { n->ring = saved; }
   } ring_swap(n);
   auto& P = n->pipe;
   if (!P.cp) {
@@ -1332,12 +1331,15 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.consumed[k], cudaEventDisableTiming));
     }
   }
-  {
-    const float* x0 = P.xs[0];
-    const void* t0 = ce ? (const void*)P.cs[0] : (const void*)P.vs[0];
-    TRY(vcnn_net_set_batch_ring(n, vcnn_net::kSlots, batch, x0, n->in_per * n->max_batch, t0,
-                                ce ? n->max_batch : n->out_units * n->max_batch));
-  }
+  if (!P.cur) VCNN_CUDA_TRY(cudaMalloc(&P.cur, 2 * sizeof(int)));
+  VCNN_CUDA_TRY(cudaMemsetAsync(P.cur, 0, 2 * sizeof(int), n->stream));
+  n->ring.x = P.xs[0];
+  n->ring.t = ce ? (const void*)P.cs[0] : (const void*)P.vs[0];
+  n->ring.nbatch = vcnn_net::kSlots;
+  n->ring.batch = batch;
+  n->ring.xs = n->in_per * n->max_batch;
+  n->ring.ts = ce ? n->max_batch : n->out_units * n->max_batch;
+  n->ring.cursor = P.cur;
   if (P.hl_cap < nsteps) {
     if (P.hl) cudaFreeHost(P.hl);
     if (P.dl) cudaFree(P.dl);
