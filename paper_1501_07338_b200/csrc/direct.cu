@@ -74,6 +74,8 @@ struct Geo {
                            // maps of one kernel row (ngx groups per row), N = NM positions
   int ns;                  // N-stacked 1-D segments: the MMA's N = T taps x Cout maps
   int gbuild;              // 2-D tile slab built straight from global (image too big to stage)
+  int rf, kh0;             // row fold (single-channel forward): MMA channel j = input row
+                           // offset j of an 8-row kernel band; kh0 = the unfolded kernel height
   int eps, off_ep;         // epilogue staging: row stride (floats), offset (bytes)
   int bsx;                 // stacked: bytes between the staged tap blocks (incl. the +1 shift)
 };
@@ -260,6 +262,16 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
             g.pad_y, g.pad_x};
     g.seg = 1;
   }
+  g.kh0 = g.kh;
+  // single-channel forward with a tall kernel (denoise-16's 16x16 first
+  // layer): fold 8 kernel rows into the MMA's 8 channels -- channel j of slab
+  // position (y, x) is the image at (y + j, x), a folded tap (ky', kx) sits
+  // 8*ky' rows down -- so K = 8 carries 8 real products instead of 1
+  if (mode == 0 && g.Cin == 1 && g.kh >= 8 && !g.seg && !tma) {
+    g.rf = 8;
+    g.Cin = 8;
+    g.kh = (int)cdiv(g.kh0, 8);
+  }
   // a forward view with < 4 input channels pads the MMA K (8 channels) by 2x
   // or more; those layers go to the small-Kd kernel or the generic implicit GEMM
   if (mode == 0 && g.Cin < 4) return false;
@@ -270,8 +282,8 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
   // and N = up to 256 positions (the slab), ~4x less operand traffic per MAC
   // (scripts/micro/mma_issue.cu: an M=128 K=8 tf32 MMA costs ~32 + N/4
   // cycles -- its shared-memory operand reads)
-  if (tapstack_enabled() && mode == 0 && !g.seg && g.Cout <= 32 && g.kw >= 3 && g.Wg <= 63 &&
-      d.kd() >= 32)
+  if (tapstack_enabled() && mode == 0 && !g.seg && !g.rf && g.Cout <= 32 && g.kw >= 3 &&
+      g.Wg <= 63 && d.kd() >= 32)
     return plan_ts(d, mode, pool, POH, POW, g, tma);
   g.eps = EPS;
   int R = g.seg ? 1 : BM / g.Wg;
@@ -291,7 +303,8 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
   g.R = R;
   g.tpi = (int)cdiv(g.Hout, R) * (g.seg ? g.nseg : 1);
   g.CG = (int)cdiv(g.Cin, 8);
-  const int maxsh = g.seg ? g.kw - 1 : (g.kh - 1) * g.Wg + g.kw - 1;
+  const int ystep = g.rf ? g.rf : 1;  // image rows per (folded) kernel row
+  const int maxsh = g.seg ? g.kw - 1 : (g.kh - 1) * ystep * g.Wg + g.kw - 1;
   g.NP = (int)cdiv(maxsh + BM, 8) * 8;
   if (tma) {
     // the tensor map box [2*CG quads][rows][Wg][4 channels] is the slab itself
@@ -303,22 +316,22 @@ bool plan(const ConvDesc& d, int mode, int pool, int POH, int POW, Geo& g, int t
     if (g.rows > 256) return false;
     g.NP = g.rows * g.Wg;
   }
-  g.raw_n = g.Cin * g.Hin * g.Win;
+  g.raw_n = (g.rf ? 1 : g.Cin) * g.Hin * g.Win;
   // an image too big to stage whole (e.g. denoise-16's 64 x 49 x 49 maps):
   // each tile builds its slab straight from global memory (not for a routed
   // data gradient, which scatters into the staged image)
   if (!g.tma && !g.seg && 4 * g.raw_n > 96 * 1024) {
-    if (mode == 1 && pool) return false;
+    if ((mode == 1 && pool) || g.rf) return false;
     g.gbuild = 1;
   }
   // the input image and the window arrays go in with single bulk copies
-  if (!g.seg && !g.gbuild && (g.Cin * g.Hin * g.Win) % 4 != 0) return false;
+  if (!g.seg && !g.gbuild && g.raw_n % 4 != 0) return false;
   if (pool && mode == 1 && (d.K * POH * POW) % 4 != 0) return false;
   // dgrad always reserves window scratch for a >= 2x2 pool, so the routed
   // and unrouted plans (and the weight pack) share one BN
   if (mode == 1 && !g.seg && !g.gbuild) g.win_n = ((d.K * ((d.OH + 1) / 2) * ((d.OW + 1) / 2)) + 3) & ~3;
   const bool staged = !(g.tma || g.seg || g.gbuild);
-  const int a_bytes = g.CG * 2 * g.NP * 16 + (staged ? 4 * g.NP : 0);  // slab + table
+  const int a_bytes = g.CG * 2 * g.NP * 16 + (staged ? (g.rf ? 8 : 4) * g.NP : 0);  // slab + table(s)
   const int raw_bytes = staged ? 4 * g.raw_n : 0;
   const int win_bytes = 2 * 4 * g.win_n;
   if (raw_bytes > 96 * 1024) return false;
@@ -392,9 +405,14 @@ __global__ void pack_kernel(Geo g, int mode, const float* __restrict__ w, float*
     const int kx = g.ts || g.ns ? (s - ky * g.ngx) * g.T + jb : s - ky * g.kw;
     if (prow < g.Cout && ch < g.Cin && kx < g.kw && jb < (g.ns ? g.T : 4)) {
       const int row = prow;
-      const int n = mode == 0 ? row : ch, c = mode == 0 ? ch : row;
-      const int wy = mode == 0 ? ky : g.kh - 1 - ky, wx = mode == 0 ? kx : g.kw - 1 - kx;
-      v = ptx::to_tf32(w[(((int64_t)n * Cch + c) * g.kh + wy) * g.kw + wx]);
+      if (g.rf) {  // folded: channel ch = row offset inside the 8-row band ky
+        const int wy = ky * g.rf + ch;
+        if (wy < g.kh0) v = ptx::to_tf32(w[((int64_t)row * g.kh0 + wy) * g.kw + kx]);
+      } else {
+        const int n = mode == 0 ? row : ch, c = mode == 0 ? ch : row;
+        const int wy = mode == 0 ? ky : g.kh - 1 - ky, wx = mode == 0 ? kx : g.kw - 1 - kx;
+        v = ptx::to_tf32(w[(((int64_t)n * Cch + c) * g.kh + wy) * g.kw + wx]);
+      }
     }
     pk[i] = v;
   }
@@ -679,9 +697,9 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     } else if (g.seg || g.gbuild) {
       // (the row segment / tile is built from global by all threads below)
     } else if (!routed) {
-      const uint32_t rb = 4u * (uint32_t)(g.Cin * g.Hin * g.Win);
+      const uint32_t rb = 4u * (uint32_t)g.raw_n;
       ptx::mbar_expect_tx(&load_bar, rb);
-      ptx::bulk_g2s(s_raw, a.in + (int64_t)b * g.Cin * g.Hin * g.Win, rb, &load_bar);
+      ptx::bulk_g2s(s_raw, a.in + (int64_t)b * g.raw_n, rb, &load_bar);
     } else {
       const uint32_t wb = 4u * (uint32_t)wsz;
       ptx::mbar_expect_tx(&load_bar, 2 * wb);
@@ -753,18 +771,22 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
     }
   } else if (!g.tma) {
     int* pos_off = reinterpret_cast<int*>(smem + g.off_a) + g.CG * 2 * g.NP * 4;
+    int* rows_left = pos_off + g.NP;  // (row fold: image rows from the position's row on)
     for (int P = tid; P < g.NP; P += NT) {
       const int yy = r0 + P / g.Wg - g.pad_y, xx = P % g.Wg - g.pad_x;
       pos_off[P] = (yy >= 0 && yy < g.Hin && xx >= 0 && xx < g.Win) ? yy * g.Win + xx : -1;
+      if (g.rf) rows_left[P] = g.Hin - yy;
     }
     __syncthreads();
     const uint32_t s_pos = ptx::smem_u32(pos_off);
-    const int hw = g.Hin * g.Win;
+    // channel stride in the staged image: a plane, or (row fold) one image row
+    const int hw = g.rf ? g.Win : g.Hin * g.Win;
     const uint32_t hstride = (uint32_t)g.NP * 16u;  // bytes per (cg, half) block
     // j = (position, channel%4); the channel-group loop inside keeps 4
     // independent loads in flight per thread
     for (int j = tid; j < 4 * g.NP; j += NT) {
       const int off = ptx::lds_s32(s_pos + 4u * (j >> 2));
+      const int cmax = g.rf ? ptx::lds_s32(s_pos + 4u * (g.NP + (j >> 2))) : g.Cin;
       const int c4 = j & 3;
       const uint32_t dst = s_a + 4u * j;
       int ch = 0;
@@ -773,14 +795,17 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = (ch + u) * 4 + c4;
-          v[u] = (c < g.Cin && off >= 0) ? ptx::lds_f32(s_raw + 4u * (c * hw + off)) : 0.f;
+          v[u] = (c < g.Cin && c < cmax && off >= 0) ? ptx::lds_f32(s_raw + 4u * (c * hw + off))
+                                                     : 0.f;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) ptx::sts_f32(dst + (uint32_t)(ch + u) * hstride, ptx::to_tf32(v[u]));
       }
       for (; ch < 2 * g.CG; ++ch) {
         const int c = ch * 4 + c4;
-        const float v = (c < g.Cin && off >= 0) ? ptx::lds_f32(s_raw + 4u * (c * hw + off)) : 0.f;
+        const float v = (c < g.Cin && c < cmax && off >= 0)
+                            ? ptx::lds_f32(s_raw + 4u * (c * hw + off))
+                            : 0.f;
         ptx::sts_f32(dst + (uint32_t)ch * hstride, ptx::to_tf32(v));
       }
     }
@@ -877,7 +902,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       uint64_t bd = ptx::interleave_desc(s_b + (uint32_t)(buf * g.wchunk), 128u, 256u) +
                     (uint64_t)(s0 - c * g.SC) * g.CG * b_blk;
       for (int sft = s0; sft <= s1; ++sft) {
-        uint64_t ad = a0 + (uint64_t)(ky * g.Wg + kx);
+        uint64_t ad = a0 + (uint64_t)(ky * (g.rf ? g.rf : 1) * g.Wg + kx);
         for (int cg = 0; cg < g.CG; ++cg) {
           ptx::mma_tf32(tmem, ad, bd, idesc, acc);
           acc = 1;
@@ -1040,6 +1065,10 @@ __device__ __forceinline__ int64_t pack_index(const Geo& g, int row, int ch, int
     const int ky = s / g.kw, kx = s - ky * g.kw;
     row += (kx % g.T) * (g.ts ? 32 : g.Cout);
     s = ky * g.ngx + kx / g.T;
+  } else if (g.rf) {  // row-folded: channel = ky % 8, folded row ky / 8
+    const int ky = s / g.kw, kx = s - ky * g.kw;
+    ch = ky % g.rf;
+    s = (ky / g.rf) * g.kw + kx;
   }
   const int nb = row / g.BN, r = row - nb * g.BN, cg = ch >> 3, kk = ch & 7;
   return ((((int64_t)nb * nshift(g) + s) * g.CG + cg) * (g.BN / 8) + (r >> 3)) * 64 +
