@@ -605,6 +605,23 @@ __global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce_kernel(
   }
 }
 
+// the float4 variant: outputs [0, nw) to dw, [nw, per) to db (per, stride
+// and nw multiples of 4, 16-byte aligned buffers); same bits as the scalar one
+__global__ void __launch_bounds__(32 * kRedSlices) wgrad_reduce4_kernel(
+    int nimg, int64_t per, int64_t stride, int64_t nw, const float* __restrict__ part,
+    float* __restrict__ dw, float* __restrict__ db) {
+  PDL_ENTRY();
+  __shared__ float4 red[kRedSlices][33];
+  const int64_t i4 = blockIdx.x * 32ll + (threadIdx.x & 31);
+  const float4 t = image_sum4(nimg, per / 4, stride / 4, i4,
+                              reinterpret_cast<const float4*>(part), red);
+  if ((threadIdx.x >> 5) == 0 && 4 * i4 < per) {
+    const int64_t i = 4 * i4;
+    if (i < nw) *reinterpret_cast<float4*>(dw + i) = t;
+    else if (db) *reinterpret_cast<float4*>(db + (i - nw)) = t;
+  }
+}
+
 bool wgrad_ok(const ConvDesc& d, const GradSrc& gs) {
   WGeo g;
   return wplan(d, gs, g);
@@ -636,9 +653,17 @@ int conv_wgrad(const ConvDesc& d, const float* x, const GradSrc& gs, float* dw, 
   VCNN_CUDA_TRY(launch_pdl(wgrad_shift_kernel, dim3((unsigned)d.B), dim3(WT), smem, st, a));
   VCNN_LAUNCHED();
   const int64_t per = a.g.part, nw = per - d.K;
-  const int64_t blocks = cdiv(per, 32);
-  VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)blocks), dim3(32 * kRedSlices), 0, st, d.B, per,
-                           a.g.pstride, nw, (const float*)ws.ptr, dw, db));
+  const bool vec = per % 4 == 0 && nw % 4 == 0 && a.g.pstride % 4 == 0 &&
+                   ((reinterpret_cast<uintptr_t>(ws.ptr) | reinterpret_cast<uintptr_t>(dw) |
+                     reinterpret_cast<uintptr_t>(db)) & 15) == 0;
+  if (vec)
+    VCNN_CUDA_TRY(launch_pdl(wgrad_reduce4_kernel, dim3((unsigned)cdiv(per / 4, 32)),
+                             dim3(32 * kRedSlices), 0, st, d.B, per, a.g.pstride, nw,
+                             (const float*)ws.ptr, dw, db));
+  else
+    VCNN_CUDA_TRY(launch_pdl(wgrad_reduce_kernel, dim3((unsigned)cdiv(per, 32)),
+                             dim3(32 * kRedSlices), 0, st, d.B, per, a.g.pstride, nw,
+                             (const float*)ws.ptr, dw, db));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
