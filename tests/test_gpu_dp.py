@@ -118,6 +118,39 @@ def test_barrier_mode_concurrent_streams_equals_group():
         assert np.array_equal(res[0][r], res[1][r])
 
 
+def test_barrier_mode_with_batch_ring_equals_explicit_loads():
+    """The bench's multi-GPU step: each replica stages its shard's next batch
+    from its own device batch ring inside its graph (vcnn_net_set_batch_ring),
+    then the fused exchange -- identical to staging every batch explicitly."""
+    spec, B, G, nb = DENOISE_MINI, 16, 2, 3
+    x, _, vals = S.synth_bench_data(spec, B * nb, 8)
+    xs = torch.as_tensor(x.reshape(nb, B, -1), device="cuda")
+    vs = torch.as_tensor(vals.reshape(nb, B, -1), device="cuda")
+    res = []
+    for ring in (False, True):
+        nets, sizes = _replicas(spec, x[:B], None, vals[:B], Precision.tf32, G, streams=True)
+        dps = DataParallel.local_group(nets, barrier=True)
+        for r, n in enumerate(nets):
+            lo, hi = shard_range(B, r, G)
+            n.enable_graph(True)
+            if ring:
+                n.set_batch_ring(xs[:, lo:hi].contiguous(), vs[:, lo:hi].contiguous())
+        for i in range(5):
+            for r, (n, d, b) in enumerate(zip(nets, dps, sizes)):
+                if not ring:
+                    lo, hi = shard_range(B, r, G)
+                    n.load_batch(xs[i % nb, lo:hi], values=vs[i % nb, lo:hi])
+                d.train_step(b, LR, MOM)
+        for d in dps:
+            d.status()
+        res.append([n.get_params() for n in nets])
+        for n in nets:
+            n.close()
+    for r in range(G):
+        assert np.array_equal(res[0][r], res[1][r])
+    assert np.array_equal(res[1][0], res[1][1])
+
+
 @pytest.fixture
 def world1_pg(tmp_path):
     import torch.distributed as dist
