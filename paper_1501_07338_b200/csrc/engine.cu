@@ -140,6 +140,7 @@ struct vcnn_net {
   // host-stream training (vcnn_net_train_host_stream): two device staging
   // slots filled by a copy stream while the previous step computes
   static constexpr int kSlots = 3;  // host-stream staging slots (H2D gets two step times)
+  static constexpr int kLossRing = 4096;  // host-stream device loss history (power of 2)
   struct Pipe {
     cudaStream_t cp = nullptr;
     cudaStream_t rd = nullptr;  // loss read-back (its own stream: it waits for each step)
@@ -178,7 +179,8 @@ struct vcnn_net {
     const void* t = nullptr;
     int nbatch = 0, batch = 0;
     int64_t xs = 0, ts = 0;
-    int* cursor = nullptr;  // [slot, blocks done]
+    int* cursor = nullptr;  // [slot, blocks done, steps]
+    float* lhist = nullptr;  // (host stream) per-step loss history, or none
   } ring;
   direct::ImageSumFold fold2{};
   int64_t fold2_off = 0;
@@ -649,7 +651,8 @@ int eager_step(vcnn_net* n, int batch, float lr, float mom) {
     TRY(launch_ring_stage(n->ring.x, n->x, n->in_per * batch, n->ring.xs, n->ring.t,
                           ce ? (void*)n->cls : (void*)n->values,
                           ce ? batch : n->out_units * batch, n->ring.ts, n->ring.nbatch,
-                          n->ring.cursor, n->stream));
+                          n->ring.cursor, n->stream, n->loss, n->ring.lhist,
+                          vcnn_net::kLossRing - 1));
   }
   TRY(run_forward(n, batch, tail));
   n->defer_fold = !n->dp || n->dp->world == 1;
@@ -1221,8 +1224,9 @@ int vcnn_net_set_batch_ring(vcnn_net* n, int nbatch, int batch, const float* x,
   if (!x || !targets || x_stride < n->in_per * batch ||
       t_stride < (ce ? batch : n->out_units * batch))
     return fail(VCNN_ESHAPE, "batch ring: buffers / strides");
-  if (!n->ring.cursor) VCNN_CUDA_TRY(cudaMalloc(&n->ring.cursor, 2 * sizeof(int)));
-  VCNN_CUDA_TRY(cudaMemsetAsync(n->ring.cursor, 0, 2 * sizeof(int), n->stream));
+  if (!n->ring.cursor) VCNN_CUDA_TRY(cudaMalloc(&n->ring.cursor, 4 * sizeof(int)));
+  VCNN_CUDA_TRY(cudaMemsetAsync(n->ring.cursor, 0, 4 * sizeof(int), n->stream));
+  n->ring.lhist = nullptr;
   n->ring.x = x;
   n->ring.t = targets;
   n->ring.nbatch = nbatch;
@@ -1331,8 +1335,8 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
       VCNN_CUDA_TRY(cudaEventCreateWithFlags(&P.consumed[k], cudaEventDisableTiming));
     }
   }
-  if (!P.cur) VCNN_CUDA_TRY(cudaMalloc(&P.cur, 2 * sizeof(int)));
-  VCNN_CUDA_TRY(cudaMemsetAsync(P.cur, 0, 2 * sizeof(int), n->stream));
+  if (!P.cur) VCNN_CUDA_TRY(cudaMalloc(&P.cur, 4 * sizeof(int)));
+  VCNN_CUDA_TRY(cudaMemsetAsync(P.cur, 0, 4 * sizeof(int), n->stream));
   n->ring.x = P.xs[0];
   n->ring.t = ce ? (const void*)P.cs[0] : (const void*)P.vs[0];
   n->ring.nbatch = vcnn_net::kSlots;
@@ -1342,15 +1346,15 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
   n->ring.cursor = P.cur;
   if (P.hl_cap < nsteps) {
     if (P.hl) cudaFreeHost(P.hl);
-    if (P.dl) cudaFree(P.dl);
     P.hl = nullptr;
-    P.dl = nullptr;
     P.hl_cap = 0;
     VCNN_CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&P.hl), sizeof(float) * nsteps,
                                 cudaHostAllocDefault));
-    VCNN_CUDA_TRY(cudaMalloc(&P.dl, sizeof(float) * nsteps));
     P.hl_cap = nsteps;
   }
+  // device loss history: a fixed ring (captured step graphs keep its pointer)
+  if (!P.dl) VCNN_CUDA_TRY(cudaMalloc(&P.dl, sizeof(float) * vcnn_net::kLossRing));
+  n->ring.lhist = P.dl;  // step i's staging kernel files step i-1's loss
   const size_t xb = sizeof(float) * n->in_per * batch;
   const size_t tb = ce ? sizeof(int) * batch : sizeof(float) * n->out_units * batch;
   // every copy is ordered after the work already queued on the net's stream
@@ -1372,17 +1376,23 @@ int vcnn_net_train_host_stream(vcnn_net* n, int nsteps, int batch, const float* 
     // compute stream: slot k -> the input slots, the step, the loss to host
     VCNN_CUDA_TRY(cudaStreamWaitEvent(n->stream, P.copied[k], 0));
     // the step's graph stages slot k (the ring cursor walks 0, 1, 2, 0, ...)
+    // and files the previous step's loss into P.dl[i - 1]
     TRY(train_step(n, batch, lr, mom));
     VCNN_CUDA_TRY(cudaEventRecord(P.consumed[k], n->stream));
-    // the step's loss: a store kernel into its own device slot (no copy-engine
-    // op between two graph launches on the compute stream), read back to the
-    // host by the copy stream once the step is done
-    TRY(launch_store_scalar(n->loss, P.dl + i, n->stream));
-    VCNN_CUDA_TRY(cudaEventRecord(P.stored, n->stream));
-    VCNN_CUDA_TRY(cudaStreamWaitEvent(P.rd, P.stored, 0));
-    VCNN_CUDA_TRY(cudaMemcpyAsync(P.hl + i, P.dl + i, sizeof(float), cudaMemcpyDeviceToHost,
-                                  P.rd));
+    if (i > 0) {  // step i-1's loss back to the host on the read-back stream
+      const int j = (i - 1) & (vcnn_net::kLossRing - 1);
+      VCNN_CUDA_TRY(cudaStreamWaitEvent(P.rd, P.consumed[k], 0));
+      VCNN_CUDA_TRY(cudaMemcpyAsync(P.hl + i - 1, P.dl + j, sizeof(float),
+                                    cudaMemcpyDeviceToHost, P.rd));
+    }
   }
+  // the last step's loss
+  const int jl = (nsteps - 1) & (vcnn_net::kLossRing - 1);
+  TRY(launch_store_scalar(n->loss, P.dl + jl, n->stream));
+  VCNN_CUDA_TRY(cudaEventRecord(P.stored, n->stream));
+  VCNN_CUDA_TRY(cudaStreamWaitEvent(P.rd, P.stored, 0));
+  VCNN_CUDA_TRY(cudaMemcpyAsync(P.hl + nsteps - 1, P.dl + jl, sizeof(float),
+                                cudaMemcpyDeviceToHost, P.rd));
   VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
   VCNN_CUDA_TRY(cudaStreamSynchronize(P.rd));
   if (losses) std::memcpy(losses, P.hl, sizeof(float) * nsteps);

@@ -78,7 +78,8 @@ int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, v
                        int64_t nt_words, cudaStream_t st);
 int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, const void* ts,
                       void* td, int64_t nt, int64_t tstride, int nbatch, int* cursor,
-                      cudaStream_t st);
+                      cudaStream_t st, const float* lsrc = nullptr, float* lhist = nullptr,
+                      int lmask = 0);
 // the network head fused: last full layer fwd + loss fwd/bwd + its
 // dW / db / dX (dX * act_prev'(x)); one cluster, fp32
 bool head_fusable(int B, int in, int out);

@@ -1073,10 +1073,18 @@ int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, v
 __global__ void ring_stage_kernel(const float* __restrict__ xs, float* __restrict__ xd, int64_t nx,
                                   int64_t xstride, const uint32_t* __restrict__ ts,
                                   uint32_t* __restrict__ td, int64_t nt, int64_t tstride,
-                                  int nbatch, int* cursor) {
+                                  int nbatch, int* cursor, const float* lsrc, float* lhist,
+                                  int lmask) {
   PDL_ENTRY();
   __shared__ int slot;
   if (threadIdx.x == 0) slot = *((volatile int*)cursor);
+  // (host stream) the previous step's loss into its history slot; cursor[2]
+  // counts the steps
+  if (lhist && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int c = cursor[2];
+    if (c > 0) lhist[(c - 1) & lmask] = *lsrc;
+    cursor[2] = c + 1;
+  }
   __syncthreads();
   const float* xsrc = xs + (int64_t)slot * xstride;
   const uint32_t* tsrc = ts + (int64_t)slot * tstride;
@@ -1100,7 +1108,7 @@ __global__ void ring_stage_kernel(const float* __restrict__ xs, float* __restric
 
 int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, const void* ts,
                       void* td, int64_t nt, int64_t tstride, int nbatch, int* cursor,
-                      cudaStream_t st) {
+                      cudaStream_t st, const float* lsrc, float* lhist, int lmask) {
   if (((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(xd)) & 15) ||
       xstride % 4)
     return fail(VCNN_ESHAPE, "batch ring: x must be 16-byte aligned, x_stride a multiple of 4");
@@ -1108,7 +1116,8 @@ int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, c
   if (blocks > 2 * sm_count()) blocks = 2 * sm_count();
   VCNN_CUDA_TRY(launch_pdl(ring_stage_kernel, dim3((unsigned)blocks), dim3(256), 0, st, xs, xd,
                            nx, xstride, static_cast<const uint32_t*>(ts),
-                           static_cast<uint32_t*>(td), nt, tstride, nbatch, cursor));
+                           static_cast<uint32_t*>(td), nt, tstride, nbatch, cursor, lsrc,
+                           lhist, lmask));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
