@@ -1213,6 +1213,10 @@ int vcnn_net_set_batch_device(vcnn_net* n, int batch, const float* x, const int*
 int vcnn_net_set_batch_ring(vcnn_net* n, int nbatch, int batch, const float* x,
                             int64_t x_stride, const void* targets, int64_t t_stride) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
+  // captured steps bake the ring's buffers, strides and size into their
+  // staging kernel: a changed ring is a fresh set of graphs
+  VCNN_CUDA_TRY(cudaStreamSynchronize(n->stream));
+  drop_graph(n);
   if (nbatch <= 0) {
     n->ring.x = nullptr;
     n->ring.t = nullptr;
