@@ -436,15 +436,24 @@ def main():
             else "nccl all-reduce + sgd"
 
     # ---- timed region: one event pair around the K steps (device time), a
-    # fresh batch from HBM each step ----
+    # fresh batch from HBM each step.  One GPU: vcnn_net_train_steps -- up to
+    # 8 steps per graph launch, each staging its ring batch (the K-step chunk
+    # graphs are captured in an untimed pass first)
+    multi = world == 1 and not args.no_graph
+    if multi:
+        net.train_steps(args.steps, B, lr, mom)
+        barrier()
     ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     launches0 = _lib.lib().vcnn_launch_count()
     with ClockSampler(local) as clk:
         barrier()
         ev[0].record(stream)
-        for i in range(args.steps):
-            load(args.warmup + i)
-            step()
+        if multi:
+            net.train_steps(args.steps, B, lr, mom)
+        else:
+            for i in range(args.steps):
+                load(args.warmup + i)
+                step()
         ev[1].record(stream)
         barrier()
     launches = _lib.lib().vcnn_launch_count() - launches0

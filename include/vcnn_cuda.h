@@ -299,6 +299,9 @@ int vcnn_net_forward(vcnn_net* net, int batch);
 int vcnn_net_sgd_step(vcnn_net* net, float lr, float mom, float grad_scale);
 /* forward_backward + sgd_step; replayed from a CUDA graph when enabled */
 int vcnn_net_train_step(vcnn_net* net, int batch, float lr, float mom);
+/* nsteps train steps, up to 8 captured in one graph launch (with graphs
+ * enabled; a batch ring attached makes every step stage its next batch) */
+int vcnn_net_train_steps(vcnn_net* net, int nsteps, int batch, float lr, float mom);
 /* end-to-end: HOST batch in (validated: class bounds -> VCNN_EBOUNDS),
  * H2D copy, train step, D2H loss; synchronous */
 int vcnn_net_train_step_host(vcnn_net* net, int batch, const float* x, const int* cls,

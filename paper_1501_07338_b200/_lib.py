@@ -128,6 +128,7 @@ _SIGS = {
     "vcnn_net_input_buffers": [c_vp, C.POINTER(c_vp), C.POINTER(c_vp), C.POINTER(c_vp)],
     "vcnn_net_set_batch_device": [c_vp, c_int, c_vp, c_vp, c_vp],
     "vcnn_net_set_batch_ring": [c_vp, c_int, c_int, c_vp, c_i64, c_vp, c_i64],
+    "vcnn_net_train_steps": [c_vp, c_int, c_int, C.c_float, C.c_float],
     "vcnn_net_forward_backward": [c_vp, c_int],
     "vcnn_net_forward": [c_vp, c_int],
     "vcnn_net_sgd_step": [c_vp, c_float, c_float, c_float],

@@ -131,6 +131,7 @@ struct vcnn_net {
     const DpLink* dp;
     int dpv;
     const void* ring;  // the batch ring the graph stages from (null: none)
+    int steps;         // training steps captured back to back in the graph
     cudaGraphExec_t exec;
     int kernels;
   };
@@ -159,6 +160,7 @@ struct vcnn_net {
   const DpLink* g_dp = nullptr;
   int g_dpv = 0;
   const void* g_ring = nullptr;
+  int g_steps = 1;
   int kernels_per_step = 0;
   bool guard = false;  // Trainer non-finite stop armed (err[2..3] on the device)
   DpLink* dp = nullptr;  // attached data-parallel group (vcnn_dp_*), or none
@@ -666,18 +668,28 @@ int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   return VCNN_OK;
 }
 
-int train_step(vcnn_net* n, int batch, float lr, float mom) {
+// k training steps in ONE graph launch (k > 1: captured back to back -- each
+// stages its own batch when a ring is attached -- so consecutive steps are
+// not separated by a graph launch)
+int train_steps_graph(vcnn_net* n, int k, int batch, float lr, float mom);
+
+int train_step(vcnn_net* n, int batch, float lr, float mom) { return train_steps_graph(n, 1, batch, lr, mom); }
+
+int train_steps_graph(vcnn_net* n, int k, int batch, float lr, float mom) {
   TRY(check_batch(n, batch));
   TRY(check_cfg(lr, mom));
-  if (!n->use_graph || n->breakdown) return eager_step(n, batch, lr, mom);
+  if (!n->use_graph || n->breakdown) {
+    for (int i = 0; i < k; ++i) TRY(eager_step(n, batch, lr, mom));
+    return VCNN_OK;
+  }
   const int dpv = n->dp ? n->dp->version : 0;
   const void* ring = n->ring.nbatch ? (const void*)n->ring.x : nullptr;
   if (!n->gexec || n->g_batch != batch || n->g_lr != lr || n->g_mom != mom ||
-      n->g_dp != n->dp || n->g_dpv != dpv || n->g_ring != ring) {
+      n->g_dp != n->dp || n->g_dpv != dpv || n->g_ring != ring || n->g_steps != k) {
     n->gexec = nullptr;
     for (auto& e : n->graphs)
       if (e.batch == batch && e.lr == lr && e.mom == mom && e.dp == n->dp &&
-          e.dpv == (n->dp ? n->dp->version : 0) && e.ring == ring) {
+          e.dpv == (n->dp ? n->dp->version : 0) && e.ring == ring && e.steps == k) {
         n->gexec = e.exec;
         n->kernels_per_step = e.kernels;
       }
@@ -689,6 +701,7 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     n->g_dp = n->dp;
     n->g_dpv = dpv;
     n->g_ring = ring;
+    n->g_steps = k;
   } else {
     if (n->graphs.size() >= 4) drop_graph(n);
     if (!n->cap_stream)
@@ -700,7 +713,8 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     VCNN_CUDA_TRY(cudaStreamSynchronize(user));
     VCNN_CUDA_TRY(cudaStreamBeginCapture(n->cap_stream, cudaStreamCaptureModeRelaxed));
     n->stream = n->cap_stream;
-    int s = eager_step(n, batch, lr, mom);
+    int s = VCNN_OK;
+    for (int i = 0; i < k && !s; ++i) s = eager_step(n, batch, lr, mom);
     n->stream = user;
     cudaError_t e = cudaStreamEndCapture(n->cap_stream, &g);
     if (s) {
@@ -712,16 +726,17 @@ int train_step(vcnn_net* n, int batch, float lr, float mom) {
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
     n->graphs.push_back(
-        vcnn_net::GraphEntry{batch, lr, mom, n->dp, dpv, ring, n->gexec, n->kernels_per_step});
+        vcnn_net::GraphEntry{batch, lr, mom, n->dp, dpv, ring, k, n->gexec, n->kernels_per_step});
     n->g_batch = batch;
     n->g_lr = lr;
     n->g_mom = mom;
     n->g_dp = n->dp;
     n->g_dpv = dpv;
     n->g_ring = ring;
+    n->g_steps = k;
   }
   VCNN_CUDA_TRY(cudaGraphLaunch(n->gexec, n->stream));
-  g_launches.fetch_add(n->kernels_per_step);
+  g_launches.fetch_add((int64_t)n->kernels_per_step * k);
   return VCNN_OK;
 }
 
@@ -1263,6 +1278,18 @@ int vcnn_net_sgd_step(vcnn_net* n, float lr, float mom, float grad_scale) {
 int vcnn_net_train_step(vcnn_net* n, int batch, float lr, float mom) {
   if (!n) return fail(VCNN_ESHAPE, "null net");
   return train_step(n, batch, lr, mom);
+}
+
+int vcnn_net_train_steps(vcnn_net* n, int nsteps, int batch, float lr, float mom) {
+  if (!n) return fail(VCNN_ESHAPE, "null net");
+  if (nsteps < 0) return fail(VCNN_ESHAPE, "train_steps: negative count");
+  constexpr int kChunk = 8;  // steps per graph launch
+  for (int done = 0; done < nsteps;) {
+    const int k = nsteps - done < kChunk ? nsteps - done : kChunk;
+    TRY(train_steps_graph(n, k, batch, lr, mom));
+    done += k;
+  }
+  return VCNN_OK;
 }
 
 int vcnn_net_train_step_host(vcnn_net* n, int batch, const float* x, const int* cls,

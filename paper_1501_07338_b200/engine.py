@@ -226,6 +226,11 @@ class Network:
     def train_step(self, batch, lr, momentum):
         check(lib().vcnn_net_train_step(self._h, int(batch), float(lr), float(momentum)))
 
+    def train_steps(self, nsteps, batch, lr, momentum):
+        """nsteps train steps, up to 8 per graph launch (vcnn_net_train_steps)."""
+        check(lib().vcnn_net_train_steps(self._h, int(nsteps), int(batch), float(lr),
+                                         float(momentum)))
+
     def train_step_host(self, x, cls=None, values=None, lr=0.01, momentum=0.0):
         """End to end: host batch in -> H2D -> step -> D2H loss (synchronous)."""
         x = np.ascontiguousarray(x, dtype=np.float32) if not isinstance(x, torch.Tensor) else x

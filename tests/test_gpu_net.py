@@ -555,6 +555,26 @@ def test_batch_ring_equals_explicit_staging():
     b.close()
 
 
+def test_train_steps_multi_step_graphs_equal_single_steps():
+    """vcnn_net_train_steps (up to 8 steps per graph launch, each staging its
+    ring batch) trains bit-identically to single graph-replayed steps."""
+    spec, B, nb = S.cifar3(), 32, 4
+    x, cls, _ = O.synth_bench_data(spec, B * nb, 8)
+    xp = torch.from_numpy(x.reshape(nb, B, -1)).cuda()
+    cp = torch.from_numpy(cls.reshape(nb, B).astype(np.int32)).cuda()
+    a, b = Network(spec, B), Network(spec, B)
+    for n in (a, b):
+        n.enable_graph(True)
+        n.set_batch_ring(xp, cp)
+    a.train_steps(11, B, 0.01, 0.9)  # chunks of 8 + 3
+    for _ in range(11):
+        b.train_step(B, 0.01, 0.9)
+    assert a.loss() == b.loss()
+    assert np.array_equal(a.get_params(), b.get_params())
+    a.close()
+    b.close()
+
+
 def test_host_stream_equals_host_steps():
     """vcnn_net_train_host_stream (H2D of batch i+1 on a copy stream while
     step i computes) gives bit-identical losses and weights to the same
