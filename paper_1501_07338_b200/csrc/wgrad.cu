@@ -233,7 +233,39 @@ __global__ void __launch_bounds__(WT, 1) wgrad_shift_kernel(const WArgs a) {
     }
     // ---- A: S shifted copies of the image from position r0*W, rows (j, c) ----
     const int pbase = r0 * g.W;
-    if (hw % 4 == 0) {
+    if (hw % 4 == 0 && g.S == 4) {
+      // 32 channels, 4 copies (CIFAR-3 conv2): two items per thread in flight
+      // (2 x 2 aligned float4 loads, then 2 x 4 stores) -- the one-item loop
+      // below is load-latency bound here
+      for (int i0 = tid; i0 < g.NG * 32; i0 += 2 * WT) {
+        float4 f[2][2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int i = i0 + t * WT, gr = i >> 5, c = i & 31;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int p = pbase + 4 * gr + 4 * u;
+            f[t][u] = (i < g.NG * 32 && c < g.C && p < hw)
+                          ? ptx::lds_f32x4(s_raw + 4u * (uint32_t)(c * hw + p))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int i = i0 + t * WT, gr = i >> 5, c = i & 31;
+          if (i >= g.NG * 32) continue;
+          const float v[8] = {ptx::to_tf32(f[t][0].x), ptx::to_tf32(f[t][0].y),
+                              ptx::to_tf32(f[t][0].z), ptx::to_tf32(f[t][0].w),
+                              ptx::to_tf32(f[t][1].x), ptx::to_tf32(f[t][1].y),
+                              ptx::to_tf32(f[t][1].z), ptx::to_tf32(f[t][1].w)};
+          const uint32_t dst = s_a + 16u * (uint32_t)(gr * 128 + c);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            ptx::sts_f32x4(dst + 16u * (uint32_t)(j * 32),
+                           make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+        }
+      }
+    } else if (hw % 4 == 0) {
       // thread -> (granule, channel): the S+3 positions from 4*gr are read as
       // aligned float4s once and written as the S copies' granule entries
       const int nq = (g.S + 6) / 4;  // float4s per item
