@@ -1106,8 +1106,10 @@ __global__ void __launch_bounds__(32 * kRedSlices) sgd_pack_kernel(
     int64_t n, float* __restrict__ w, float* __restrict__ v, float* __restrict__ g, float lr,
     float mom, float scale, const PackTable t, const float* __restrict__ loss,
     int* __restrict__ guard, const ImageSumFold fold, int64_t fold_off, const ImageSumFold fold2,
-    int64_t fold2_off) {
+    int64_t fold2_off, int* __restrict__ ring_step) {
   PDL_ENTRY();
+  // the step's batch ring advances (its staging kernel only reads the count)
+  if (ring_step && blockIdx.x == 0 && threadIdx.x == 0) *ring_step += 1;
   // Trainer::fit's non-finite stop (training.hpp:77-80): while the guard is
   // armed, a non-finite batch loss skips this update and every later one, so
   // the weights stay those the offending batch ran on
@@ -1201,8 +1203,9 @@ __device__ __forceinline__ void dp_barrier(const DpPeers& P, int phase, uint32_t
 
 __global__ void dp_sgd_pack_kernel(int64_t n, int64_t chunk, float* __restrict__ w,
                                    float* __restrict__ v, float lr, float mom, const PackTable t,
-                                   const DpPeers P) {
+                                   const DpPeers P, int* __restrict__ ring_step) {
   PDL_ENTRY();
+  if (ring_step && blockIdx.x == 0 && threadIdx.x == 0) *ring_step += 1;
   uint32_t e = 0;
   if (P.barrier) {
     if (threadIdx.x < 32) {
@@ -1255,7 +1258,7 @@ int pack_table(const std::vector<PackSpec>& layers, PackTable& t) {
 int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss,
              int* guard, const ImageSumFold* fold, int64_t fold_off, const ImageSumFold* fold2,
-             int64_t fold2_off) {
+             int64_t fold2_off, int* ring_step) {
   PackTable t;
   if (int s = pack_table(layers, t)) return s;
   constexpr int kT = 32 * kRedSlices;
@@ -1274,7 +1277,7 @@ int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float
       return fail(VCNN_ESHAPE, "sgd_pack: fold range");
     f2 = *fold2;
   }
-  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(kT), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard, f, fold_off, f2, fold2_off));
+  VCNN_CUDA_TRY(launch_pdl(sgd_pack_kernel, dim3((unsigned)blocks), dim3(kT), 0, st, n, w, v, g, lr, mom, scale, t, loss, guard, f, fold_off, f2, fold2_off, ring_step));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }
@@ -1287,14 +1290,15 @@ int dp_blocks(int64_t n) {
 }
 
 int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
-                const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st) {
+                const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st,
+                int* ring_step) {
   PackTable t;
   if (int s = pack_table(layers, t)) return s;
   if (peers.world < 1 || peers.world > kMaxWorld) return fail(VCNN_ECONFIG, "dp: world size");
   const int blocks = peers.nslot;
   if (blocks < 1 || blocks > kMaxDpSlots) return fail(VCNN_ECONFIG, "dp: block count");
   const int64_t chunk = cdiv(n, blocks);
-  VCNN_CUDA_TRY(launch_pdl(dp_sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, chunk, w, v, lr, mom, t, peers));
+  VCNN_CUDA_TRY(launch_pdl(dp_sgd_pack_kernel, dim3((unsigned)blocks), dim3(256), 0, st, n, chunk, w, v, lr, mom, t, peers, ring_step));
   VCNN_LAUNCHED();
   return VCNN_OK;
 }

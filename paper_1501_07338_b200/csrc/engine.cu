@@ -568,7 +568,7 @@ int prep_weights(vcnn_net* n) {
   return VCNN_OK;
 }
 
-int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
+int run_sgd(vcnn_net* n, float lr, float mom, float scale, int* ring_step = nullptr) {
   Mark m(n, OTHER_B, -1, OP_SGD);
   // one launch: the update + the direct kernels' weight packs; only layers
   // on the slab fallback still need their plain tf32 copies refreshed
@@ -590,20 +590,22 @@ int run_sgd(vcnn_net* n, float lr, float mom, float scale) {
   if (!dp || dp->world == 1) {
     TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom, scale, packs,
                          n->stream, n->loss, n->err + 2, n->fold.part ? &n->fold : nullptr,
-                         n->L[0].w_off, n->fold2.part ? &n->fold2 : nullptr, n->fold2_off));
+                         n->L[0].w_off, n->fold2.part ? &n->fold2 : nullptr, n->fold2_off,
+                         ring_step));
     n->fold = direct::ImageSumFold{};
     n->fold2 = direct::ImageSumFold{};
   } else if (dp->mode == VCNN_DP_P2P) {
     // one kernel: rank-ordered sum of every replica's gradient (peers over
     // NVLink) + SGD + packs
     TRY(direct::dp_sgd_pack(n->nparams, n->params, n->vel, lr, mom, packs, dp->peers,
-                            n->stream));
+                            n->stream, ring_step));
   } else {
     // NCCL fallback: weight, all-reduce (sum) in place, replicated update
     if (!dp->equal) TRY(dp_scale(n->nparams, n->grads, dp->local_w, n->stream));
     TRY(dp->allreduce(dp, n->grads, n->nparams, n->stream));
     TRY(direct::sgd_pack(n->nparams, n->params, n->vel, n->grads, lr, mom,
-                         dp->equal ? scale / (float)dp->world : scale, packs, n->stream));
+                         dp->equal ? scale / (float)dp->world : scale, packs, n->stream, nullptr,
+                         nullptr, nullptr, 0, nullptr, 0, ring_step));
   }
   for (const LayerRt* l : repack) {
     const ConvDesc d = conv_of(*l, 1);
@@ -663,7 +665,7 @@ int eager_step(vcnn_net* n, int batch, float lr, float mom) {
   const int sb = run_backward(n, batch, tail);
   n->defer_fold = false;
   if (sb) return sb;
-  TRY(run_sgd(n, lr, mom, 1.0f));
+  TRY(run_sgd(n, lr, mom, 1.0f, n->ring.nbatch ? n->ring.cursor + 2 : nullptr));
   n->kernels_per_step = (int)(g_launches.load() - before);
   return VCNN_OK;
 }

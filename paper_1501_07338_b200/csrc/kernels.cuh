@@ -77,7 +77,7 @@ int launch_store_scalar(const float* src, float* dst, cudaStream_t st);
 int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, void* td,
                        int64_t nt_words, cudaStream_t st);
 int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, const void* ts,
-                      void* td, int64_t nt, int64_t tstride, int nbatch, int* cursor,
+                      void* td, int64_t nt, int64_t tstride, int nbatch, const int* cursor,
                       cudaStream_t st, const float* lsrc = nullptr, float* lhist = nullptr,
                       int lmask = 0);
 // the network head fused: last full layer fwd + loss fwd/bwd + its
@@ -273,10 +273,12 @@ int sum_partials(int nimg, int64_t per, int64_t stride, const float* part, float
 int sgd_pack(int64_t n, float* w, float* v, float* g, float lr, float mom, float scale,
              const std::vector<PackSpec>& layers, cudaStream_t st, const float* loss = nullptr,
              int* guard = nullptr, const ImageSumFold* fold = nullptr, int64_t fold_off = 0,
-             const ImageSumFold* fold2 = nullptr, int64_t fold2_off = 0);
+             const ImageSumFold* fold2 = nullptr, int64_t fold2_off = 0,
+             int* ring_step = nullptr);
 int dp_blocks(int64_t n);
 int dp_sgd_pack(int64_t n, float* w, float* v, float lr, float mom,
-                const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st);
+                const std::vector<PackSpec>& layers, const DpPeers& peers, cudaStream_t st,
+                int* ring_step = nullptr);
 // weight gradient of a 1-D (kh == 1) conv with a long kernel (kw 16..128) on
 // tcgen05 (wgrad1d.cu): M = taps, N = maps, K = a row's positions, the row
 // staged as 4-element granules; row-group partials + fixed-order reduce

@@ -1068,24 +1068,20 @@ int launch_stage_batch(const float* xs, float* xd, int64_t nx, const void* ts, v
   return VCNN_OK;
 }
 
-// the ring variant: the batch index comes from a device cursor, advanced by
-// the last block to finish (a graph replays the same launch every step)
+// the ring variant: the batch index is the step counter cursor[2] (mod
+// nbatch), advanced by the step's update kernel (sgd_pack), so this kernel
+// only reads it -- no ticket, fence or barrier between the staging blocks
 __global__ void ring_stage_kernel(const float* __restrict__ xs, float* __restrict__ xd, int64_t nx,
                                   int64_t xstride, const uint32_t* __restrict__ ts,
                                   uint32_t* __restrict__ td, int64_t nt, int64_t tstride,
-                                  int nbatch, int* cursor, const float* lsrc, float* lhist,
+                                  int nbatch, const int* cursor, const float* lsrc, float* lhist,
                                   int lmask) {
   PDL_ENTRY();
-  __shared__ int slot;
-  if (threadIdx.x == 0) slot = *((volatile int*)cursor);
-  // (host stream) the previous step's loss into its history slot; cursor[2]
-  // counts the steps
-  if (lhist && blockIdx.x == 0 && threadIdx.x == 0) {
-    const int c = cursor[2];
-    if (c > 0) lhist[(c - 1) & lmask] = *lsrc;
-    cursor[2] = c + 1;
-  }
-  __syncthreads();
+  const int step = *((volatile const int*)(cursor + 2));
+  const int slot = step % nbatch;
+  // (host stream) the previous step's loss into its history slot
+  if (lhist && blockIdx.x == 0 && threadIdx.x == 0 && step > 0)
+    lhist[(step - 1) & lmask] = *lsrc;
   const float* xsrc = xs + (int64_t)slot * xstride;
   const uint32_t* tsrc = ts + (int64_t)slot * tstride;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1095,19 +1091,10 @@ __global__ void ring_stage_kernel(const float* __restrict__ xs, float* __restric
   for (int64_t i = i0; i < nx / 4; i += stride) d4[i] = __ldg(s4 + i);
   for (int64_t i = nx / 4 * 4 + i0; i < nx; i += stride) xd[i] = __ldg(xsrc + i);
   for (int64_t i = i0; i < nt; i += stride) td[i] = __ldg(tsrc + i);
-  // every block has read the cursor; the last one advances it
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(cursor + 1, 1) == (int)gridDim.x - 1) {
-      cursor[1] = 0;
-      cursor[0] = slot + 1 == nbatch ? 0 : slot + 1;
-    }
-  }
 }
 
 int launch_ring_stage(const float* xs, float* xd, int64_t nx, int64_t xstride, const void* ts,
-                      void* td, int64_t nt, int64_t tstride, int nbatch, int* cursor,
+                      void* td, int64_t nt, int64_t tstride, int nbatch, const int* cursor,
                       cudaStream_t st, const float* lsrc, float* lhist, int lmask) {
   if (((reinterpret_cast<uintptr_t>(xs) | reinterpret_cast<uintptr_t>(xd)) & 15) ||
       xstride % 4)
