@@ -620,7 +620,10 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-template <int TMEM_COLS>
+// MODE (0 forward, 1 data gradient) is a template parameter so each
+// instantiation carries only its own staging / MMA / epilogue code (the
+// kernel's instruction footprint is fetched cold once per CTA)
+template <int TMEM_COLS, int MODE>
 __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constant__ Args a) {
   pdl_launch_dependents();
   const Geo& g = a.g;
@@ -647,7 +650,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   pdl_wait();  // TMEM allocation above overlapped the previous kernel
   // ---- TMA bulk loads: prepacked B, the input image (or routed windows) ----
   const int64_t pk_per = pack_floats_per_block(g);
-  const bool routed = g.mode == 1 && a.gs.pool;
+  const bool routed = MODE == 1 && a.gs.pool;
   const int wsz = routed ? a.gs.POH * a.gs.POW * g.Cin : 0;
   const float* pack = a.pack + nb * pk_per;
   // the shifts that can touch a valid output of this tile: a 1-D dgrad tile
@@ -655,7 +658,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   // for every valid position (they would add exact zeros) -- 121 -> 92 taps
   // per tile on deconv-121's 1x121 layer; their pack chunks are not loaded
   int s_lo = 0, s_hi = nshift(g) - 1;
-  if (g.seg && g.mode == 1) {
+  if (g.seg && MODE == 1) {
     const int wid = (x0 + g.segw < g.Wout ? x0 + g.segw : g.Wout) - x0;
     const int lo = g.pad_x - x0 - (wid - 1), hi = g.pad_x - x0 + g.Win - 1;
     s_lo = lo > 0 ? lo : 0;
@@ -828,7 +831,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   DPHASE(3);
   // ---- one elected lane of warp 0 issues every MMA (converged warp: the
   // tcgen05 issue stays on the uniform datapath) ----
-  if (g.ts && warp == 0 && ptx::elect_one()) {
+  if (MODE == 0 && g.ts && warp == 0 && ptx::elect_one()) {
     // stacked: A = the pack block of (kernel row ky, tap group gx, channel
     // group) -- 128 rows = 4 taps x 32 maps; B = the slab viewed at the
     // group's first tap (ky * Wg + gx * T), N = NM positions.  Row block j of
@@ -884,7 +887,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
       ptx::mma_commit(&wempty[buf]);
     }
     ptx::mma_commit(&done_bar);
-  } else if (!g.ts && !g.ns && warp == 0 && ptx::elect_one()) {
+  } else if (!(MODE == 0 && g.ts) && !g.ns && warp == 0 && ptx::elect_one()) {
     const uint32_t idesc = ptx::idesc_tf32(BM, g.BN);  // both operands K-major
     const uint32_t half = (uint32_t)g.NP * 16u;          // LBO: the two 4-channel halves
     // descriptors advance by plain additions on the start-address field
@@ -936,7 +939,7 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
 
   // ---- epilogue: TMEM -> smem [n][128] (over raw / window / slab) -> stores ----
   const uint32_t s_ep = sbase + (uint32_t)g.off_ep;
-  if (g.ts) {
+  if (MODE == 0 && g.ts) {
     // warp j holds row block j (tap offset j): stage all four; the epilogue
     // reads out[m][p] = ((S0[m][p] + S1[m][p+1]) + S2[m][p+2]) + S3[m][p+3]
     const int quad = warp & 3;
@@ -978,14 +981,14 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   if (blockIdx.x == 0 && blockIdx.y == 0)
     for (int i = tid; i < 256; i += NT) g_dump[3][i] = ptx::lds_f32(s_raw + 4u * i);
 #endif
-  if (g.mode == 0)
+  if constexpr (MODE == 0)
     with_act(a.fe.act, [&](auto A) {
       if (g.ts || g.ns) fwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
       else fwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
     });
   else
     with_act(a.be.act_prev, [&](auto A) {
-      if (g.ts || g.ns) bwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
+      if (g.ns) bwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
       else bwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
     });
   DPHASE(5);
@@ -1008,12 +1011,18 @@ int launch(const Args& a, cudaStream_t st) {
     VCNN_LAUNCHED();
     return VCNN_OK;
   };
-  static size_t cfg32 = 0, cfg64 = 0, cfg128 = 0, cfg256 = 0;
-  if (g.ts) return go(direct_conv_kernel<256>, cfg256);
-  if (g.BN <= 32) return go(direct_conv_kernel<32>, cfg32);
-  if (g.BN <= 64) return go(direct_conv_kernel<64>, cfg64);
-  if (g.BN <= 128) return go(direct_conv_kernel<128>, cfg128);
-  return go(direct_conv_kernel<256>, cfg256);
+  static size_t cfg[2][4] = {};
+  if (g.mode == 0) {
+    if (g.ts) return go(direct_conv_kernel<256, 0>, cfg[0][3]);
+    if (g.BN <= 32) return go(direct_conv_kernel<32, 0>, cfg[0][0]);
+    if (g.BN <= 64) return go(direct_conv_kernel<64, 0>, cfg[0][1]);
+    if (g.BN <= 128) return go(direct_conv_kernel<128, 0>, cfg[0][2]);
+    return go(direct_conv_kernel<256, 0>, cfg[0][3]);
+  }
+  if (g.BN <= 32) return go(direct_conv_kernel<32, 1>, cfg[1][0]);
+  if (g.BN <= 64) return go(direct_conv_kernel<64, 1>, cfg[1][1]);
+  if (g.BN <= 128) return go(direct_conv_kernel<128, 1>, cfg[1][2]);
+  return go(direct_conv_kernel<256, 1>, cfg[1][3]);
 }
 
 }  // namespace
