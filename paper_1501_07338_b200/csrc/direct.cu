@@ -620,10 +620,11 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-// MODE (0 forward, 1 data gradient) is a template parameter so each
-// instantiation carries only its own staging / MMA / epilogue code (the
-// kernel's instruction footprint is fetched cold once per CTA)
-template <int TMEM_COLS, int MODE>
+// MODE (0 forward, 1 data gradient) and the epilogue's activation are
+// template parameters so each instantiation carries only its own staging /
+// MMA / epilogue code (the kernel's instruction footprint is fetched cold once
+// per CTA)
+template <int TMEM_COLS, int MODE, int ACT>
 __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constant__ Args a) {
   pdl_launch_dependents();
   const Geo& g = a.g;
@@ -981,16 +982,13 @@ __global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constan
   if (blockIdx.x == 0 && blockIdx.y == 0)
     for (int i = tid; i < 256; i += NT) g_dump[3][i] = ptx::lds_f32(s_raw + 4u * i);
 #endif
-  if constexpr (MODE == 0)
-    with_act(a.fe.act, [&](auto A) {
-      if (g.ts || g.ns) fwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
-      else fwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
-    });
-  else
-    with_act(a.be.act_prev, [&](auto A) {
-      if (g.ns) bwd_epilogue<decltype(A)::value, true>(a, s_ep, b, r0, n0, x0);
-      else bwd_epilogue<decltype(A)::value, false>(a, s_ep, b, r0, n0, x0);
-    });
+  if constexpr (MODE == 0) {
+    if (g.ts || g.ns) fwd_epilogue<ACT, true>(a, s_ep, b, r0, n0, x0);
+    else fwd_epilogue<ACT, false>(a, s_ep, b, r0, n0, x0);
+  } else {
+    if (g.ns) bwd_epilogue<ACT, true>(a, s_ep, b, r0, n0, x0);
+    else bwd_epilogue<ACT, false>(a, s_ep, b, r0, n0, x0);
+  }
   DPHASE(5);
   __syncthreads();
   if (warp == 0) ptx::tmem_dealloc(tmem, TMEM_COLS);
@@ -1011,18 +1009,28 @@ int launch(const Args& a, cudaStream_t st) {
     VCNN_LAUNCHED();
     return VCNN_OK;
   };
-  static size_t cfg[2][4] = {};
-  if (g.mode == 0) {
-    if (g.ts) return go(direct_conv_kernel<256, 0>, cfg[0][3]);
-    if (g.BN <= 32) return go(direct_conv_kernel<32, 0>, cfg[0][0]);
-    if (g.BN <= 64) return go(direct_conv_kernel<64, 0>, cfg[0][1]);
-    if (g.BN <= 128) return go(direct_conv_kernel<128, 0>, cfg[0][2]);
-    return go(direct_conv_kernel<256, 0>, cfg[0][3]);
-  }
-  if (g.BN <= 32) return go(direct_conv_kernel<32, 1>, cfg[1][0]);
-  if (g.BN <= 64) return go(direct_conv_kernel<64, 1>, cfg[1][1]);
-  if (g.BN <= 128) return go(direct_conv_kernel<128, 1>, cfg[1][2]);
-  return go(direct_conv_kernel<256, 1>, cfg[1][3]);
+  static size_t cfg[2][4][4] = {};  // configured smem per instantiation
+  (void)cfg;
+  const int act = g.mode == 0 ? a.fe.act : a.be.act_prev;
+  auto pick = [&](auto M, auto A) -> int {
+    constexpr int MD = decltype(M)::value, AC = decltype(A)::value;
+    const int ai = AC == VCNN_ACT_RELU ? 0 : AC == VCNN_ACT_SIGMOID ? 1 : AC == VCNN_ACT_TANH ? 2 : 3;
+    if (MD == 0 && g.ts) return go(direct_conv_kernel<256, MD, AC>, cfg[MD][3][ai]);
+    if (g.BN <= 32) return go(direct_conv_kernel<32, MD, AC>, cfg[MD][0][ai]);
+    if (g.BN <= 64) return go(direct_conv_kernel<64, MD, AC>, cfg[MD][1][ai]);
+    if (g.BN <= 128) return go(direct_conv_kernel<128, MD, AC>, cfg[MD][2][ai]);
+    return go(direct_conv_kernel<256, MD, AC>, cfg[MD][3][ai]);
+  };
+  auto by_act = [&](auto M) -> int {
+    switch (act) {
+      case VCNN_ACT_RELU: return pick(M, std::integral_constant<int, VCNN_ACT_RELU>{});
+      case VCNN_ACT_SIGMOID: return pick(M, std::integral_constant<int, VCNN_ACT_SIGMOID>{});
+      case VCNN_ACT_TANH: return pick(M, std::integral_constant<int, VCNN_ACT_TANH>{});
+      default: return pick(M, std::integral_constant<int, VCNN_ACT_IDENTITY>{});
+    }
+  };
+  return g.mode == 0 ? by_act(std::integral_constant<int, 0>{})
+                     : by_act(std::integral_constant<int, 1>{});
 }
 
 }  // namespace
