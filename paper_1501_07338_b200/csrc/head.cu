@@ -203,7 +203,10 @@ __device__ __forceinline__ void stage_cols(float* dst, int s, const float* src, 
 
 // TB/TIN/TH/TOUT: compile-time dims for the common shape (CIFAR-3's tail:
 // every index division and loop bound folds), 0 = read from the arguments
-template <int TB, int TIN, int TH, int TOUT>
+// (LOSS, AH, AO, AP: compile-time loss kind and activations of layer H,
+// layer O and the layer below, -1 = read from the arguments -- the
+// specialised kernel carries only its own loss / activation code)
+template <int TB, int TIN, int TH, int TOUT, int LOSS = -1, int AH = -1, int AO = -1, int AP = -1>
 __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   HPHASE(0);
   // every CTA of the cluster has started before anyone writes into its smem
@@ -214,6 +217,9 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   const int rank = (int)cluster.block_rank();
   const int B = TB ? TB : a.B, in = TIN ? TIN : a.in, h = TH ? TH : a.h,
             out = TOUT ? TOUT : a.out;
+  const int loss_kind = LOSS >= 0 ? LOSS : a.loss_kind;
+  const int actH = AH >= 0 ? AH : a.actH, actO = AO >= 0 ? AO : a.actO;
+  const int act_prev = AP >= 0 ? AP : a.act_prev;
   // this cluster's batch slice (rows rb .. rb + B of the Bg-row batch)
   const int cid = (int)(blockIdx.x / kC), Bg = a.Bg;
   const size_t rb = (size_t)cid * B;
@@ -259,7 +265,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
   // loaded into registers first so their latency overlaps the x / W_H staging
   const int r0 = rank * d.R < B ? rank * d.R : B;
   const int nr = r0 + d.R <= B ? d.R : B - r0;
-  const bool ce = a.loss_kind == VCNN_LOSS_SOFTMAX_CE;
+  const bool ce = loss_kind == VCNN_LOSS_SOFTMAX_CE;
   const int nw5 = out * h, ntg = ce ? nr : nr * out;
   const int nsmall = nw5 + h + out + ntg;
   auto small_src = [&](int i) -> float {
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     float acc = 0.f;
 #pragma unroll
     for (int c = 0; c < kC; ++c) acc += Ps[(c * d.R + b) * sH + o];
-    hs[b * lh + o] = actf(a.actH, acc + sbH[o]);
+    hs[b * lh + o] = AH >= 0 ? act_fwd(AH, acc + sbH[o]) : actf(actH, acc + sbH[o]);
   }
   __syncthreads();
   HPHASE(10);
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     if (ok && part == 0) {
-      const float v = actf(a.actO, acc + sbO[o]);
+      const float v = AO >= 0 ? act_fwd(AO, acc + sbO[o]) : actf(actO, acc + sbO[o]);
       g5[e] = v;
       y5[e] = v;
     }
@@ -391,7 +397,8 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
         const float yv = l[u];
         float gv = expf(yv - m) * inv;
         if (u == c) gv -= inv_b;
-        if (a.actO != VCNN_ACT_IDENTITY) gv *= actg(a.actO, yv);
+        if (actO != VCNN_ACT_IDENTITY)
+          gv *= AO >= 0 ? act_grad_from_out(AO, yv) : actg(actO, yv);
         l[u] = gv;
       }
     }
@@ -403,7 +410,8 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
       const float yv = g5[t], dd = yv - tg[t];
       mine += dd * dd;
       float gv = scale * dd;
-      if (a.actO != VCNN_ACT_IDENTITY) gv *= actg(a.actO, yv);
+      if (actO != VCNN_ACT_IDENTITY)
+        gv *= AO >= 0 ? act_grad_from_out(AO, yv) : actg(actO, yv);
       g5[t] = gv;
     }
 #pragma unroll
@@ -438,7 +446,8 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     if (b < nr && i < h) {
 #pragma unroll 4
       for (int o = 0; o < out; ++o) acc += g5[b * out + o] * W5[o * lh + i];
-      if (a.actH != VCNN_ACT_IDENTITY) acc *= actg(a.actH, hs[b * lh + i]);
+      if (actH != VCNN_ACT_IDENTITY)
+        acc *= AH >= 0 ? act_grad_from_out(AH, hs[b * lh + i]) : actg(actH, hs[b * lh + i]);
     }
     gl[b * sH + i] = acc;
   }
@@ -490,7 +499,7 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
     float v = 0.f;
 #pragma unroll 1
     for (int c = 0; c < kC; ++c) v += lossp[c];
-    const float norm = a.loss_kind == VCNN_LOSS_SOFTMAX_CE ? (float)Bg : (float)(Bg * out);
+    const float norm = loss_kind == VCNN_LOSS_SOFTMAX_CE ? (float)Bg : (float)(Bg * out);
     if (a.ncl == 1) {
       *a.loss = v / norm;
     } else {  // the last slice to finish sums the partials in slice order
@@ -571,12 +580,12 @@ __global__ void __launch_bounds__(kThreadsM) mlp_head_kernel(MlpArgs a) {
             const int col = n0 + j * 8 + 2 * t;
             if (j >= nv || col >= nc) continue;
             float v0 = c[j][2 * hf], v1 = c[j][2 * hf + 1];
-            if (a.act_prev == VCNN_ACT_RELU) {  // the common case inline
+            if (act_prev == VCNN_ACT_RELU) {  // the common case inline
               v0 *= xr[b * sK + col] > 0.f ? 1.f : 0.f;
               v1 *= xr[b * sK + col + 1] > 0.f ? 1.f : 0.f;
-            } else if (a.act_prev != VCNN_ACT_IDENTITY) {
-              v0 *= actg(a.act_prev, xr[b * sK + col]);
-              if (col + 1 < nc) v1 *= actg(a.act_prev, xr[b * sK + col + 1]);
+            } else if (act_prev != VCNN_ACT_IDENTITY) {
+              v0 *= actg(act_prev, xr[b * sK + col]);
+              if (col + 1 < nc) v1 *= actg(act_prev, xr[b * sK + col + 1]);
             }
             float* p = dx_ + (size_t)b * in + k0 + col;
             if (col + 1 < nc && (reinterpret_cast<uintptr_t>(p) & 7) == 0) {
@@ -611,21 +620,30 @@ size_t mlp_head_smem(int B, int in, int h, int out) {
 
 using HeadFn = void (*)(MlpArgs);
 // the specialised shape (CIFAR-3: B 128, 5*5*32 -> 64 -> 10) or the generic kernel
-static HeadFn head_fn(int B, int in, int h, int out) {
-  if (B == 128 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<128, 800, 64, 10>;
-  if (B == 64 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<64, 800, 64, 10>;
-  if (B == 32 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<32, 800, 64, 10>;
-  if (B == 16 && in == 800 && h == 64 && out == 10) return mlp_head_kernel<16, 800, 64, 10>;
+static HeadFn head_fn(int B, int in, int h, int out, int loss = -1, int actH = -1, int actO = -1,
+                      int act_prev = -1) {
+  const bool cifar = in == 800 && h == 64 && out == 10;
+  // CIFAR-3's tail: softmax-CE, relu dense conv, identity fc10, relu below
+  const bool prof = loss == VCNN_LOSS_SOFTMAX_CE && actH == VCNN_ACT_RELU &&
+                    actO == VCNN_ACT_IDENTITY && act_prev == VCNN_ACT_RELU;
+  constexpr int CE = VCNN_LOSS_SOFTMAX_CE, RL = VCNN_ACT_RELU, ID = VCNN_ACT_IDENTITY;
+  if (cifar && prof && B == 16) return mlp_head_kernel<16, 800, 64, 10, CE, RL, ID, RL>;
+  if (cifar && prof && B == 32) return mlp_head_kernel<32, 800, 64, 10, CE, RL, ID, RL>;
+  if (cifar && B == 128) return mlp_head_kernel<128, 800, 64, 10>;
+  if (cifar && B == 64) return mlp_head_kernel<64, 800, 64, 10>;
+  if (cifar && B == 32) return mlp_head_kernel<32, 800, 64, 10>;
+  if (cifar && B == 16) return mlp_head_kernel<16, 800, 64, 10>;
   return mlp_head_kernel<0, 0, 0, 0>;
 }
 
 // cluster of kC CTAs with this kernel's shared memory schedulable? (cached per kernel)
 static bool cluster_ok(HeadFn fn, size_t smem) {
   struct Cache { HeadFn fn; size_t ok_upto, bad_from; };
-  static Cache cache[6] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
+  static Cache cache[8] = {{nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
+                           {nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
                            {nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0},
                            {nullptr, 0, ~(size_t)0}, {nullptr, 0, ~(size_t)0}};
-  Cache* c = &cache[5];
+  Cache* c = &cache[7];
   for (Cache& e : cache)
     if (e.fn == fn || e.fn == nullptr) {
       c = &e;
@@ -692,7 +710,7 @@ int launch_mlp_head(int B, int in, int h, int out, const float* x, const float* 
     return fail(VCNN_ECONFIG, "mlp head: bad batch slicing");
   const int Bc = B / ncl;
   const size_t smem = mlp_head_smem(Bc, in, h, out);
-  const HeadFn fn = head_fn(Bc, in, h, out);
+  const HeadFn fn = head_fn(Bc, in, h, out, loss_kind, actH, actO, act_prev);
   if (!cluster_ok(fn, smem)) return fail(VCNN_ECUDA, "mlp head: cluster not schedulable");
   const bool vec = in % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) |
                                     reinterpret_cast<uintptr_t>(WH)) & 15) == 0;
