@@ -625,7 +625,8 @@ __device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map
 // MMA / epilogue code (the kernel's instruction footprint is fetched cold once
 // per CTA)
 template <int TMEM_COLS, int MODE, int ACT>
-__global__ void __launch_bounds__(NT, 1) direct_conv_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(NT, MODE == 1 ? 3 : 1)  // (dgrad: <= 85 registers, 3 CTAs/SM)
+    direct_conv_kernel(const __grid_constant__ Args a) {
   pdl_launch_dependents();
   const Geo& g = a.g;
   extern __shared__ uint8_t smem_raw[];
