@@ -161,6 +161,7 @@ struct vcnn_net {
   int g_dpv = 0;
   const void* g_ring = nullptr;
   int g_steps = 1;
+  int cap_steps = 1;  // steps in the graph being captured (1 when eager)
   int kernels_per_step = 0;
   bool guard = false;  // Trainer non-finite stop armed (err[2..3] on the device)
   DpLink* dp = nullptr;  // attached data-parallel group (vcnn_dp_*), or none
@@ -451,11 +452,21 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
   // per-op events live on the main stream)
   static const bool no_side = getenv("VCNN_NO_SIDE") != nullptr;  // A/B experiments
   const bool par = n->side && !n->breakdown && !no_side;
-  const cudaStream_t sw = par ? n->side : st;
-  const Workspace& wsw = par ? n->ws2 : n->ws;
+  const cudaStream_t sws = par ? n->side : st;
+  const Workspace& wss = par ? n->ws2 : n->ws;
+  static const bool l0_side = getenv("VCNN_L0_SIDE") != nullptr;  // A/B experiments
   for (int i = nl - 1 - (tail ? tail : 0); i >= 0; --i) {
     LayerRt& l = n->L[i];
-    if (par) {  // this layer's gradient inputs are ready on the main stream
+    // layer 0 has no data gradient: its weight gradient runs on the main
+    // stream right after layer 1's data gradient (and its own workspace),
+    // not queued behind the side stream's weight gradients above it.  Only
+    // in one-step graphs / eager steps: inside a multi-step graph the
+    // side-stream placement measured faster (83.4 vs 85.8 us per CIFAR-3
+    // b128 step; one-step graphs 84.9 vs 86.1, scripts/dbg_l0.py)
+    const bool l0m = par && i == 0 && !l0_side && n->cap_steps == 1;
+    const cudaStream_t sw = l0m ? st : sws;
+    const Workspace& wsw = l0m ? n->ws : wss;
+    if (par && !l0m) {  // this layer's gradient inputs are ready on the main stream
       VCNN_CUDA_TRY(cudaEventRecord(n->fork_ev[i], st));
       VCNN_CUDA_TRY(cudaStreamWaitEvent(n->side, n->fork_ev[i], 0));
     }
@@ -716,7 +727,9 @@ int train_steps_graph(vcnn_net* n, int k, int batch, float lr, float mom) {
     VCNN_CUDA_TRY(cudaStreamBeginCapture(n->cap_stream, cudaStreamCaptureModeRelaxed));
     n->stream = n->cap_stream;
     int s = VCNN_OK;
+    n->cap_steps = k;
     for (int i = 0; i < k && !s; ++i) s = eager_step(n, batch, lr, mom);
+    n->cap_steps = 1;
     n->stream = user;
     cudaError_t e = cudaStreamEndCapture(n->cap_stream, &g);
     if (s) {
