@@ -455,6 +455,7 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
   const cudaStream_t sws = par ? n->side : st;
   const Workspace& wss = par ? n->ws2 : n->ws;
   static const bool l0_side = getenv("VCNN_L0_SIDE") != nullptr;  // A/B experiments
+  bool forked = false;  // the side stream took work (and must be joined)
   for (int i = nl - 1 - (tail ? tail : 0); i >= 0; --i) {
     LayerRt& l = n->L[i];
     // layer 0 has no data gradient: its weight gradient runs on the main
@@ -467,6 +468,7 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
     const cudaStream_t sw = l0m ? st : sws;
     const Workspace& wsw = l0m ? n->ws : wss;
     if (par && !l0m) {  // this layer's gradient inputs are ready on the main stream
+      forked = true;
       VCNN_CUDA_TRY(cudaEventRecord(n->fork_ev[i], st));
       VCNN_CUDA_TRY(cudaStreamWaitEvent(n->side, n->fork_ev[i], 0));
     }
@@ -559,7 +561,7 @@ int run_backward(vcnn_net* n, int B, int tail = 0) {
       }
     }
   }
-  if (par) {  // join: the update (and any host read) sees every gradient
+  if (forked) {  // join: the update (and any host read) sees every gradient
     VCNN_CUDA_TRY(cudaEventRecord(n->join_ev, n->side));
     VCNN_CUDA_TRY(cudaStreamWaitEvent(st, n->join_ev, 0));
   }

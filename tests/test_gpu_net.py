@@ -270,6 +270,32 @@ def test_deterministic_and_graph_equivalent(prec):
     assert np.array_equal(runs[0], runs[2])
 
 
+@pytest.mark.parametrize("name", ["single-conv", "denoise16"])
+def test_graph_equivalent_single_and_multi_step(name):
+    """Graph capture of nets whose weight gradients are placed differently
+    across the streams (a one-layer net: nothing on the side stream; layer 0
+    on the main stream in one-step graphs, on the side stream inside
+    multi-step graphs) -- eager, one-step graphs and multi-step graphs
+    give the same bits."""
+    spec = S.PRESETS[name]() if name != "single-conv" else S.single_conv(8, 5, 16)
+    B = 8
+    x, _, vals = O.synth_bench_data(spec, B, 8)
+    runs = []
+    for mode in ("eager", "graph", "steps"):
+        net = Network(spec, B)
+        net.enable_graph(mode != "eager")
+        _load(net, spec, x, None, vals)
+        if mode == "steps":
+            net.train_steps(4, B, 0.01, 0.9)
+        else:
+            for _ in range(4):
+                net.train_step(B, 0.01, 0.9)
+        runs.append(net.get_params())
+        net.close()
+    assert np.array_equal(runs[0], runs[1])
+    assert np.array_equal(runs[0], runs[2])
+
+
 def test_host_path_equals_device_path():
     spec = S.cifar3()
     B = 32
